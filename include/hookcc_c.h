@@ -1,0 +1,259 @@
+/*
+ * hookcc_c.h — C-ABI of the B200-native Hook-Compress connected-components
+ * library (libhookcc_cuda.so).
+ *
+ * This is the drop-in boundary for the reference `hookcc` hot path
+ * (reference: /root/reference/proj/include/hookcc/{engines,forest,graph}.hpp).
+ * Plain pointers and sizes only; no C++ or torch types cross it. The C++
+ * header-compatible API in include/hookcc/*.hpp is a thin shim over these
+ * entry points, and Python binds them with ctypes
+ * (paper_1612_01178_b200/capi.py). Each entry point cites the reference
+ * interface it replaces.
+ *
+ * Conventions
+ *   - Every function returns an hcc_status; 0 is success. On failure a
+ *     thread-local message is available from hcc_last_error().
+ *   - Vertex ids on the device are uint32 (the reference uses uint64; SPEC
+ *     permits 32-bit packing when n < 2^32). n >= 2^32 is rejected with
+ *     HCC_EINVAL. Edge counts and offsets are uint64.
+ *   - Host buffers are caller-owned; device memory is owned by the handles.
+ *   - There is no CPU fallback: without a usable sm_100 device every
+ *     compute entry point fails with HCC_ENODEV.
+ */
+#ifndef HOOKCC_C_H_
+#define HOOKCC_C_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HCC_ABI_VERSION 1
+
+typedef enum hcc_status {
+  HCC_OK = 0,
+  HCC_EINVAL = 1,    /* bad argument; reference: std::invalid_argument    */
+  HCC_ENOMEM = 2,    /* device or host allocation failed                  */
+  HCC_ECUDA = 3,     /* CUDA runtime error                                */
+  HCC_ENCCL = 4,     /* NCCL error (multi-GPU merge)                      */
+  HCC_ENOTSTAR = 5,  /* forest not star-shaped; reference: std::logic_error
+                        from extract_labels (engines.hpp:66-70)            */
+  HCC_ENODEV = 6,    /* no usable sm_100 GPU                              */
+  HCC_ERANGE = 7     /* endpoint out of range; reference: check_endpoints
+                        (graph.hpp:89-94) std::invalid_argument           */
+} hcc_status;
+
+/* Algorithms; names follow the reference's Algorithm enum (bench.hpp:23-33). */
+typedef enum hcc_algo {
+  HCC_ALGO_BASELINE = 0,     /* Fig. 1: atomic-free hook over all edges +
+                                jump-until-fixpoint (engines.hpp:123-179)  */
+  HCC_ALGO_BASELINE_MJ = 1,  /* atomic-free hook + Multi-Jump compress,
+                                repeated to convergence (engines.hpp:183-231).
+                                On B200 this is the north-star engine: a
+                                topology-driven first pass, then data-driven
+                                passes over a device-compacted worklist.   */
+  HCC_ALGO_ATOMIC = 2,       /* single CAS-hook pass + Multi-Jump
+                                (single_hook_cc, engines.hpp:295-300)      */
+  HCC_ALGO_ADAPTIVE = 3      /* segmented CAS hook + Multi-Jump per segment
+                                (adaptive_cc, engines.hpp:238-291)         */
+} hcc_algo;
+
+/* Option flags (hcc_opts.flags). */
+#define HCC_FLAG_FULL_PASSES   0x1u /* baseline-mj: re-hook ALL edges every
+                                       outer iteration (the reference's
+                                       literal loop) instead of the worklist */
+#define HCC_FLAG_HOST_LOOP     0x2u /* drive iterations from the host (one
+                                       4-byte D2H per iteration) instead of
+                                       the device-side CUDA-graph loop      */
+#define HCC_FLAG_NO_GRAPH      0x4u /* launch kernels directly, no CUDA graph*/
+#define HCC_FLAG_CHECK_STAR    0x8u /* verify the final forest is a star
+                                       (extract_labels' debug check)        */
+
+/* Phase identifiers passed to the observer; reference Phase enum
+ * (engines.hpp:84). */
+#define HCC_PHASE_HOOK 0
+#define HCC_PHASE_COMPRESS 1
+
+typedef struct hcc_ctx hcc_ctx;
+typedef struct hcc_graph hcc_graph;
+typedef struct hcc_forest hcc_forest;
+
+/* Observer called with the quiesced device forest after every phase
+ * barrier (reference DriverOptions::phase_observer, engines.hpp:86-90).
+ * Setting it forces the host-stepped loop (one sync per phase). */
+typedef void (*hcc_phase_cb)(void* user, int phase, hcc_forest* pi);
+
+typedef struct hcc_opts {
+  int algo;                      /* hcc_algo                                */
+  uint64_t segments;             /* adaptive: s (0 = auto, choose_segment_count
+                                    of the device stats)                    */
+  uint64_t first_pass_segments;  /* baseline-mj: segments of the topology
+                                    pass, each followed by a compress
+                                    (0 = auto)                              */
+  uint64_t max_threads;          /* 0 = whole GPU; k > 0 caps the launch at
+                                    k threads (1 = one thread, ascending and
+                                    deterministic: the reference's
+                                    workers = 1 inline path, parallel.hpp:29) */
+  uint32_t flags;                /* HCC_FLAG_*                              */
+  hcc_phase_cb observer;         /* optional                                */
+  void* observer_user;
+} hcc_opts;
+
+/* Reference KernelCounters (forest.hpp:65-75). */
+typedef struct hcc_counters {
+  uint64_t hook_traversal_steps;
+  uint64_t cas_failures;
+  uint64_t jump_steps;
+} hcc_counters;
+
+/* Reference RunMetrics (metrics.hpp:18-41), the fields a driver fills,
+ * plus B200 additions appended at the end. Times are device times. */
+typedef struct hcc_metrics {
+  double total_ms;          /* pi init through convergence                 */
+  double hook_ms;
+  double compress_ms;
+  uint64_t s;               /* segments actually used                      */
+  int segments_clamped;
+  uint64_t outer_iterations;
+  hcc_counters counters;
+  uint64_t components;
+  /* B200 additions */
+  uint64_t n, m;
+  uint64_t passes;          /* hook passes (segments + worklist passes)    */
+  uint64_t edges_processed; /* edge records streamed by hook kernels       */
+  uint64_t records;         /* per-phase records available (hcc_ctx_segments)*/
+  int used_device_loop;     /* 1 = CUDA-graph conditional loop             */
+} hcc_metrics;
+
+/* One record per segment / outer iteration / worklist pass
+ * (RunMetrics::segment_ms + segment_counters, metrics.hpp:30-31). */
+typedef struct hcc_segment_rec {
+  double hook_ms;
+  double compress_ms;
+  hcc_counters counters;
+  uint64_t edges_in;        /* records the hook phase streamed             */
+  uint64_t edges_out;       /* records appended to the next worklist       */
+  double hook_event_ms;     /* hook kernel time from CUDA events recorded
+                               around the launch on the launch stream (the
+                               unrolled topology segments); -1 if not taken */
+} hcc_segment_rec;
+
+/* Reference GraphStats (graph.hpp:33-40), computed on the device. */
+typedef struct hcc_graph_stats {
+  uint64_t n;
+  uint64_t m_stored;
+  uint64_t m_unique;
+  double avg_degree;
+  uint64_t max_degree;
+} hcc_graph_stats;
+
+/* ---- library / context -------------------------------------------------*/
+int hcc_abi_version(void);
+const char* hcc_last_error(void);
+/* Number of usable devices (0 when no sm_100 GPU is visible). */
+int hcc_device_count(void);
+/* One context per host thread: device, stream, scratch, control block.
+ * Replaces the per-call ThreadPool (engines.hpp:125-126, parallel.hpp:28). */
+int hcc_create(int device, hcc_ctx** out);
+int hcc_destroy(hcc_ctx* ctx);
+int hcc_ctx_segments(hcc_ctx* ctx, hcc_segment_rec* out, uint64_t cap,
+                     uint64_t* count);
+int hcc_ctx_sm_count(hcc_ctx* ctx, int* out);
+
+/* ---- graphs (reference Graph{n, vector<Edge>}, graph.hpp:13-31) --------*/
+/* uv = interleaved u0,v0,u1,v1,... (the memory layout of vector<Edge>);
+ * narrowed to u32 and endpoint-checked on the device (check_endpoints). */
+int hcc_graph_from_edges_u64(hcc_ctx* ctx, const uint64_t* uv, uint64_t m,
+                             uint64_t n, hcc_graph** out);
+int hcc_graph_from_edges_u32(hcc_ctx* ctx, const uint32_t* uv, uint64_t m,
+                             uint64_t n, hcc_graph** out);
+/* CSR: row_ptr[n+1], col[row_ptr[n]]; every stored entry (u, col[j]) is one
+ * edge record, in row order. (North-star addition; the reference's only CSR
+ * is internal to bfs_cc, oracle.hpp:68-83.) */
+int hcc_graph_from_csr(hcc_ctx* ctx, const uint64_t* row_ptr,
+                       const uint32_t* col, uint64_t n, hcc_graph** out);
+/* Device generators. spec: "grid:RxC" (identical to generators.hpp:71-87),
+ * "rmatx:scale=K,ef=F[,seed=S][,a=..,b=..,c=..,d=..]" and
+ * "erx:n=N,m=M[,seed=S]" (counter-based twins of generators.hpp:14-62,
+ * restated bit-exactly on the CPU in oracle/). */
+int hcc_graph_generate(hcc_ctx* ctx, const char* spec, uint64_t default_seed,
+                       hcc_graph** out);
+int hcc_graph_info(const hcc_graph* g, uint64_t* n, uint64_t* m);
+/* Copy the packed device edges (u32 pairs) to the host. */
+int hcc_graph_download_u32(hcc_ctx* ctx, const hcc_graph* g, uint32_t* uv,
+                           uint64_t first, uint64_t count);
+/* FNV-style order-dependent checksum of the edge stream (size-independent
+ * generator parity). */
+int hcc_graph_checksum(hcc_ctx* ctx, const hcc_graph* g, uint64_t* out);
+/* Device compute_stats (graph.hpp:43-68): radix sort + unique. */
+int hcc_graph_compute_stats(hcc_ctx* ctx, const hcc_graph* g,
+                            hcc_graph_stats* out);
+int hcc_graph_free(hcc_graph* g);
+
+/* ---- the CC entry point -------------------------------------------------
+ * Replaces baseline_cc / baseline_mj_cc / single_hook_cc / adaptive_cc and
+ * their *_into variants (engines.hpp:123-338). `pi` may be NULL (the
+ * context's scratch forest is used) or a caller forest of size n (the
+ * in-place *_into contract: reset inside, final forest left in it).
+ * labels_out (host, n entries, may be NULL) receives the canonical labels:
+ * label(v) = minimum vertex id of v's component. */
+int hcc_cc(hcc_ctx* ctx, const hcc_graph* g, const hcc_opts* opts,
+           hcc_forest* pi, uint32_t* labels_out, hcc_metrics* out);
+/* Same, labels widened to u64 (ComponentLabeling::label, engines.hpp:19-24). */
+int hcc_cc_u64(hcc_ctx* ctx, const hcc_graph* g, const hcc_opts* opts,
+               hcc_forest* pi, uint64_t* labels_out, hcc_metrics* out);
+/* Reference choose_segment_count (engines.hpp:35-41). */
+uint64_t hcc_choose_segment_count(const hcc_graph_stats* stats);
+
+/* ---- parent forest (reference ParentForest, forest.hpp:19-63) -----------
+ * A device-resident u32 pi. Element operations run as device kernels on
+ * the calling thread's per-thread stream, so concurrent host threads really
+ * race on the device (test_forest.cpp:185-211). */
+int hcc_forest_create(hcc_ctx* ctx, uint64_t n, hcc_forest** out);
+int hcc_forest_free(hcc_forest* f);
+int hcc_forest_size(const hcc_forest* f, uint64_t* n);
+int hcc_forest_reset(hcc_forest* f);                        /* forest.hpp:25 */
+int hcc_forest_download_u64(hcc_forest* f, uint64_t* out); /* snapshot 45-49*/
+int hcc_forest_download_u32(hcc_forest* f, uint32_t* out);
+int hcc_forest_upload_u64(hcc_forest* f, const uint64_t* in);
+int hcc_forest_load(hcc_forest* f, uint64_t v, uint64_t* out);   /* 30-32 */
+int hcc_forest_store(hcc_forest* f, uint64_t v, uint64_t p);     /* 34-36 */
+/* CAS; on failure *expected receives the observed value (39-43). */
+int hcc_forest_cas(hcc_forest* f, uint64_t v, uint64_t* expected,
+                   uint64_t desired, int* ok);
+/* Per-element kernels of Figs. 2-3 (forest.hpp:83-136). */
+int hcc_forest_hook(hcc_forest* f, uint64_t u, uint64_t v, int* changed);
+int hcc_forest_jump(hcc_forest* f, uint64_t v, int* changed);
+int hcc_forest_atomic_hook(hcc_forest* f, uint64_t u, uint64_t v,
+                           hcc_counters* c);
+int hcc_forest_multi_jump(hcc_forest* f, uint64_t v, hcc_counters* c);
+/* One multi_jump per vertex over [begin,end), ascending (descending != 0:
+ * descending) by one device thread: the schedule-order pass of
+ * test_forest.cpp:150-169. */
+int hcc_forest_multi_jump_range(hcc_forest* f, uint64_t begin, uint64_t end,
+                                int descending, hcc_counters* c);
+int hcc_forest_is_star(hcc_forest* f, int* out);           /* 140-146 */
+/* max over v of (pi(v) > v): the bound invariant (SPEC: pi(v) <= v). */
+int hcc_forest_check_bound(hcc_forest* f, int* ok);
+
+/* ---- multi-GPU edge-partitioned CC (north-star (5)) ----------
+ * One process per GPU. Rank r runs the local CC on its shard of the edge
+ * list (partition_edges(m, world) semantics, engines.hpp:43-58), then the
+ * forests are merged over NVLink with NCCL and re-hooked as
+ * (v, pi_remote(v)) pairs until global convergence. */
+int hcc_nccl_unique_id_size(void);
+int hcc_nccl_get_unique_id(void* id_out);
+int hcc_comm_init(hcc_ctx* ctx, int world, int rank, const void* id);
+int hcc_comm_destroy(hcc_ctx* ctx);
+/* Shard [first, first+count) of a host edge array, uploaded as a graph. */
+int hcc_cc_distributed(hcc_ctx* ctx, const hcc_graph* shard, uint64_t n,
+                       const hcc_opts* opts, uint32_t* labels_out,
+                       hcc_metrics* out);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif  /* HOOKCC_C_H_ */

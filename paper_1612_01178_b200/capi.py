@@ -1,0 +1,361 @@
+"""ctypes binding of the libhookcc_cuda.so C-ABI (include/hookcc_c.h).
+
+This is plumbing: every call goes straight to the CUDA library.  There is no
+CPU fallback anywhere in this package; loading fails loudly when the shared
+library is missing and compute calls fail with HCC_ENODEV without a B200.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "lib" / "libhookcc_cuda.so"
+
+HCC_OK, HCC_EINVAL, HCC_ENOMEM, HCC_ECUDA, HCC_ENCCL, HCC_ENOTSTAR, HCC_ENODEV, HCC_ERANGE = range(8)
+ALGO_BASELINE, ALGO_BASELINE_MJ, ALGO_ATOMIC, ALGO_ADAPTIVE = range(4)
+ALGOS = {"baseline": ALGO_BASELINE, "baseline-mj": ALGO_BASELINE_MJ,
+         "atomic": ALGO_ATOMIC, "adaptive": ALGO_ADAPTIVE}
+FLAG_FULL_PASSES, FLAG_HOST_LOOP, FLAG_NO_GRAPH, FLAG_CHECK_STAR = 0x1, 0x2, 0x4, 0x8
+PHASE_HOOK, PHASE_COMPRESS = 0, 1
+
+u64, u32, i32 = C.c_uint64, C.c_uint32, C.c_int
+vp = C.c_void_p
+
+PHASE_CB = C.CFUNCTYPE(None, vp, i32, vp)
+
+
+class Opts(C.Structure):
+    _fields_ = [("algo", i32), ("segments", u64), ("first_pass_segments", u64),
+                ("max_threads", u64), ("flags", u32), ("observer", PHASE_CB),
+                ("observer_user", vp)]
+
+
+class Counters(C.Structure):
+    _fields_ = [("hook_traversal_steps", u64), ("cas_failures", u64), ("jump_steps", u64)]
+
+
+class Metrics(C.Structure):
+    _fields_ = [("total_ms", C.c_double), ("hook_ms", C.c_double), ("compress_ms", C.c_double),
+                ("s", u64), ("segments_clamped", i32), ("outer_iterations", u64),
+                ("counters", Counters), ("components", u64), ("n", u64), ("m", u64),
+                ("passes", u64), ("edges_processed", u64), ("records", u64),
+                ("used_device_loop", i32)]
+
+
+class SegmentRec(C.Structure):
+    _fields_ = [("hook_ms", C.c_double), ("compress_ms", C.c_double), ("counters", Counters),
+                ("edges_in", u64), ("edges_out", u64), ("hook_event_ms", C.c_double)]
+
+
+class GraphStats(C.Structure):
+    _fields_ = [("n", u64), ("m_stored", u64), ("m_unique", u64), ("avg_degree", C.c_double),
+                ("max_degree", u64)]
+
+
+class HccError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"hcc error {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "hcc_abi_version": (i32, []),
+    "hcc_last_error": (C.c_char_p, []),
+    "hcc_device_count": (i32, []),
+    "hcc_create": (i32, [i32, C.POINTER(vp)]),
+    "hcc_destroy": (i32, [vp]),
+    "hcc_ctx_segments": (i32, [vp, vp, u64, C.POINTER(u64)]),
+    "hcc_ctx_sm_count": (i32, [vp, C.POINTER(i32)]),
+    "hcc_graph_from_edges_u64": (i32, [vp, vp, u64, u64, C.POINTER(vp)]),
+    "hcc_graph_from_edges_u32": (i32, [vp, vp, u64, u64, C.POINTER(vp)]),
+    "hcc_graph_from_csr": (i32, [vp, vp, vp, u64, C.POINTER(vp)]),
+    "hcc_graph_generate": (i32, [vp, C.c_char_p, u64, C.POINTER(vp)]),
+    "hcc_graph_info": (i32, [vp, C.POINTER(u64), C.POINTER(u64)]),
+    "hcc_graph_download_u32": (i32, [vp, vp, vp, u64, u64]),
+    "hcc_graph_checksum": (i32, [vp, vp, C.POINTER(u64)]),
+    "hcc_graph_compute_stats": (i32, [vp, vp, C.POINTER(GraphStats)]),
+    "hcc_graph_free": (i32, [vp]),
+    "hcc_cc": (i32, [vp, vp, C.POINTER(Opts), vp, vp, C.POINTER(Metrics)]),
+    "hcc_cc_u64": (i32, [vp, vp, C.POINTER(Opts), vp, vp, C.POINTER(Metrics)]),
+    "hcc_choose_segment_count": (u64, [C.POINTER(GraphStats)]),
+    "hcc_forest_create": (i32, [vp, u64, C.POINTER(vp)]),
+    "hcc_forest_free": (i32, [vp]),
+    "hcc_forest_size": (i32, [vp, C.POINTER(u64)]),
+    "hcc_forest_reset": (i32, [vp]),
+    "hcc_forest_download_u64": (i32, [vp, vp]),
+    "hcc_forest_download_u32": (i32, [vp, vp]),
+    "hcc_forest_upload_u64": (i32, [vp, vp]),
+    "hcc_forest_load": (i32, [vp, u64, C.POINTER(u64)]),
+    "hcc_forest_store": (i32, [vp, u64, u64]),
+    "hcc_forest_cas": (i32, [vp, u64, C.POINTER(u64), u64, C.POINTER(i32)]),
+    "hcc_forest_hook": (i32, [vp, u64, u64, C.POINTER(i32)]),
+    "hcc_forest_jump": (i32, [vp, u64, C.POINTER(i32)]),
+    "hcc_forest_atomic_hook": (i32, [vp, u64, u64, C.POINTER(Counters)]),
+    "hcc_forest_multi_jump": (i32, [vp, u64, C.POINTER(Counters)]),
+    "hcc_forest_multi_jump_range": (i32, [vp, u64, u64, i32, C.POINTER(Counters)]),
+    "hcc_forest_is_star": (i32, [vp, C.POINTER(i32)]),
+    "hcc_forest_check_bound": (i32, [vp, C.POINTER(i32)]),
+    "hcc_nccl_unique_id_size": (i32, []),
+    "hcc_nccl_get_unique_id": (i32, [vp]),
+    "hcc_comm_init": (i32, [vp, i32, i32, vp]),
+    "hcc_comm_destroy": (i32, [vp]),
+    "hcc_cc_distributed": (i32, [vp, vp, u64, C.POINTER(Opts), vp, C.POINTER(Metrics)]),
+}
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGS)
+
+
+def lib() -> C.CDLL:
+    """Load libhookcc_cuda.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        path = Path(os.environ.get("HCC_LIB", LIB_PATH))
+        if not path.exists():
+            raise ImportError(f"{path} not built; run `python -m paper_1612_01178_b200.build`")
+        L = C.CDLL(str(path))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(code: int) -> None:
+    if code != HCC_OK:
+        raise HccError(code, lib().hcc_last_error().decode())
+
+
+def device_count() -> int:
+    return lib().hcc_device_count()
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+class Context:
+    """hcc_ctx: one device, stream and scratch (per host thread)."""
+
+    def __init__(self, device: int = 0):
+        h = vp()
+        check(lib().hcc_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self) -> None:
+        if self.h:
+            lib().hcc_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def sm_count(self) -> int:
+        out = i32()
+        check(lib().hcc_ctx_sm_count(self.h, C.byref(out)))
+        return out.value
+
+    def segments(self) -> list[dict]:
+        cnt = u64()
+        check(lib().hcc_ctx_segments(self.h, None, 0, C.byref(cnt)))
+        arr = (SegmentRec * max(cnt.value, 1))()
+        check(lib().hcc_ctx_segments(self.h, C.cast(arr, vp), cnt.value, C.byref(cnt)))
+        out = []
+        for i in range(cnt.value):
+            r = arr[i]
+            out.append(dict(hook_ms=r.hook_ms, compress_ms=r.compress_ms,
+                            hook_traversal_steps=r.counters.hook_traversal_steps,
+                            cas_failures=r.counters.cas_failures,
+                            jump_steps=r.counters.jump_steps,
+                            edges_in=r.edges_in, edges_out=r.edges_out,
+                            hook_event_ms=r.hook_event_ms))
+        return out
+
+    # -- graphs --
+    def graph_from_edges(self, edges: np.ndarray, n: int) -> "Graph":
+        """edges: (m, 2) array of uint32 or uint64 endpoint pairs."""
+        e = np.ascontiguousarray(edges)
+        if e.ndim != 2 or (e.size and e.shape[1] != 2):
+            raise ValueError("edges must have shape (m, 2)")
+        m = e.shape[0]
+        h = vp()
+        if e.dtype == np.uint32:
+            check(lib().hcc_graph_from_edges_u32(self.h, _ptr(e) if m else None, m, n, C.byref(h)))
+        else:
+            e = np.ascontiguousarray(e, dtype=np.uint64)
+            check(lib().hcc_graph_from_edges_u64(self.h, _ptr(e) if m else None, m, n, C.byref(h)))
+        return Graph(self, h)
+
+    def graph_from_csr(self, row_ptr: np.ndarray, col: np.ndarray) -> "Graph":
+        rp = np.ascontiguousarray(row_ptr, dtype=np.uint64)
+        cl = np.ascontiguousarray(col, dtype=np.uint32)
+        h = vp()
+        check(lib().hcc_graph_from_csr(self.h, _ptr(rp), _ptr(cl) if cl.size else None,
+                                       len(rp) - 1, C.byref(h)))
+        return Graph(self, h)
+
+    def generate(self, spec: str, default_seed: int = 1) -> "Graph":
+        h = vp()
+        check(lib().hcc_graph_generate(self.h, spec.encode(), default_seed, C.byref(h)))
+        return Graph(self, h)
+
+    def forest(self, n: int) -> "Forest":
+        h = vp()
+        check(lib().hcc_forest_create(self.h, n, C.byref(h)))
+        return Forest(self, h, n)
+
+    # -- the CC entry point --
+    def cc(self, graph: "Graph", algo: str | int = "baseline-mj", segments: int = 0,
+           first_pass_segments: int = 0, max_threads: int = 0, flags: int = 0,
+           forest: "Forest | None" = None, labels: bool = True, observer=None,
+           labels_out: np.ndarray | None = None):
+        """Run connected components; returns (labels u32 | None, metrics dict)."""
+        a = ALGOS[algo] if isinstance(algo, str) else int(algo)
+        cb = PHASE_CB(0)
+        if observer is not None:
+            def _cb(user, phase, fh, _obs=observer, _n=graph.n):
+                _obs(phase, Forest(self, vp(fh), _n, owned=False))
+            cb = PHASE_CB(_cb)
+        o = Opts(a, segments, first_pass_segments, max_threads, flags, cb, None)
+        mx = Metrics()
+        out = None
+        if labels:
+            out = labels_out if labels_out is not None else np.empty(graph.n, dtype=np.uint32)
+        check(lib().hcc_cc(self.h, graph.h, C.byref(o), forest.h if forest else None,
+                           _ptr(out) if (out is not None and graph.n) else None, C.byref(mx)))
+        return out, metrics_dict(mx)
+
+
+def metrics_dict(mx: Metrics) -> dict:
+    return dict(total_ms=mx.total_ms, hook_ms=mx.hook_ms, compress_ms=mx.compress_ms,
+                s=mx.s, segments_clamped=bool(mx.segments_clamped),
+                outer_iterations=mx.outer_iterations,
+                hook_traversal_steps=mx.counters.hook_traversal_steps,
+                cas_failures=mx.counters.cas_failures, jump_steps=mx.counters.jump_steps,
+                components=mx.components, n=mx.n, m=mx.m, passes=mx.passes,
+                edges_processed=mx.edges_processed, records=mx.records,
+                used_device_loop=bool(mx.used_device_loop))
+
+
+class Graph:
+    def __init__(self, ctx: Context, h):
+        self.ctx, self.h = ctx, h
+        n, m = u64(), u64()
+        check(lib().hcc_graph_info(h, C.byref(n), C.byref(m)))
+        self.n, self.m = n.value, m.value
+
+    def close(self):
+        if self.h:
+            lib().hcc_graph_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def edges(self, first: int = 0, count: int | None = None) -> np.ndarray:
+        count = self.m - first if count is None else count
+        out = np.empty((count, 2), dtype=np.uint32)
+        check(lib().hcc_graph_download_u32(self.ctx.h, self.h, _ptr(out) if count else None,
+                                           first, count))
+        return out
+
+    def checksum(self) -> int:
+        out = u64()
+        check(lib().hcc_graph_checksum(self.ctx.h, self.h, C.byref(out)))
+        return out.value
+
+    def stats(self) -> dict:
+        st = GraphStats()
+        check(lib().hcc_graph_compute_stats(self.ctx.h, self.h, C.byref(st)))
+        return dict(n=st.n, m_stored=st.m_stored, m_unique=st.m_unique,
+                    avg_degree=st.avg_degree, max_degree=st.max_degree)
+
+
+class Forest:
+    """Device ParentForest (forest.hpp:19-63)."""
+
+    def __init__(self, ctx: Context, h, n: int, owned: bool = True):
+        self.ctx, self.h, self.n, self.owned = ctx, h, n, owned
+
+    def close(self):
+        if self.h and self.owned:
+            lib().hcc_forest_free(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def reset(self):
+        check(lib().hcc_forest_reset(self.h))
+
+    def snapshot(self) -> np.ndarray:
+        out = np.empty(self.n, dtype=np.uint64)
+        check(lib().hcc_forest_download_u64(self.h, _ptr(out) if self.n else None))
+        return out
+
+    def upload(self, parents) -> None:
+        a = np.ascontiguousarray(parents, dtype=np.uint64)
+        check(lib().hcc_forest_upload_u64(self.h, _ptr(a) if self.n else None))
+
+    def load(self, v: int) -> int:
+        out = u64()
+        check(lib().hcc_forest_load(self.h, v, C.byref(out)))
+        return out.value
+
+    def store(self, v: int, p: int) -> None:
+        check(lib().hcc_forest_store(self.h, v, p))
+
+    def cas(self, v: int, expected: int, desired: int):
+        e = u64(expected)
+        ok = i32()
+        check(lib().hcc_forest_cas(self.h, v, C.byref(e), desired, C.byref(ok)))
+        return bool(ok.value), e.value
+
+    def hook(self, u: int, v: int) -> bool:
+        ch = i32()
+        check(lib().hcc_forest_hook(self.h, u, v, C.byref(ch)))
+        return bool(ch.value)
+
+    def jump(self, v: int) -> bool:
+        ch = i32()
+        check(lib().hcc_forest_jump(self.h, v, C.byref(ch)))
+        return bool(ch.value)
+
+    def atomic_hook(self, u: int, v: int, counters: Counters) -> None:
+        check(lib().hcc_forest_atomic_hook(self.h, u, v, C.byref(counters)))
+
+    def multi_jump(self, v: int, counters: Counters) -> None:
+        check(lib().hcc_forest_multi_jump(self.h, v, C.byref(counters)))
+
+    def multi_jump_range(self, begin: int, end: int, descending: bool, counters: Counters) -> None:
+        check(lib().hcc_forest_multi_jump_range(self.h, begin, end, int(descending), C.byref(counters)))
+
+    def is_star(self) -> bool:
+        out = i32()
+        check(lib().hcc_forest_is_star(self.h, C.byref(out)))
+        return bool(out.value)
+
+    def bound_ok(self) -> bool:
+        out = i32()
+        check(lib().hcc_forest_check_bound(self.h, C.byref(out)))
+        return bool(out.value)

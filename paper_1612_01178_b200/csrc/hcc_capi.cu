@@ -1,0 +1,1464 @@
+// C-ABI implementation of libhookcc_cuda.so: contexts, graph handles,
+// device forests and the CC engines.
+//
+// Engines (reference drivers, /root/reference/proj/include/hookcc/engines.hpp):
+//   BASELINE     (123-179)  loop { hook all edges ; loop { jump } } until no
+//                           hook changed
+//   BASELINE_MJ  (183-231)  north-star engine: segmented topology-driven
+//                           hook pass, then data-driven passes over the
+//                           device-compacted worklist of (H, L) pairs, each
+//                           followed by Multi-Jump; converged when a pass
+//                           appends nothing.  HCC_FLAG_FULL_PASSES gives the
+//                           reference's literal "re-hook every edge" loop.
+//   ATOMIC/ADAPTIVE (238-300) per segment: CAS hook + Multi-Jump.
+//
+// Every loop runs on the device: the body is captured into the body graph
+// of a CUDA-graph conditional WHILE node and the last kernel of the body
+// sets the condition, so an hcc_cc call is one cudaGraphLaunch with no
+// host round trip per iteration (HCC_FLAG_HOST_LOOP / observer mode drive
+// the same kernels from the host instead).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "hcc_gen.h"
+#include "hcc_internal.cuh"
+#include "hookcc_c.h"
+
+using namespace hcc;
+
+// ---------------------------------------------------------------------------
+// errors
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+struct CudaFail {
+  int code;
+};
+
+#define HCC_CUDA(call)                                                       \
+  do {                                                                       \
+    cudaError_t e_ = (call);                                                 \
+    if (e_ != cudaSuccess) {                                                 \
+      g_err = std::string(#call) + ": " + cudaGetErrorString(e_);            \
+      throw CudaFail{e_ == cudaErrorMemoryAllocation ? HCC_ENOMEM           \
+                                                      : HCC_ECUDA};         \
+    }                                                                        \
+  } while (0)
+
+#define HCC_GUARD_BEGIN try {
+#define HCC_GUARD_END                                                        \
+  }                                                                          \
+  catch (const CudaFail& f) {                                                \
+    return f.code;                                                           \
+  }                                                                          \
+  catch (const std::bad_alloc&) {                                            \
+    return fail(HCC_ENOMEM, "host allocation failed");                       \
+  }                                                                          \
+  catch (const std::exception& ex) {                                         \
+    return fail(HCC_ECUDA, ex.what());                                       \
+  }
+
+// Device-side narrowing works on 32-bit ids.
+constexpr u64 kMaxN = 0xffffffffull;
+// Topology segments unrolled into the root graph (with per-launch events).
+constexpr u64 kMaxUnrolledSegments = 64;
+
+int usable_devices() {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int usable = 0;
+  for (int d = 0; d < count; ++d) {
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10)
+      ++usable;
+  }
+  return usable;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// handles
+
+struct GraphKey {
+  int algo = -1;
+  const void* edges = nullptr;
+  const void* pi = nullptr;
+  const void* wl0 = nullptr;
+  u64 n = 0, m = 0, nseg = 0, max_threads = 0;
+  u32 flags = 0;
+  bool operator==(const GraphKey& o) const {
+    return algo == o.algo && edges == o.edges && pi == o.pi && wl0 == o.wl0 &&
+           n == o.n && m == o.m && nseg == o.nseg &&
+           max_threads == o.max_threads && flags == o.flags;
+  }
+};
+
+struct hcc_ctx {
+  int dev = 0;
+  int sms = 148;
+  cudaStream_t stream = nullptr;
+  DevCtrl* d_ctrl = nullptr;
+  DevRec* d_recs = nullptr;
+  DevCtrl* h_ctrl = nullptr;  // pinned
+  DevRec* h_recs = nullptr;   // pinned
+  u32* scratch_pi = nullptr;
+  u64 scratch_n = 0;
+  uint2* wl[2] = {nullptr, nullptr};
+  u64 wl_cap = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int occ_hook = 1, occ_vert = 1;
+  // cached executable graph for repeated calls with identical arguments
+  cudaGraphExec_t exec = nullptr;
+  GraphKey key;
+  std::vector<hcc_segment_rec> last_recs;
+  // CUDA events around the unrolled topology hook launches
+  std::vector<cudaEvent_t> seg_ev;   // 2 per segment
+  u64 seg_ev_used = 0;
+  u64 exec_seg_ev = 0;  // seg_ev_used of the cached executable graph
+  // multi-GPU
+  void* comm = nullptr;
+  int world = 1, rank = 0;
+};
+
+struct hcc_graph {
+  hcc_ctx* ctx = nullptr;
+  u64 n = 0, m = 0;
+  uint2* d_edges = nullptr;
+  bool has_stats = false;
+  hcc_graph_stats stats{};
+};
+
+struct hcc_forest {
+  hcc_ctx* ctx = nullptr;
+  int dev = 0;
+  u64 n = 0;
+  u32* d_pi = nullptr;
+};
+
+namespace {
+
+// Per-host-thread scratch for element operations (ParentForest API):
+// results travel through a pinned buffer on the thread's default stream.
+struct ThreadScratch {
+  int dev = -1;
+  u64* d_res = nullptr;
+  u64* h_res = nullptr;
+  ~ThreadScratch() {
+    // process teardown: leaking is harmless and avoids calls into a
+    // possibly-destroyed runtime
+  }
+};
+thread_local ThreadScratch t_scratch;
+
+u64* thread_scratch(int dev, u64** host) {
+  if (t_scratch.dev != dev) {
+    HCC_CUDA(cudaSetDevice(dev));
+    u64* d = nullptr;
+    u64* h = nullptr;
+    HCC_CUDA(cudaMalloc(&d, 8 * sizeof(u64)));
+    HCC_CUDA(cudaMallocHost(&h, 8 * sizeof(u64)));
+    t_scratch.dev = dev;
+    t_scratch.d_res = d;
+    t_scratch.h_res = h;
+  }
+  *host = t_scratch.h_res;
+  return t_scratch.d_res;
+}
+
+void ensure_pi(hcc_ctx* c, u64 n) {
+  if (c->scratch_n >= n && c->scratch_pi) return;
+  if (c->scratch_pi) HCC_CUDA(cudaFree(c->scratch_pi));
+  c->scratch_pi = nullptr;
+  c->scratch_n = 0;
+  HCC_CUDA(cudaMalloc(&c->scratch_pi, std::max<u64>(n, 4) * sizeof(u32)));
+  c->scratch_n = n;
+}
+
+void ensure_wl(hcc_ctx* c, u64 cap) {
+  cap = std::max<u64>(cap, 1024);
+  if (c->wl_cap >= cap) return;
+  for (int i = 0; i < 2; ++i) {
+    if (c->wl[i]) HCC_CUDA(cudaFree(c->wl[i]));
+    c->wl[i] = nullptr;
+  }
+  c->wl_cap = 0;
+  for (int i = 0; i < 2; ++i) HCC_CUDA(cudaMalloc(&c->wl[i], cap * sizeof(uint2)));
+  c->wl_cap = cap;
+}
+
+void drop_exec(hcc_ctx* c) {
+  if (c->exec) cudaGraphExecDestroy(c->exec);
+  c->exec = nullptr;
+  c->key = GraphKey{};
+}
+
+unsigned grid_for(u64 work, unsigned block, u64 cap) {
+  u64 g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  if (g > 0x7fffffffull) g = 0x7fffffffull;
+  return (unsigned)g;
+}
+
+// ---- sequence builder: CUDA-graph capture or host-driven loop -------------
+
+struct Seq {
+  hcc_ctx* c;
+  bool graph_mode;
+  std::vector<cudaStream_t> streams;  // streams[d] captures nesting depth d
+  int depth = 0;
+  std::function<void(int)> on_phase;  // observer hook (host mode only)
+
+  cudaStream_t s() const { return streams[depth]; }
+
+  void phase_done(int phase) {
+    if (!graph_mode && on_phase) on_phase(phase);
+  }
+
+  // Event record usable both eagerly and inside a stream capture (an
+  // external event-record node of the root graph).
+  void record(cudaEvent_t ev) {
+    if (graph_mode)
+      HCC_CUDA(cudaEventRecordWithFlags(ev, s(), cudaEventRecordExternal));
+    else
+      HCC_CUDA(cudaEventRecord(ev, s()));
+  }
+
+  // while (cond) body(h, use_cond); the body's last kernel sets the
+  // condition. The body always executes at least once.
+  void loop(const std::function<void(cudaGraphConditionalHandle, int)>& body) {
+    if (!graph_mode) {
+      for (;;) {
+        body(0, 0);
+        HCC_CUDA(cudaMemcpyAsync(&c->h_ctrl->cond, &c->d_ctrl->cond,
+                                 sizeof(u32), cudaMemcpyDeviceToHost, s()));
+        HCC_CUDA(cudaStreamSynchronize(s()));
+        if (!c->h_ctrl->cond) break;
+      }
+      return;
+    }
+    cudaStreamCaptureStatus st;
+    cudaGraph_t g = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    HCC_CUDA(cudaStreamGetCaptureInfo(s(), &st, nullptr, &g, &deps, &nd));
+    cudaGraphConditionalHandle h;
+    HCC_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1,
+                                              cudaGraphCondAssignDefault));
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeWhile;
+    p.conditional.size = 1;
+    cudaGraphNode_t node;
+    HCC_CUDA(cudaGraphAddNode(&node, g, deps, nd, &p));
+    HCC_CUDA(cudaStreamUpdateCaptureDependencies(
+        s(), &node, 1, cudaStreamSetCaptureDependencies));
+    cudaGraph_t body_graph = p.conditional.phGraph_out[0];
+    if ((int)streams.size() <= depth + 1) {
+      cudaStream_t ns;
+      HCC_CUDA(cudaStreamCreateWithFlags(&ns, cudaStreamNonBlocking));
+      streams.push_back(ns);
+    }
+    ++depth;
+    HCC_CUDA(cudaStreamBeginCaptureToGraph(s(), body_graph, nullptr, nullptr,
+                                           0, cudaStreamCaptureModeRelaxed));
+    body(h, 1);
+    cudaGraph_t out = nullptr;
+    HCC_CUDA(cudaStreamEndCapture(s(), &out));
+    --depth;
+  }
+};
+
+struct Plan {
+  int algo;
+  bool full_passes;
+  u64 n, m;
+  const uint2* edges;
+  u32* pi;
+  uint2* wl0;
+  uint2* wl1;
+  u64 nseg;
+  unsigned grid_hook, block_hook, grid_vert, block_vert;
+};
+
+HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
+  HookArgs a;
+  a.edges = P.edges;
+  a.m = P.m;
+  a.b = 0;
+  a.e = P.m;
+  a.mode = mode;
+  a.append = append;
+  a.pi = P.pi;
+  a.wl0 = P.wl0;
+  a.wl1 = P.wl1;
+  a.ctrl = c->d_ctrl;
+  a.recs = c->d_recs;
+  return a;
+}
+
+// Enqueue one full CC run (pi init through convergence) on seq.
+void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
+  c->seg_ev_used = 0;
+  k_begin<<<1, 1, 0, q.s()>>>(c->d_ctrl, c->d_recs, P.nseg);
+  k_init_pi<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n);
+  HCC_CUDA(cudaGetLastError());
+  DevCtrl* ctrl = c->d_ctrl;
+  DevRec* recs = c->d_recs;
+
+  switch (P.algo) {
+    case HCC_ALGO_BASELINE: {
+      q.loop([&](cudaGraphConditionalHandle ho, int uo) {
+        k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(
+            hook_args(c, P, kSrcRange, 0));
+        q.phase_done(HCC_PHASE_HOOK);
+        q.loop([&](cudaGraphConditionalHandle hi, int ui) {
+          k_jump<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl, recs);
+          k_step_jump<<<1, 1, 0, q.s()>>>(ctrl, hi, ui);
+        });
+        q.phase_done(HCC_PHASE_COMPRESS);
+        k_step_outer<<<1, 1, 0, q.s()>>>(ctrl, recs, ho, uo);
+      });
+      break;
+    }
+    case HCC_ALGO_BASELINE_MJ: {
+      if (P.full_passes) {
+        q.loop([&](cudaGraphConditionalHandle h, int u) {
+          k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(
+              hook_args(c, P, kSrcRange, 0));
+          q.phase_done(HCC_PHASE_HOOK);
+          k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
+                                                              recs, 0);
+          q.phase_done(HCC_PHASE_COMPRESS);
+          k_step_outer<<<1, 1, 0, q.s()>>>(ctrl, recs, h, u);
+        });
+        break;
+      }
+      // topology-driven first pass, segmented.  Few segments: unrolled in
+      // the root graph with CUDA events around every hook launch (the
+      // dominant kernel's per-launch time); many: a device loop.
+      c->seg_ev_used = 0;
+      if (P.nseg <= kMaxUnrolledSegments) {
+        while (c->seg_ev.size() < 2 * P.nseg) {
+          cudaEvent_t ev;
+          HCC_CUDA(cudaEventCreate(&ev));
+          c->seg_ev.push_back(ev);
+        }
+        for (u64 sgi = 0; sgi < P.nseg; ++sgi) {
+          q.record(c->seg_ev[2 * sgi]);
+          k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(
+              hook_args(c, P, kSrcSegment, 1));
+          q.record(c->seg_ev[2 * sgi + 1]);
+          q.phase_done(HCC_PHASE_HOOK);
+          k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
+                                                              recs, 1);
+          q.phase_done(HCC_PHASE_COMPRESS);
+          k_step_segment<<<1, 1, 0, q.s()>>>(ctrl, recs, 0, 0);
+        }
+        c->seg_ev_used = P.nseg;
+      } else {
+        q.loop([&](cudaGraphConditionalHandle h, int u) {
+          k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(
+              hook_args(c, P, kSrcSegment, 1));
+          q.phase_done(HCC_PHASE_HOOK);
+          k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
+                                                              recs, 1);
+          q.phase_done(HCC_PHASE_COMPRESS);
+          k_step_segment<<<1, 1, 0, q.s()>>>(ctrl, recs, h, u);
+        });
+      }
+      // data-driven passes over the compacted worklist
+      q.loop([&](cudaGraphConditionalHandle h, int u) {
+        k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(
+            hook_args(c, P, kSrcWorklist, 1));
+        q.phase_done(HCC_PHASE_HOOK);
+        k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
+                                                            recs, 1);
+        q.phase_done(HCC_PHASE_COMPRESS);
+        k_step_worklist<<<1, 1, 0, q.s()>>>(ctrl, recs, h, u);
+      });
+      break;
+    }
+    default: {  // ATOMIC / ADAPTIVE
+      q.loop([&](cudaGraphConditionalHandle h, int u) {
+        k_cas_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(
+            hook_args(c, P, kSrcSegment, 0));
+        q.phase_done(HCC_PHASE_HOOK);
+        k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
+                                                            recs, 0);
+        q.phase_done(HCC_PHASE_COMPRESS);
+        k_step_segment<<<1, 1, 0, q.s()>>>(ctrl, recs, h, u);
+      });
+      break;
+    }
+  }
+  HCC_CUDA(cudaGetLastError());
+}
+
+int ctx_enter(hcc_ctx* c) {
+  if (!c) return fail(HCC_EINVAL, "null context");
+  cudaError_t e = cudaSetDevice(c->dev);
+  if (e != cudaSuccess) return fail(HCC_ECUDA, cudaGetErrorString(e));
+  return HCC_OK;
+}
+
+// Device compute_stats (graph.hpp:43-68): keys (min<<32|max) of non-loop
+// edges, radix sort, unique, degree histogram over the unique pairs.
+__global__ void k_stat_keys(const uint2* e, u64 m, u64* keys) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    uint2 x = e[i];
+    keys[i] = x.x == x.y ? ~0ull
+                         : ((u64)min(x.x, x.y) << 32) | (u64)max(x.x, x.y);
+  }
+}
+
+__global__ void k_stat_unique(const u64* k, u64 m, u32* deg, u64* uniq) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  u64 cnt = 0;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    u64 x = k[i];
+    if (x == ~0ull) continue;
+    if (i > 0 && k[i - 1] == x) continue;
+    ++cnt;
+    atomicAdd(deg + (x >> 32), 1u);
+    atomicAdd(deg + (x & 0xffffffffull), 1u);
+  }
+  if (cnt) atomicAdd(uniq, cnt);
+}
+
+__global__ void k_stat_max(const u32* deg, u64 n, u32* out) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  u32 mx = 0;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    mx = max(mx, deg[i]);
+  if (mx) atomicMax(out, mx);
+}
+
+int compute_stats_dev(hcc_ctx* c, hcc_graph* g) {
+  hcc_graph_stats st{};
+  st.n = g->n;
+  st.m_stored = g->m;
+  if (g->n == 0) {
+    g->stats = st;
+    g->has_stats = true;
+    return HCC_OK;
+  }
+  u64 *keys = nullptr, *keys2 = nullptr, *d_uniq = nullptr;
+  u32 *deg = nullptr, *d_max = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  cudaStream_t s = c->stream;
+  const u64 m = g->m;
+  auto cleanup = [&] {
+    cudaFree(keys);
+    cudaFree(keys2);
+    cudaFree(d_uniq);
+    cudaFree(deg);
+    cudaFree(d_max);
+    cudaFree(tmp);
+  };
+  try {
+    HCC_CUDA(cudaMalloc(&deg, std::max<u64>(g->n, 1) * sizeof(u32)));
+    HCC_CUDA(cudaMalloc(&d_uniq, sizeof(u64)));
+    HCC_CUDA(cudaMalloc(&d_max, sizeof(u32)));
+    HCC_CUDA(cudaMemsetAsync(deg, 0, g->n * sizeof(u32), s));
+    HCC_CUDA(cudaMemsetAsync(d_uniq, 0, sizeof(u64), s));
+    HCC_CUDA(cudaMemsetAsync(d_max, 0, sizeof(u32), s));
+    if (m > 0) {
+      HCC_CUDA(cudaMalloc(&keys, m * sizeof(u64)));
+      HCC_CUDA(cudaMalloc(&keys2, m * sizeof(u64)));
+      k_stat_keys<<<grid_for(m, 256, 65536), 256, 0, s>>>(g->d_edges, m, keys);
+      // radix sort in chunks of at most 2^31 keys per call is not needed for
+      // CUB's 64-bit offset overload; use it directly.
+      HCC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys, keys2,
+                                               (int64_t)m, 0, 64, s));
+      HCC_CUDA(cudaMalloc(&tmp, tmp_bytes));
+      HCC_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys, keys2,
+                                               (int64_t)m, 0, 64, s));
+      k_stat_unique<<<grid_for(m, 256, 65536), 256, 0, s>>>(keys2, m, deg,
+                                                            d_uniq);
+    }
+    k_stat_max<<<grid_for(g->n, 256, 65536), 256, 0, s>>>(deg, g->n, d_max);
+    HCC_CUDA(cudaGetLastError());
+    u64 uniq = 0;
+    u32 mx = 0;
+    HCC_CUDA(cudaMemcpyAsync(&uniq, d_uniq, sizeof(u64), cudaMemcpyDeviceToHost, s));
+    HCC_CUDA(cudaMemcpyAsync(&mx, d_max, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    HCC_CUDA(cudaStreamSynchronize(s));
+    st.m_unique = uniq;
+    st.avg_degree = 2.0 * (double)uniq / (double)g->n;
+    st.max_degree = mx;
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+  g->stats = st;
+  g->has_stats = true;
+  return HCC_OK;
+}
+
+// Parse "k=v,k=v" parameters of a generator spec.
+bool spec_get(const std::string& params, const std::string& key,
+              std::string* out) {
+  size_t pos = 0;
+  while (pos <= params.size()) {
+    size_t comma = params.find(',', pos);
+    std::string item = params.substr(
+        pos, comma == std::string::npos ? std::string::npos : comma - pos);
+    size_t eq = item.find('=');
+    if (eq != std::string::npos && item.substr(0, eq) == key) {
+      *out = item.substr(eq + 1);
+      return true;
+    }
+    if (comma == std::string::npos) break;
+    pos = comma + 1;
+  }
+  return false;
+}
+
+bool parse_u64(const std::string& s, u64* out) {
+  if (s.empty()) return false;
+  u64 v = 0;
+  for (char ch : s) {
+    if (ch < '0' || ch > '9') return false;
+    v = v * 10 + (u64)(ch - '0');
+  }
+  *out = v;
+  return true;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+
+extern "C" {
+
+int hcc_abi_version(void) { return HCC_ABI_VERSION; }
+
+const char* hcc_last_error(void) { return g_err.c_str(); }
+
+int hcc_device_count(void) { return usable_devices(); }
+
+int hcc_create(int device, hcc_ctx** out) {
+  if (!out) return fail(HCC_EINVAL, "null output");
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(HCC_ENODEV, "no CUDA device visible (libhookcc_cuda has no "
+                            "CPU fallback)");
+  }
+  if (device < 0 || device >= count)
+    return fail(HCC_EINVAL, "device index out of range");
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess)
+    return fail(HCC_ECUDA, "cudaGetDeviceProperties failed");
+  if (prop.major != 10)
+    return fail(HCC_ENODEV, std::string("device ") + prop.name +
+                                " is not sm_100 (this build targets sm_100a)");
+  hcc_ctx* c = new hcc_ctx;
+  HCC_GUARD_BEGIN
+  c->dev = device;
+  HCC_CUDA(cudaSetDevice(device));
+  c->sms = prop.multiProcessorCount;
+  HCC_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  HCC_CUDA(cudaMalloc(&c->d_ctrl, sizeof(DevCtrl)));
+  HCC_CUDA(cudaMalloc(&c->d_recs, sizeof(DevRec) * kMaxRecs));
+  HCC_CUDA(cudaMallocHost(&c->h_ctrl, sizeof(DevCtrl)));
+  HCC_CUDA(cudaMallocHost(&c->h_recs, sizeof(DevRec) * kMaxRecs));
+  HCC_CUDA(cudaMemset(c->d_ctrl, 0, sizeof(DevCtrl)));
+  HCC_CUDA(cudaEventCreate(&c->ev0));
+  HCC_CUDA(cudaEventCreate(&c->ev1));
+  int occ = 0;
+  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook,
+                                                          kHookThreads, 0));
+  c->occ_hook = std::max(occ, 1);
+  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_compress,
+                                                          kVertThreads, 0));
+  c->occ_vert = std::max(occ, 1);
+  *out = c;
+  return HCC_OK;
+  }
+  catch (const CudaFail& f) {
+    hcc_destroy(c);
+    return f.code;
+  }
+}
+
+int hcc_destroy(hcc_ctx* c) {
+  if (!c) return HCC_OK;
+  cudaSetDevice(c->dev);
+  drop_exec(c);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  cudaFree(c->d_ctrl);
+  cudaFree(c->d_recs);
+  cudaFreeHost(c->h_ctrl);
+  cudaFreeHost(c->h_recs);
+  cudaFree(c->scratch_pi);
+  cudaFree(c->wl[0]);
+  cudaFree(c->wl[1]);
+  for (cudaEvent_t ev : c->seg_ev) cudaEventDestroy(ev);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return HCC_OK;
+}
+
+int hcc_ctx_segments(hcc_ctx* c, hcc_segment_rec* out, uint64_t cap,
+                     uint64_t* count) {
+  if (!c) return fail(HCC_EINVAL, "null context");
+  u64 k = std::min<u64>(cap, c->last_recs.size());
+  if (out)
+    for (u64 i = 0; i < k; ++i) out[i] = c->last_recs[i];
+  if (count) *count = c->last_recs.size();
+  return HCC_OK;
+}
+
+int hcc_ctx_sm_count(hcc_ctx* c, int* out) {
+  if (!c || !out) return fail(HCC_EINVAL, "null argument");
+  *out = c->sms;
+  return HCC_OK;
+}
+
+// ---- graphs ----------------------------------------------------------------
+
+int hcc_graph_from_edges_u64(hcc_ctx* c, const uint64_t* uv, uint64_t m,
+                             uint64_t n, hcc_graph** out) {
+  if (!out) return fail(HCC_EINVAL, "null output");
+  *out = nullptr;
+  if (int r = ctx_enter(c)) return r;
+  if (n > kMaxN)
+    return fail(HCC_EINVAL, "vertex count >= 2^32 is not supported by the "
+                            "device forest (u32 ids)");
+  if (m > 0 && !uv) return fail(HCC_EINVAL, "null edge buffer");
+  hcc_graph* g = new hcc_graph;
+  g->ctx = c;
+  g->n = n;
+  g->m = m;
+  u64* stage = nullptr;
+  u32* d_err = nullptr;
+  HCC_GUARD_BEGIN
+  HCC_CUDA(cudaMalloc(&g->d_edges, std::max<u64>(m, 2) * sizeof(uint2)));
+  HCC_CUDA(cudaMalloc(&d_err, sizeof(u32)));
+  HCC_CUDA(cudaMemsetAsync(d_err, 0, sizeof(u32), c->stream));
+  const u64 chunk = std::min<u64>(m, 1ull << 26);  // 1 GiB of u64 pairs
+  if (m > 0) HCC_CUDA(cudaMalloc(&stage, chunk * 2 * sizeof(u64)));
+  for (u64 off = 0; off < m; off += chunk) {
+    u64 k = std::min(chunk, m - off);
+    HCC_CUDA(cudaMemcpyAsync(stage, uv + 2 * off, k * 2 * sizeof(u64),
+                             cudaMemcpyHostToDevice, c->stream));
+    k_narrow_u64<<<grid_for(k, 256, 65536), 256, 0, c->stream>>>(
+        stage, g->d_edges + off, k, n, d_err);
+    HCC_CUDA(cudaGetLastError());
+  }
+  u32 err = 0;
+  HCC_CUDA(cudaMemcpyAsync(&err, d_err, sizeof(u32), cudaMemcpyDeviceToHost,
+                           c->stream));
+  HCC_CUDA(cudaStreamSynchronize(c->stream));
+  cudaFree(stage);
+  cudaFree(d_err);
+  stage = nullptr;
+  d_err = nullptr;
+  if (err) {
+    hcc_graph_free(g);
+    return fail(HCC_ERANGE, "edge endpoint out of range");
+  }
+  *out = g;
+  return HCC_OK;
+  }
+  catch (const CudaFail& f) {
+    cudaFree(stage);
+    cudaFree(d_err);
+    hcc_graph_free(g);
+    return f.code;
+  }
+}
+
+int hcc_graph_from_edges_u32(hcc_ctx* c, const uint32_t* uv, uint64_t m,
+                             uint64_t n, hcc_graph** out) {
+  if (!out) return fail(HCC_EINVAL, "null output");
+  *out = nullptr;
+  if (int r = ctx_enter(c)) return r;
+  if (n > kMaxN) return fail(HCC_EINVAL, "vertex count >= 2^32");
+  if (m > 0 && !uv) return fail(HCC_EINVAL, "null edge buffer");
+  hcc_graph* g = new hcc_graph;
+  g->ctx = c;
+  g->n = n;
+  g->m = m;
+  u32* d_err = nullptr;
+  HCC_GUARD_BEGIN
+  HCC_CUDA(cudaMalloc(&g->d_edges, std::max<u64>(m, 2) * sizeof(uint2)));
+  HCC_CUDA(cudaMalloc(&d_err, sizeof(u32)));
+  HCC_CUDA(cudaMemsetAsync(d_err, 0, sizeof(u32), c->stream));
+  if (m > 0) {
+    HCC_CUDA(cudaMemcpyAsync(g->d_edges, uv, m * sizeof(uint2),
+                             cudaMemcpyHostToDevice, c->stream));
+    k_check_u32<<<grid_for(m, 256, 65536), 256, 0, c->stream>>>(g->d_edges, m,
+                                                                n, d_err);
+    HCC_CUDA(cudaGetLastError());
+  }
+  u32 err = 0;
+  HCC_CUDA(cudaMemcpyAsync(&err, d_err, sizeof(u32), cudaMemcpyDeviceToHost,
+                           c->stream));
+  HCC_CUDA(cudaStreamSynchronize(c->stream));
+  cudaFree(d_err);
+  d_err = nullptr;
+  if (err) {
+    hcc_graph_free(g);
+    return fail(HCC_ERANGE, "edge endpoint out of range");
+  }
+  *out = g;
+  return HCC_OK;
+  }
+  catch (const CudaFail& f) {
+    cudaFree(d_err);
+    hcc_graph_free(g);
+    return f.code;
+  }
+}
+
+int hcc_graph_from_csr(hcc_ctx* c, const uint64_t* row_ptr, const uint32_t* col,
+                       uint64_t n, hcc_graph** out) {
+  if (!out) return fail(HCC_EINVAL, "null output");
+  *out = nullptr;
+  if (int r = ctx_enter(c)) return r;
+  if (n > kMaxN) return fail(HCC_EINVAL, "vertex count >= 2^32");
+  if (!row_ptr) return fail(HCC_EINVAL, "null row_ptr");
+  if (row_ptr[0] != 0) return fail(HCC_EINVAL, "row_ptr[0] must be 0");
+  for (u64 i = 0; i < n; ++i)
+    if (row_ptr[i + 1] < row_ptr[i])
+      return fail(HCC_EINVAL, "row_ptr must be non-decreasing");
+  const u64 m = row_ptr[n];
+  if (m > 0 && !col) return fail(HCC_EINVAL, "null col");
+  hcc_graph* g = new hcc_graph;
+  g->ctx = c;
+  g->n = n;
+  g->m = m;
+  u64* d_rp = nullptr;
+  u32 *d_col = nullptr, *d_err = nullptr;
+  HCC_GUARD_BEGIN
+  HCC_CUDA(cudaMalloc(&g->d_edges, std::max<u64>(m, 2) * sizeof(uint2)));
+  HCC_CUDA(cudaMalloc(&d_err, sizeof(u32)));
+  HCC_CUDA(cudaMemsetAsync(d_err, 0, sizeof(u32), c->stream));
+  if (m > 0) {
+    HCC_CUDA(cudaMalloc(&d_rp, (n + 1) * sizeof(u64)));
+    HCC_CUDA(cudaMalloc(&d_col, m * sizeof(u32)));
+    HCC_CUDA(cudaMemcpyAsync(d_rp, row_ptr, (n + 1) * sizeof(u64),
+                             cudaMemcpyHostToDevice, c->stream));
+    HCC_CUDA(cudaMemcpyAsync(d_col, col, m * sizeof(u32),
+                             cudaMemcpyHostToDevice, c->stream));
+    k_csr_expand<<<grid_for(m, 256, 65536), 256, 0, c->stream>>>(
+        d_rp, d_col, n, g->d_edges, m, d_err);
+    HCC_CUDA(cudaGetLastError());
+  }
+  u32 err = 0;
+  HCC_CUDA(cudaMemcpyAsync(&err, d_err, sizeof(u32), cudaMemcpyDeviceToHost,
+                           c->stream));
+  HCC_CUDA(cudaStreamSynchronize(c->stream));
+  cudaFree(d_rp);
+  cudaFree(d_col);
+  cudaFree(d_err);
+  d_rp = nullptr;
+  d_col = nullptr;
+  d_err = nullptr;
+  if (err) {
+    hcc_graph_free(g);
+    return fail(HCC_ERANGE, "column index out of range");
+  }
+  *out = g;
+  return HCC_OK;
+  }
+  catch (const CudaFail& f) {
+    cudaFree(d_rp);
+    cudaFree(d_col);
+    cudaFree(d_err);
+    hcc_graph_free(g);
+    return f.code;
+  }
+}
+
+int hcc_graph_generate(hcc_ctx* c, const char* spec_c, uint64_t default_seed,
+                       hcc_graph** out) {
+  if (!out || !spec_c) return fail(HCC_EINVAL, "null argument");
+  *out = nullptr;
+  if (int r = ctx_enter(c)) return r;
+  std::string spec(spec_c);
+  size_t colon = spec.find(':');
+  if (colon == std::string::npos)
+    return fail(HCC_EINVAL, "generator spec needs the form kind:params");
+  std::string kind = spec.substr(0, colon), params = spec.substr(colon + 1);
+  u64 n = 0, m = 0, rows = 0, cols = 0, seed = default_seed, scale = 0, ef = 0;
+  double a = 0.57, b = 0.19, cc = 0.19, d = 0.05;
+  std::string v;
+  if (kind == "grid") {
+    size_t x = params.find('x');
+    if (x == std::string::npos || !parse_u64(params.substr(0, x), &rows) ||
+        !parse_u64(params.substr(x + 1), &cols))
+      return fail(HCC_EINVAL, "grid spec needs RxC");
+    if (rows == 0 || cols == 0) return fail(HCC_EINVAL, "grid: zero vertices");
+    n = rows * cols;
+    m = rows * (cols - 1) + (rows - 1) * cols;
+  } else if (kind == "rmatx") {
+    if (!spec_get(params, "scale", &v) || !parse_u64(v, &scale) ||
+        !spec_get(params, "ef", &v) || !parse_u64(v, &ef))
+      return fail(HCC_EINVAL, "rmatx spec needs scale= and ef=");
+    if (scale > 32) return fail(HCC_EINVAL, "rmatx: scale > 32");
+    if (spec_get(params, "seed", &v) && !parse_u64(v, &seed))
+      return fail(HCC_EINVAL, "rmatx: bad seed");
+    if (spec_get(params, "a", &v)) a = atof(v.c_str());
+    if (spec_get(params, "b", &v)) b = atof(v.c_str());
+    if (spec_get(params, "c", &v)) cc = atof(v.c_str());
+    if (spec_get(params, "d", &v)) d = atof(v.c_str());
+    if (std::fabs(a + b + cc + d - 1.0) > 1e-9)
+      return fail(HCC_EINVAL, "rmat: quadrant probabilities must sum to 1");
+    n = 1ull << scale;
+    m = ef * n;
+  } else if (kind == "erx") {
+    if (!spec_get(params, "n", &v) || !parse_u64(v, &n) ||
+        !spec_get(params, "m", &v) || !parse_u64(v, &m))
+      return fail(HCC_EINVAL, "erx spec needs n= and m=");
+    if (spec_get(params, "seed", &v) && !parse_u64(v, &seed))
+      return fail(HCC_EINVAL, "erx: bad seed");
+    if (n == 0) return fail(HCC_EINVAL, "erdos_renyi: zero vertices");
+  } else {
+    return fail(HCC_EINVAL, "unknown device generator kind `" + kind + "`");
+  }
+  if (n > kMaxN + 1 || (kind != "rmatx" && n > kMaxN))
+    return fail(HCC_EINVAL, "vertex count >= 2^32");
+  if (kind == "rmatx" && n > kMaxN)
+    return fail(HCC_EINVAL, "rmatx: scale 32 needs 2^32 vertices (> u32)");
+  hcc_graph* g = new hcc_graph;
+  g->ctx = c;
+  g->n = n;
+  g->m = m;
+  HCC_GUARD_BEGIN
+  HCC_CUDA(cudaMalloc(&g->d_edges, std::max<u64>(m, 2) * sizeof(uint2)));
+  if (m > 0) {
+    unsigned grid = grid_for(m, 256, (u64)c->sms * 32);
+    if (kind == "grid") {
+      k_gen_grid<<<grid, 256, 0, c->stream>>>(g->d_edges, rows, cols);
+    } else if (kind == "rmatx") {
+      k_gen_rmatx<<<grid, 256, 0, c->stream>>>(
+          g->d_edges, 0, m, (u32)scale, seed, prob_threshold(a),
+          prob_threshold(a + b), prob_threshold(a + b + cc));
+    } else {
+      k_gen_erx<<<grid, 256, 0, c->stream>>>(g->d_edges, 0, m, n, seed);
+    }
+    HCC_CUDA(cudaGetLastError());
+  }
+  HCC_CUDA(cudaStreamSynchronize(c->stream));
+  *out = g;
+  return HCC_OK;
+  }
+  catch (const CudaFail& f) {
+    hcc_graph_free(g);
+    return f.code;
+  }
+}
+
+int hcc_graph_info(const hcc_graph* g, uint64_t* n, uint64_t* m) {
+  if (!g) return fail(HCC_EINVAL, "null graph");
+  if (n) *n = g->n;
+  if (m) *m = g->m;
+  return HCC_OK;
+}
+
+int hcc_graph_download_u32(hcc_ctx* c, const hcc_graph* g, uint32_t* uv,
+                           uint64_t first, uint64_t count) {
+  if (!g || (count && !uv)) return fail(HCC_EINVAL, "null argument");
+  if (first > g->m || count > g->m - first)
+    return fail(HCC_EINVAL, "range out of bounds");
+  if (int r = ctx_enter(c)) return r;
+  HCC_GUARD_BEGIN
+  if (count)
+    HCC_CUDA(cudaMemcpy(uv, g->d_edges + first, count * sizeof(uint2),
+                        cudaMemcpyDeviceToHost));
+  return HCC_OK;
+  HCC_GUARD_END
+}
+
+int hcc_graph_checksum(hcc_ctx* c, const hcc_graph* g, uint64_t* out) {
+  if (!g || !out) return fail(HCC_EINVAL, "null argument");
+  if (int r = ctx_enter(c)) return r;
+  u64* d = nullptr;
+  HCC_GUARD_BEGIN
+  HCC_CUDA(cudaMalloc(&d, sizeof(u64)));
+  HCC_CUDA(cudaMemsetAsync(d, 0, sizeof(u64), c->stream));
+  if (g->m)
+    k_checksum<<<grid_for(g->m, 256, (u64)c->sms * 16), 256, 0, c->stream>>>(
+        g->d_edges, g->m, d);
+  HCC_CUDA(cudaGetLastError());
+  HCC_CUDA(cudaMemcpyAsync(out, d, sizeof(u64), cudaMemcpyDeviceToHost,
+                           c->stream));
+  HCC_CUDA(cudaStreamSynchronize(c->stream));
+  cudaFree(d);
+  return HCC_OK;
+  }
+  catch (const CudaFail& f) {
+    cudaFree(d);
+    return f.code;
+  }
+}
+
+int hcc_graph_compute_stats(hcc_ctx* c, const hcc_graph* g_c,
+                            hcc_graph_stats* out) {
+  if (!g_c || !out) return fail(HCC_EINVAL, "null argument");
+  if (int r = ctx_enter(c)) return r;
+  hcc_graph* g = const_cast<hcc_graph*>(g_c);
+  HCC_GUARD_BEGIN
+  if (!g->has_stats)
+    if (int r = compute_stats_dev(c, g)) return r;
+  *out = g->stats;
+  return HCC_OK;
+  HCC_GUARD_END
+}
+
+int hcc_graph_free(hcc_graph* g) {
+  if (!g) return HCC_OK;
+  if (g->ctx) {
+    cudaSetDevice(g->ctx->dev);
+    // the cached executable graph may reference these edges
+    if (g->ctx->key.edges == g->d_edges) drop_exec(g->ctx);
+  }
+  cudaFree(g->d_edges);
+  delete g;
+  return HCC_OK;
+}
+
+uint64_t hcc_choose_segment_count(const hcc_graph_stats* st) {
+  // engines.hpp:35-41
+  if (!st || st->n == 0) return 1;
+  u64 s = (u64)std::floor(st->avg_degree + 0.5);
+  if (s < 1) s = 1;
+  if (st->m_stored > 0 && s > st->m_stored) s = st->m_stored;
+  return s;
+}
+
+// ---- the CC engine -----------------------------------------------------------
+
+static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
+                  hcc_forest* f, hcc_metrics* mx) {
+  const hcc_opts defaults = {HCC_ALGO_BASELINE_MJ, 0, 0, 0, 0, nullptr, nullptr};
+  if (!o) o = &defaults;
+  if (o->algo < HCC_ALGO_BASELINE || o->algo > HCC_ALGO_ADAPTIVE)
+    return fail(HCC_EINVAL, "unknown algorithm");
+  const u64 n = g->n, m = g->m;
+  if (f && f->n != n)
+    return fail(HCC_EINVAL, "forest size does not match the graph");
+  if (f && f->ctx && f->dev != c->dev)
+    return fail(HCC_EINVAL, "forest lives on another device");
+
+  hcc_metrics out{};
+  out.n = n;
+  out.m = m;
+  c->last_recs.clear();
+
+  // segments (engines.hpp:243-247 and partition_edges 43-62)
+  u64 requested = 1;
+  if (o->algo == HCC_ALGO_ADAPTIVE) {
+    requested = o->segments;
+    if (requested == 0) {
+      hcc_graph_stats st;
+      if (int r = hcc_graph_compute_stats(c, g, &st)) return r;
+      requested = hcc_choose_segment_count(&st);
+    }
+  } else if (o->algo == HCC_ALGO_BASELINE_MJ &&
+             !(o->flags & HCC_FLAG_FULL_PASSES)) {
+    requested = o->first_pass_segments;
+    if (requested == 0) {
+      // cost model: the first segment's hooks all land in
+      // the worklist (m/s records) while every segment costs one compress
+      // over n; s ~ sqrt(m/n) balances the two.
+      double r = n ? std::sqrt((double)m / (double)n) : 1.0;
+      requested = (u64)std::max(1.0, std::floor(r + 0.5));
+    }
+  }
+  if (requested < 1) requested = 1;
+  u64 nseg = std::max<u64>(1, std::min(requested, std::max<u64>(m, 1)));
+  out.s = nseg;
+  out.segments_clamped = requested > m && m > 0;
+
+  if (n == 0) {  // nothing to launch (test_engines.cpp:124)
+    if (mx) *mx = out;
+    return HCC_OK;
+  }
+
+  HCC_GUARD_BEGIN
+  u32* pi;
+  if (f) {
+    pi = f->d_pi;
+  } else {
+    ensure_pi(c, n);
+    pi = c->scratch_pi;
+  }
+  const bool uses_wl =
+      o->algo == HCC_ALGO_BASELINE_MJ && !(o->flags & HCC_FLAG_FULL_PASSES);
+  if (uses_wl) ensure_wl(c, m);
+
+  Plan P;
+  P.algo = o->algo;
+  P.full_passes = (o->flags & HCC_FLAG_FULL_PASSES) != 0;
+  P.n = n;
+  P.m = m;
+  P.edges = g->d_edges;
+  P.pi = pi;
+  P.wl0 = uses_wl ? c->wl[0] : nullptr;
+  P.wl1 = uses_wl ? c->wl[1] : nullptr;
+  P.nseg = nseg;
+  if (o->max_threads == 0) {
+    P.block_hook = kHookThreads;
+    P.grid_hook = (unsigned)(c->sms * c->occ_hook);
+    P.block_vert = kVertThreads;
+    P.grid_vert = grid_for(n, kVertThreads, 0x7fffffffull);
+  } else {
+    u64 t = o->max_threads;
+    unsigned blk = (unsigned)std::min<u64>(t, 256);
+    if (blk >= 32) blk &= ~31u;
+    unsigned grd = (unsigned)std::max<u64>(1, std::min<u64>(t / blk, 1u << 20));
+    P.block_hook = P.block_vert = blk;
+    P.grid_hook = P.grid_vert = grd;
+  }
+
+  const bool observer = o->observer != nullptr;
+  const bool graph_mode =
+      !observer && !(o->flags & (HCC_FLAG_HOST_LOOP | HCC_FLAG_NO_GRAPH));
+  out.used_device_loop = graph_mode ? 1 : 0;
+
+  Seq q;
+  q.c = c;
+  q.graph_mode = graph_mode;
+  q.streams.push_back(c->stream);
+  if (observer) {
+    hcc_forest view;
+    view.ctx = c;
+    view.dev = c->dev;
+    view.n = n;
+    view.d_pi = pi;
+    q.on_phase = [&, view](int phase) mutable {
+      HCC_CUDA(cudaStreamSynchronize(c->stream));
+      o->observer(o->observer_user, phase, &view);
+    };
+  }
+
+  GraphKey key;
+  key.algo = o->algo;
+  key.edges = g->d_edges;
+  key.pi = pi;
+  key.wl0 = P.wl0;
+  key.n = n;
+  key.m = m;
+  key.nseg = nseg;
+  key.max_threads = o->max_threads;
+  key.flags = o->flags;
+
+  if (graph_mode) {
+    if (!(c->exec && c->key == key)) {
+      drop_exec(c);
+      cudaGraph_t graph = nullptr;
+      HCC_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+      try {
+        enqueue_run(c, P, q);
+      } catch (...) {
+        cudaGraph_t tmp = nullptr;
+        cudaStreamEndCapture(c->stream, &tmp);
+        if (tmp) cudaGraphDestroy(tmp);
+        for (size_t i = 1; i < q.streams.size(); ++i)
+          cudaStreamDestroy(q.streams[i]);
+        throw;
+      }
+      HCC_CUDA(cudaStreamEndCapture(c->stream, &graph));
+      cudaError_t ie = cudaGraphInstantiate(&c->exec, graph, 0);
+      cudaGraphDestroy(graph);
+      for (size_t i = 1; i < q.streams.size(); ++i)
+        cudaStreamDestroy(q.streams[i]);
+      q.streams.resize(1);
+      if (ie != cudaSuccess) {
+        c->exec = nullptr;
+        return fail(HCC_ECUDA, std::string("cudaGraphInstantiate: ") +
+                                   cudaGetErrorString(ie));
+      }
+      c->key = key;
+      c->exec_seg_ev = c->seg_ev_used;
+    }
+    c->seg_ev_used = c->exec_seg_ev;
+    HCC_CUDA(cudaEventRecord(c->ev0, c->stream));
+    HCC_CUDA(cudaGraphLaunch(c->exec, c->stream));
+    HCC_CUDA(cudaEventRecord(c->ev1, c->stream));
+  } else {
+    HCC_CUDA(cudaEventRecord(c->ev0, c->stream));
+    enqueue_run(c, P, q);
+    HCC_CUDA(cudaEventRecord(c->ev1, c->stream));
+  }
+  HCC_CUDA(cudaEventSynchronize(c->ev1));
+  float ms = 0.f;
+  HCC_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  out.total_ms = ms;
+
+  // roots = components (count_components, engines.hpp:77-82), untimed
+  k_count_roots<<<grid_for(n, 256, (u64)c->sms * 16), 256, 0, c->stream>>>(
+      pi, n, c->d_ctrl);
+  if (o->flags & HCC_FLAG_CHECK_STAR)
+    k_is_star<<<grid_for(n, 256, (u64)c->sms * 16), 256, 0, c->stream>>>(
+        pi, n, c->d_ctrl);
+  HCC_CUDA(cudaGetLastError());
+  HCC_CUDA(cudaMemcpyAsync(c->h_ctrl, c->d_ctrl, sizeof(DevCtrl),
+                           cudaMemcpyDeviceToHost, c->stream));
+  HCC_CUDA(cudaStreamSynchronize(c->stream));
+  const u64 nrec = std::min<u64>(c->h_ctrl->rec, kMaxRecs);
+  if (nrec)
+    HCC_CUDA(cudaMemcpyAsync(c->h_recs, c->d_recs, nrec * sizeof(DevRec),
+                             cudaMemcpyDeviceToHost, c->stream));
+  HCC_CUDA(cudaStreamSynchronize(c->stream));
+  const DevCtrl& hc = *c->h_ctrl;
+  out.components = hc.components;
+  out.passes = hc.passes;
+  out.edges_processed = hc.edges_processed;
+  out.records = nrec;
+  c->last_recs.resize(nrec);
+  for (u64 i = 0; i < nrec; ++i) {
+    const DevRec& r = c->h_recs[i];
+    hcc_segment_rec sr{};
+    if (r.hook_t1 > r.hook_t0 && r.hook_t0 != ~0ull)
+      sr.hook_ms = (double)(r.hook_t1 - r.hook_t0) * 1e-6;
+    if (r.comp_t1 > r.comp_t0 && r.comp_t0 != ~0ull)
+      sr.compress_ms = (double)(r.comp_t1 - r.comp_t0) * 1e-6;
+    sr.counters.hook_traversal_steps = r.traversal;
+    sr.counters.cas_failures = r.cas_fail;
+    sr.counters.jump_steps = r.jump_steps;
+    sr.edges_in = r.edges_in;
+    sr.edges_out = r.edges_out;
+    sr.hook_event_ms = -1.0;
+    if (i < c->seg_ev_used) {
+      float ems = 0.f;
+      if (cudaEventElapsedTime(&ems, c->seg_ev[2 * i], c->seg_ev[2 * i + 1]) ==
+          cudaSuccess)
+        sr.hook_event_ms = ems;
+      else
+        cudaGetLastError();
+    }
+    c->last_recs[i] = sr;
+    out.hook_ms += sr.hook_ms;
+    out.compress_ms += sr.compress_ms;
+    out.counters.hook_traversal_steps += r.traversal;
+    out.counters.cas_failures += r.cas_fail;
+    out.counters.jump_steps += r.jump_steps;
+  }
+  if (o->algo == HCC_ALGO_BASELINE_MJ && !P.full_passes)
+    out.outer_iterations = 1 + (nrec > nseg ? nrec - nseg : 0);
+  else if (o->algo == HCC_ALGO_ADAPTIVE || o->algo == HCC_ALGO_ATOMIC)
+    out.outer_iterations = nseg;  // engines.hpp:288
+  else
+    out.outer_iterations = nrec;
+  if (mx) *mx = out;
+  if ((o->flags & HCC_FLAG_CHECK_STAR) && hc.flag)
+    return fail(HCC_ENOTSTAR, "extract_labels: forest is not star-shaped");
+  return HCC_OK;
+  HCC_GUARD_END
+}
+
+int hcc_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o, hcc_forest* f,
+           uint32_t* labels_out, hcc_metrics* mx) {
+  if (!g) return fail(HCC_EINVAL, "null graph");
+  if (int r = ctx_enter(c)) return r;
+  if (int r = run_cc(c, g, o, f, mx)) return r;
+  if (labels_out && g->n) {
+    const u32* pi = f ? f->d_pi : c->scratch_pi;
+    HCC_GUARD_BEGIN
+    HCC_CUDA(cudaMemcpy(labels_out, pi, g->n * sizeof(u32),
+                        cudaMemcpyDeviceToHost));
+    HCC_GUARD_END
+  }
+  return HCC_OK;
+}
+
+int hcc_cc_u64(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
+               hcc_forest* f, uint64_t* labels_out, hcc_metrics* mx) {
+  if (!g) return fail(HCC_EINVAL, "null graph");
+  if (int r = ctx_enter(c)) return r;
+  if (int r = run_cc(c, g, o, f, mx)) return r;
+  if (labels_out && g->n) {
+    const u32* pi = f ? f->d_pi : c->scratch_pi;
+    HCC_GUARD_BEGIN
+    // widen in place from the top: copy u32 labels into the upper half of
+    // the caller's u64 buffer, then expand forward-safely from the end.
+    uint32_t* tmp = reinterpret_cast<uint32_t*>(labels_out) + g->n;
+    HCC_CUDA(cudaMemcpy(tmp, pi, g->n * sizeof(u32), cudaMemcpyDeviceToHost));
+    for (u64 i = 0; i < g->n; ++i) labels_out[i] = tmp[i];
+    HCC_GUARD_END
+  }
+  return HCC_OK;
+}
+
+// ---- forests -----------------------------------------------------------------
+
+int hcc_forest_create(hcc_ctx* c, uint64_t n, hcc_forest** out) {
+  if (!out) return fail(HCC_EINVAL, "null output");
+  *out = nullptr;
+  if (int r = ctx_enter(c)) return r;
+  if (n > kMaxN) return fail(HCC_EINVAL, "forest size >= 2^32");
+  hcc_forest* f = new hcc_forest;
+  f->ctx = c;
+  f->dev = c->dev;
+  f->n = n;
+  HCC_GUARD_BEGIN
+  HCC_CUDA(cudaMalloc(&f->d_pi, std::max<u64>(n, 4) * sizeof(u32)));
+  *out = f;
+  int r = hcc_forest_reset(f);
+  if (r) {
+    hcc_forest_free(f);
+    *out = nullptr;
+  }
+  return r;
+  }
+  catch (const CudaFail& fl) {
+    hcc_forest_free(f);
+    return fl.code;
+  }
+}
+
+int hcc_forest_free(hcc_forest* f) {
+  if (!f) return HCC_OK;
+  cudaSetDevice(f->dev);
+  if (f->ctx && f->ctx->key.pi == f->d_pi) drop_exec(f->ctx);
+  cudaFree(f->d_pi);
+  delete f;
+  return HCC_OK;
+}
+
+int hcc_forest_size(const hcc_forest* f, uint64_t* n) {
+  if (!f || !n) return fail(HCC_EINVAL, "null argument");
+  *n = f->n;
+  return HCC_OK;
+}
+
+int hcc_forest_reset(hcc_forest* f) {
+  if (!f) return fail(HCC_EINVAL, "null forest");
+  HCC_GUARD_BEGIN
+  HCC_CUDA(cudaSetDevice(f->dev));
+  if (f->n) {
+    k_init_pi<<<grid_for(f->n, 256, 65536), 256, 0, cudaStreamPerThread>>>(
+        f->d_pi, f->n);
+    HCC_CUDA(cudaGetLastError());
+  }
+  HCC_CUDA(cudaStreamSynchronize(cudaStreamPerThread));
+  return HCC_OK;
+  HCC_GUARD_END
+}
+
+int hcc_forest_download_u32(hcc_forest* f, uint32_t* out) {
+  if (!f || (f->n && !out)) return fail(HCC_EINVAL, "null argument");
+  HCC_GUARD_BEGIN
+  HCC_CUDA(cudaSetDevice(f->dev));
+  if (f->n)
+    HCC_CUDA(cudaMemcpyAsync(out, f->d_pi, f->n * sizeof(u32),
+                             cudaMemcpyDeviceToHost, cudaStreamPerThread));
+  HCC_CUDA(cudaStreamSynchronize(cudaStreamPerThread));
+  return HCC_OK;
+  HCC_GUARD_END
+}
+
+int hcc_forest_download_u64(hcc_forest* f, uint64_t* out) {
+  if (!f || (f->n && !out)) return fail(HCC_EINVAL, "null argument");
+  std::vector<u32> tmp(f->n);
+  if (int r = hcc_forest_download_u32(f, tmp.data())) return r;
+  for (u64 i = 0; i < f->n; ++i) out[i] = tmp[i];
+  return HCC_OK;
+}
+
+int hcc_forest_upload_u64(hcc_forest* f, const uint64_t* in) {
+  if (!f || (f->n && !in)) return fail(HCC_EINVAL, "null argument");
+  std::vector<u32> tmp(f->n);
+  for (u64 i = 0; i < f->n; ++i) {
+    if (in[i] >= f->n) return fail(HCC_EINVAL, "parent out of range");
+    tmp[i] = (u32)in[i];
+  }
+  HCC_GUARD_BEGIN
+  HCC_CUDA(cudaSetDevice(f->dev));
+  if (f->n)
+    HCC_CUDA(cudaMemcpyAsync(f->d_pi, tmp.data(), f->n * sizeof(u32),
+                             cudaMemcpyHostToDevice, cudaStreamPerThread));
+  HCC_CUDA(cudaStreamSynchronize(cudaStreamPerThread));
+  return HCC_OK;
+  HCC_GUARD_END
+}
+
+static int elem(hcc_forest* f, int op, u64 a, u64 b, u64 cc, u64 res[3]) {
+  if (!f) return fail(HCC_EINVAL, "null forest");
+  HCC_GUARD_BEGIN
+  HCC_CUDA(cudaSetDevice(f->dev));
+  u64* h = nullptr;
+  u64* d = thread_scratch(f->dev, &h);
+  k_elem<<<1, 1, 0, cudaStreamPerThread>>>(f->d_pi, op, a, b, cc, d);
+  HCC_CUDA(cudaGetLastError());
+  HCC_CUDA(cudaMemcpyAsync(h, d, 3 * sizeof(u64), cudaMemcpyDeviceToHost,
+                           cudaStreamPerThread));
+  HCC_CUDA(cudaStreamSynchronize(cudaStreamPerThread));
+  res[0] = h[0];
+  res[1] = h[1];
+  res[2] = h[2];
+  return HCC_OK;
+  HCC_GUARD_END
+}
+
+#define HCC_CHECK_V(x)                                                      \
+  if ((x) >= f->n) return fail(HCC_EINVAL, "vertex out of range")
+
+int hcc_forest_load(hcc_forest* f, uint64_t v, uint64_t* out) {
+  if (!f || !out) return fail(HCC_EINVAL, "null argument");
+  HCC_CHECK_V(v);
+  u64 r[3];
+  if (int e = elem(f, kOpLoad, v, 0, 0, r)) return e;
+  *out = r[0];
+  return HCC_OK;
+}
+
+int hcc_forest_store(hcc_forest* f, uint64_t v, uint64_t p) {
+  if (!f) return fail(HCC_EINVAL, "null forest");
+  HCC_CHECK_V(v);
+  HCC_CHECK_V(p);
+  u64 r[3];
+  return elem(f, kOpStore, v, p, 0, r);
+}
+
+int hcc_forest_cas(hcc_forest* f, uint64_t v, uint64_t* expected,
+                   uint64_t desired, int* ok) {
+  if (!f || !expected || !ok) return fail(HCC_EINVAL, "null argument");
+  HCC_CHECK_V(v);
+  HCC_CHECK_V(desired);
+  u64 r[3];
+  if (*expected > kMaxN) {  // can never match a u32 slot
+    if (int e = hcc_forest_load(f, v, expected)) return e;
+    *ok = 0;
+    return HCC_OK;
+  }
+  if (int e = elem(f, kOpCas, v, *expected, desired, r)) return e;
+  *ok = (int)r[1];
+  if (!r[1]) *expected = r[0];
+  return HCC_OK;
+}
+
+int hcc_forest_hook(hcc_forest* f, uint64_t u, uint64_t v, int* changed) {
+  if (!f) return fail(HCC_EINVAL, "null forest");
+  HCC_CHECK_V(u);
+  HCC_CHECK_V(v);
+  u64 r[3];
+  if (int e = elem(f, kOpHook, u, v, 0, r)) return e;
+  if (changed) *changed = (int)r[0];
+  return HCC_OK;
+}
+
+int hcc_forest_jump(hcc_forest* f, uint64_t v, int* changed) {
+  if (!f) return fail(HCC_EINVAL, "null forest");
+  HCC_CHECK_V(v);
+  u64 r[3];
+  if (int e = elem(f, kOpJump, v, 0, 0, r)) return e;
+  if (changed) *changed = (int)r[0];
+  return HCC_OK;
+}
+
+int hcc_forest_atomic_hook(hcc_forest* f, uint64_t u, uint64_t v,
+                           hcc_counters* c) {
+  if (!f) return fail(HCC_EINVAL, "null forest");
+  HCC_CHECK_V(u);
+  HCC_CHECK_V(v);
+  u64 r[3];
+  if (int e = elem(f, kOpAtomicHook, u, v, 0, r)) return e;
+  if (c) {
+    c->hook_traversal_steps += r[0];
+    c->cas_failures += r[1];
+  }
+  return HCC_OK;
+}
+
+int hcc_forest_multi_jump(hcc_forest* f, uint64_t v, hcc_counters* c) {
+  if (!f) return fail(HCC_EINVAL, "null forest");
+  HCC_CHECK_V(v);
+  u64 r[3];
+  if (int e = elem(f, kOpMultiJump, v, 0, 0, r)) return e;
+  if (c) c->jump_steps += r[2];
+  return HCC_OK;
+}
+
+int hcc_forest_multi_jump_range(hcc_forest* f, uint64_t begin, uint64_t end,
+                                int descending, hcc_counters* c) {
+  if (!f) return fail(HCC_EINVAL, "null forest");
+  if (begin > end || end > f->n) return fail(HCC_EINVAL, "bad range");
+  if (begin == end) return HCC_OK;
+  u64 r[3];
+  if (int e = elem(f, kOpMultiJumpRange, begin, end, descending ? 1 : 0, r))
+    return e;
+  if (c) c->jump_steps += r[2];
+  return HCC_OK;
+}
+
+static int forest_flag_kernel(hcc_forest* f, bool star, int* out) {
+  if (!f || !out) return fail(HCC_EINVAL, "null argument");
+  if (f->n == 0) {
+    *out = 1;
+    return HCC_OK;
+  }
+  HCC_GUARD_BEGIN
+  HCC_CUDA(cudaSetDevice(f->dev));
+  u64* h = nullptr;
+  u64* d = thread_scratch(f->dev, &h);
+  // reuse the scratch as a DevCtrl-shaped flag holder: only ->flag is used
+  DevCtrl* dc = nullptr;
+  HCC_CUDA(cudaMalloc(&dc, sizeof(DevCtrl)));
+  HCC_CUDA(cudaMemsetAsync(dc, 0, sizeof(DevCtrl), cudaStreamPerThread));
+  unsigned grid = grid_for(f->n, 256, 4096);
+  if (star)
+    k_is_star<<<grid, 256, 0, cudaStreamPerThread>>>(f->d_pi, f->n, dc);
+  else
+    k_check_bound<<<grid, 256, 0, cudaStreamPerThread>>>(f->d_pi, f->n, dc);
+  cudaError_t le = cudaGetLastError();
+  u32 flag = 0;
+  cudaError_t ce = cudaMemcpyAsync(&flag, &dc->flag, sizeof(u32),
+                                   cudaMemcpyDeviceToHost, cudaStreamPerThread);
+  cudaError_t se = cudaStreamSynchronize(cudaStreamPerThread);
+  cudaFree(dc);
+  (void)d;
+  if (le != cudaSuccess || ce != cudaSuccess || se != cudaSuccess)
+    return fail(HCC_ECUDA, "flag kernel failed");
+  *out = flag ? 0 : 1;
+  return HCC_OK;
+  HCC_GUARD_END
+}
+
+int hcc_forest_is_star(hcc_forest* f, int* out) {
+  return forest_flag_kernel(f, true, out);
+}
+
+int hcc_forest_check_bound(hcc_forest* f, int* ok) {
+  return forest_flag_kernel(f, false, ok);
+}
+
+// ---- multi-GPU (implemented in hcc_multi.cu when NCCL is linked) -------------
+
+}  // extern "C"

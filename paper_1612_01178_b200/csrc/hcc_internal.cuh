@@ -1,0 +1,123 @@
+// Internal declarations shared by the hookcc CUDA translation units.
+//
+// Device data layout:
+//   edges  : uint2[m]      packed (u, v) u32 pairs, stored order preserved
+//                          (reference Graph.edges, graph.hpp:24-31, 16 B/edge
+//                          AoS u64 -> 8 B/edge here)
+//   pi     : uint32[n]     parent forest (reference ParentForest slots,
+//                          forest.hpp:62), pi(v) <= v always
+//   wl[2]  : uint2[cap]    ping-pong worklists of (H, L) root pairs
+//   ctrl   : DevCtrl       device-side loop state (counts, parity, flags)
+//   recs   : DevRec[]      per-phase timing / counter records
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hookcc_c.h"
+
+namespace hcc {
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+
+constexpr int kMaxRecs = 4096;    // per-run phase records kept on device
+constexpr int kHookThreads = 256;
+constexpr int kHookEPT = 8;       // edges per thread per tile (4 x uint4)
+constexpr int kVertThreads = 256;
+
+// One record per hook+compress phase pair (segment, outer iteration or
+// worklist pass).  Times are %globaltimer nanoseconds (first block start,
+// last block end).
+struct DevRec {
+  u64 hook_t0, hook_t1, comp_t0, comp_t1;
+  u64 traversal, cas_fail, jump_steps;
+  u64 edges_in, edges_out;
+};
+
+struct DevCtrl {
+  u64 wl_count[2];   // worklist fill counts
+  u64 seg;           // current segment (segmented loops)
+  u64 nseg;          // number of segments
+  u64 passes;        // hook passes executed
+  u64 edges_processed;
+  u64 components;
+  u32 parity;        // worklist index that is the NEXT hook input
+  u32 rec;           // current record index
+  u32 dirty;         // a hook in the current phase wrote pi
+  u32 changed;       // baseline: some hook saw pi(u) != pi(v)
+  u32 jchanged;      // baseline: some jump changed a slot
+  u32 cond;          // last loop condition (host-loop mode reads it)
+  u32 err;           // sticky device error bits
+  u32 flag;          // scratch result flag (is_star / bound checks)
+};
+
+// Source of a hook phase.
+enum HookMode : int {
+  kSrcRange = 0,     // edges[b, e)
+  kSrcSegment = 1,   // segment ctrl->seg of partition_edges(m, ctrl->nseg)
+  kSrcWorklist = 2,  // wl[ctrl->parity][0, wl_count[parity])
+};
+
+struct HookArgs {
+  const uint2* edges;
+  u64 m;
+  u64 b, e;
+  int mode;
+  int append;        // append (H, L) of every write to the next worklist
+  u32* pi;
+  uint2* wl0;
+  uint2* wl1;
+  DevCtrl* ctrl;
+  DevRec* recs;
+};
+
+// Launch shape chosen on the host.
+struct Launch {
+  int grid_hook;     // persistent hook grid
+  int block_hook;
+  int grid_vert;     // vertex-parallel grid (0 = cover n)
+  int block_vert;
+  u64 max_threads;   // 0 = unlimited
+};
+
+// ---- kernels (hcc_kernels.cu) -------------------------------------------
+__global__ void k_begin(DevCtrl* ctrl, DevRec* recs, u64 nseg);
+__global__ void k_init_pi(u32* pi, u64 n);
+__global__ void k_hook(HookArgs a);
+__global__ void k_cas_hook(HookArgs a);
+__global__ void k_compress(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
+                           int skip_if_clean);
+__global__ void k_jump(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs);
+__global__ void k_step_worklist(DevCtrl* ctrl, DevRec* recs,
+                                cudaGraphConditionalHandle h, int use_cond);
+__global__ void k_step_segment(DevCtrl* ctrl, DevRec* recs,
+                               cudaGraphConditionalHandle h, int use_cond);
+__global__ void k_step_outer(DevCtrl* ctrl, DevRec* recs,
+                             cudaGraphConditionalHandle h, int use_cond);
+__global__ void k_step_jump(DevCtrl* ctrl, cudaGraphConditionalHandle h,
+                            int use_cond);
+__global__ void k_count_roots(const u32* pi, u64 n, DevCtrl* ctrl);
+__global__ void k_is_star(const u32* pi, u64 n, DevCtrl* ctrl);
+__global__ void k_check_bound(const u32* pi, u64 n, DevCtrl* ctrl);
+
+// Element kernels (single thread) for the ParentForest API.
+enum ElemOp : int {
+  kOpLoad = 0, kOpStore, kOpCas, kOpHook, kOpJump, kOpAtomicHook,
+  kOpMultiJump, kOpMultiJumpRange
+};
+__global__ void k_elem(u32* pi, int op, u64 a, u64 b, u64 c, u64* res);
+
+// Ingestion / generators (hcc_graph.cu).
+__global__ void k_narrow_u64(const u64* uv, uint2* out, u64 m, u64 n,
+                             u32* err);
+__global__ void k_check_u32(const uint2* e, u64 m, u64 n, u32* err);
+__global__ void k_csr_expand(const u64* row_ptr, const u32* col, u64 n,
+                             uint2* out, u64 m, u32* err);
+__global__ void k_gen_grid(uint2* out, u64 rows, u64 cols);
+__global__ void k_gen_rmatx(uint2* out, u64 first, u64 count, u32 scale,
+                            u64 seed, u32 ta, u32 tab, u32 tabc);
+__global__ void k_gen_erx(uint2* out, u64 first, u64 count, u64 n, u64 seed);
+__global__ void k_checksum(const uint2* e, u64 m, u64* out);
+
+}  // namespace hcc

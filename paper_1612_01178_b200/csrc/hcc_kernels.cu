@@ -1,0 +1,553 @@
+// Hook-Compress kernels for sm_100a.
+//
+// Reference semantics (all paths relative to /root/reference):
+//   hook         proj/include/hookcc/forest.hpp:83-89   (paper Fig. 2)
+//   jump         proj/include/hookcc/forest.hpp:93-99
+//   atomic_hook  proj/include/hookcc/forest.hpp:107-122 (paper Fig. 3)
+//   multi_jump   proj/include/hookcc/forest.hpp:127-136 (paper Fig. 3)
+//   is_star      proj/include/hookcc/forest.hpp:140-146
+//   loops        proj/include/hookcc/engines.hpp:123-291
+//
+// B200 design:
+//   * k_hook is the atomic-free Hook.  It streams packed u32 edge pairs with
+//     16-byte streaming loads (two edges per uint4, 8 edges per thread per
+//     tile), gathers pi(u), pi(v) for all 8 edges before any store (16 loads
+//     in flight per thread), stores pi[max] = min with a plain st.global,
+//     and appends the (H, L) pair of every store to the next worklist with a
+//     block-aggregated reservation (one global atomic per 2048-edge tile).
+//     The same kernel serves the topology pass (mode range/segment) and the
+//     data-driven passes (mode worklist); the worklist length lives on the
+//     device, so passes chain without host round trips.
+//   * k_compress is Multi-Jump with eager writes, ascending vertex order and
+//     warp-level early exit (a warp whose lanes all see star parents leaves
+//     after one coalesced read + one hot gather).
+//   * Step kernels advance device-side loop state and set the CUDA-graph
+//     conditional-node value.
+#include <cuda_runtime.h>
+
+#include "hcc_internal.cuh"
+
+namespace hcc {
+
+namespace {
+
+__device__ __forceinline__ u64 gtime() {
+  u64 t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Streaming 16-byte edge load: read once, do not allocate in L1, evict first
+// from L2 so the edge stream does not push pi out of the 126 MB L2.
+__device__ __forceinline__ u64 policy_evict_first() {
+  u64 pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;"
+               : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ uint4 ld_stream16(const uint4* p, u64 pol) {
+  uint4 r;
+  asm volatile(
+      "ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, "
+      "[%4], %5;"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p), "l"(pol));
+  return r;
+}
+
+// pi gather that may hit a stale L1 line; fine for the atomic-free hook
+// (any value ever held by the slot is a valid ancestor).
+__device__ __forceinline__ u32 ld_pi(const u32* p) { return *p; }
+
+// Coherent (L2) read: sees other threads' stores made during this kernel.
+__device__ __forceinline__ u32 ld_fresh(const u32* p) { return __ldcg(p); }
+
+__device__ __forceinline__ void rec_clear(DevRec& r) {
+  r.hook_t0 = ~0ull;
+  r.hook_t1 = 0;
+  r.comp_t0 = ~0ull;
+  r.comp_t1 = 0;
+  r.traversal = r.cas_fail = r.jump_steps = 0;
+  r.edges_in = r.edges_out = 0;
+}
+
+__device__ __forceinline__ DevRec* cur_rec(DevCtrl* c, DevRec* recs) {
+  u32 i = c->rec;
+  return recs + (i < (u32)kMaxRecs ? i : (u32)kMaxRecs - 1);
+}
+
+__device__ __forceinline__ void next_rec(DevCtrl* c, DevRec* recs) {
+  if (c->rec + 1 < (u32)kMaxRecs) {
+    c->rec += 1;
+    rec_clear(recs[c->rec]);
+  }
+}
+
+__device__ __forceinline__ void block_t0(u64* t0) {
+  if (threadIdx.x == 0) atomicMin(t0, gtime());
+}
+
+__device__ __forceinline__ void block_t1(u64* t1) {
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(t1, gtime());
+}
+
+// Adds a per-thread counter into a global u64.  Must be reached by every
+// thread of the block (uniform control flow).
+__device__ __forceinline__ void add_counter(u64* dst, u64 v) {
+  if ((blockDim.x & 31u) == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31u) == 0 && v) atomicAdd(dst, v);
+  } else if (v) {
+    atomicAdd(dst, v);
+  }
+}
+
+__device__ __forceinline__ void resolve_src(const HookArgs& a, const uint2*& src,
+                                            u64& b, u64& e, u32& out) {
+  const DevCtrl* c = a.ctrl;
+  if (a.mode == kSrcRange) {
+    src = a.edges;
+    b = a.b;
+    e = a.e;
+    out = c->parity;
+  } else if (a.mode == kSrcSegment) {
+    // partition_edges(m, s) (engines.hpp:43-58): the first m % s segments
+    // get one extra edge.
+    u64 s = c->nseg ? c->nseg : 1, seg = c->seg;
+    u64 base = a.m / s, rem = a.m % s;
+    b = seg * base + (seg < rem ? seg : rem);
+    e = b + base + (seg < rem ? 1 : 0);
+    if (e > a.m) e = a.m;
+    if (b > e) b = e;
+    src = a.edges;
+    out = c->parity;
+  } else {
+    u32 p = c->parity;
+    src = p ? a.wl1 : a.wl0;
+    b = 0;
+    e = c->wl_count[p];
+    out = p ^ 1u;
+  }
+}
+
+// Reserve space for `c` entries of this thread in the output worklist with
+// one global atomic per block; returns this thread's first slot.
+__device__ __forceinline__ bool block_reserve(u32 c, u64* cnt, DevRec* r,
+                                              DevCtrl* ctrl, u64& pos) {
+  __shared__ u32 s_w[32];
+  __shared__ u64 s_base;
+  if (!__syncthreads_or(c != 0)) return false;
+  if ((blockDim.x & 31u) != 0) {
+    // Tiny launches (max_threads < 32): per-thread reservation, in thread
+    // order so a single-thread launch is deterministic.
+    for (u32 t = 0; t < blockDim.x; ++t) {
+      if (t == threadIdx.x && c) {
+        pos = atomicAdd(cnt, (u64)c);
+        atomicAdd(&r->edges_out, (u64)c);
+        ctrl->dirty = 1;
+      }
+      __syncthreads();
+    }
+    return c != 0;
+  }
+  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  u32 x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    u32 y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= (u32)o) x += y;
+  }
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const u32 nw = blockDim.x >> 5;
+    u32 w = lane < nw ? s_w[lane] : 0u;
+    u32 inc = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      u32 y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= (u32)o) inc += y;
+    }
+    if (lane < nw) s_w[lane] = inc - w;
+    if (lane == 31) {
+      s_base = atomicAdd(cnt, (u64)inc);
+      atomicAdd(&r->edges_out, (u64)inc);
+      ctrl->dirty = 1;
+    }
+  }
+  __syncthreads();
+  pos = s_base + s_w[warp] + (x - c);
+  return c != 0;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+
+__global__ void k_begin(DevCtrl* ctrl, DevRec* recs, u64 nseg) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    DevCtrl c = {};
+    c.nseg = nseg ? nseg : 1;
+    *ctrl = c;
+    rec_clear(recs[0]);
+  }
+}
+
+// pi(v) = v (ParentForest::reset, forest.hpp:25-28), 16-byte stores.
+__global__ void k_init_pi(u32* pi, u64 n) {
+  const u64 tid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  const u64 n4 = n >> 2;
+  uint4* p4 = reinterpret_cast<uint4*>(pi);
+  for (u64 i = tid; i < n4; i += stride) {
+    u32 v = (u32)(i << 2);
+    p4[i] = make_uint4(v, v + 1, v + 2, v + 3);
+  }
+  for (u64 v = (n4 << 2) + tid; v < n; v += stride) pi[v] = (u32)v;
+}
+
+// Atomic-free Hook (forest.hpp:83-89) over an edge range, a segment or the
+// current worklist.  See the file comment for the design.
+__global__ void __launch_bounds__(kHookThreads) k_hook(HookArgs a) {
+  const uint2* src;
+  u64 b, e;
+  u32 out;
+  resolve_src(a, src, b, e, out);
+  DevCtrl* ctrl = a.ctrl;
+  DevRec* r = cur_rec(ctrl, a.recs);
+  block_t0(&r->hook_t0);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && e > b) {
+    atomicAdd(&r->edges_in, e - b);
+    atomicAdd(&ctrl->edges_processed, e - b);
+  }
+  u32* pi = a.pi;
+  uint2* wl_out = out ? a.wl1 : a.wl0;
+  u64* cnt_out = &ctrl->wl_count[out];
+
+  // Head / tail edges that do not fill a 16-byte pair: thread 0 of block 0.
+  u64 b2 = b + (b & 1ull);
+  if (b2 > e) b2 = e;
+  const u64 n4 = (e - b2) >> 1;
+  u32 any_change = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    u64 idx[2];
+    int k = 0;
+    if (b2 != b) idx[k++] = b;
+    if ((e - b2) & 1ull) idx[k++] = e - 1;
+    for (int j = 0; j < k; ++j) {
+      uint2 ed = src[idx[j]];
+      u32 pu = ld_pi(pi + ed.x), pv = ld_pi(pi + ed.y);
+      if (pu != pv) {
+        u32 h = max(pu, pv), l = min(pu, pv);
+        pi[h] = l;
+        any_change = 1;
+        if (a.append) {
+          u64 pos = atomicAdd(cnt_out, 1ull);
+          wl_out[pos] = make_uint2(h, l);
+          atomicAdd(&r->edges_out, 1ull);
+          ctrl->dirty = 1;
+        }
+      }
+    }
+  }
+
+  const uint4* s4 = reinterpret_cast<const uint4*>(src + b2);
+  const u64 pol = policy_evict_first();
+  const u64 tile = (u64)blockDim.x * (kHookEPT / 2);
+  const u64 ntiles = (n4 + tile - 1) / tile;
+  for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    uint2 ed[kHookEPT];
+#pragma unroll
+    for (int j = 0; j < kHookEPT / 2; ++j) {
+      const u64 i = t * tile + (u64)j * blockDim.x + threadIdx.x;
+      if (i < n4) {
+        uint4 q = ld_stream16(s4 + i, pol);
+        ed[2 * j] = make_uint2(q.x, q.y);
+        ed[2 * j + 1] = make_uint2(q.z, q.w);
+      } else {
+        // Out-of-range slots become the self-loop (0,0): a no-op hook.
+        ed[2 * j] = make_uint2(0u, 0u);
+        ed[2 * j + 1] = make_uint2(0u, 0u);
+      }
+    }
+    u32 pu[kHookEPT], pv[kHookEPT];
+#pragma unroll
+    for (int k = 0; k < kHookEPT; ++k) {
+      pu[k] = ld_pi(pi + ed[k].x);
+      pv[k] = ld_pi(pi + ed[k].y);
+    }
+    u32 act = 0;
+#pragma unroll
+    for (int k = 0; k < kHookEPT; ++k) {
+      if (pu[k] != pv[k]) {
+        const u32 h = max(pu[k], pv[k]), l = min(pu[k], pv[k]);
+        pi[h] = l;
+        pu[k] = h;
+        pv[k] = l;
+        act |= 1u << k;
+      }
+    }
+    if (a.append) {
+      u64 pos;
+      if (block_reserve(__popc(act), cnt_out, r, ctrl, pos)) {
+#pragma unroll
+        for (int k = 0; k < kHookEPT; ++k)
+          if (act & (1u << k)) wl_out[pos++] = make_uint2(pu[k], pv[k]);
+      }
+    } else {
+      any_change |= act;
+    }
+  }
+  if (!a.append) {
+    if (__syncthreads_or(any_change != 0) && threadIdx.x == 0) {
+      ctrl->changed = 1;
+      ctrl->dirty = 1;
+    }
+  }
+  block_t1(&r->hook_t1);
+}
+
+// CAS-verified hook (forest.hpp:107-122): walks down until it acquires a
+// root slot; counters follow the reference definitions.
+__global__ void __launch_bounds__(kHookThreads) k_cas_hook(HookArgs a) {
+  const uint2* src;
+  u64 b, e;
+  u32 out;
+  resolve_src(a, src, b, e, out);
+  DevCtrl* ctrl = a.ctrl;
+  DevRec* r = cur_rec(ctrl, a.recs);
+  block_t0(&r->hook_t0);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && e > b) {
+    atomicAdd(&r->edges_in, e - b);
+    atomicAdd(&ctrl->edges_processed, e - b);
+  }
+  u32* pi = a.pi;
+  u64 trav = 0, fails = 0;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = b + (u64)blockIdx.x * blockDim.x + threadIdx.x; i < e;
+       i += stride) {
+    uint2 ed = src[i];
+    u32 u = ed.x, v = ed.y;
+    for (;;) {
+      u32 pu = ld_fresh(pi + u), pv = ld_fresh(pi + v);
+      if (pu == pv) break;
+      ++trav;
+      u32 h = max(pu, pv), l = min(pu, pv);
+      u32 old = atomicCAS(pi + h, h, l);
+      if (old == h) break;
+      ++fails;
+      u = old;
+      v = l;
+    }
+  }
+  add_counter(&r->traversal, trav);
+  add_counter(&r->cas_fail, fails);
+  if (threadIdx.x == 0 && blockIdx.x == 0) ctrl->dirty = 1;
+  block_t1(&r->hook_t1);
+}
+
+// Multi-Jump compress (forest.hpp:127-136) over all vertices in ascending
+// block order, eager writes.  A vertex that is a root or already points at a
+// root costs one coalesced read and one (usually L1/L2-hot) gather; warps
+// whose lanes are all in that state exit the chase loop together.
+__global__ void __launch_bounds__(kVertThreads)
+    k_compress(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs, int skip_if_clean) {
+  if (skip_if_clean && *(volatile u32*)&ctrl->dirty == 0) return;
+  DevRec* r = cur_rec(ctrl, recs);
+  block_t0(&r->comp_t0);
+  u64 steps = 0;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 v = (u64)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+    u32 p = ld_fresh(pi + v);
+    if (p == (u32)v) continue;
+    u32 gp = ld_fresh(pi + p);
+    while (gp != p) {
+      pi[v] = gp;
+      ++steps;
+      p = gp;
+      gp = ld_fresh(pi + p);
+    }
+  }
+  add_counter(&r->jump_steps, steps);
+  block_t1(&r->comp_t1);
+}
+
+// Single-level jump pass (forest.hpp:93-99) with a device change flag.
+__global__ void __launch_bounds__(kVertThreads)
+    k_jump(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs) {
+  DevRec* r = cur_rec(ctrl, recs);
+  block_t0(&r->comp_t0);
+  u64 steps = 0;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 v = (u64)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+    u32 p = ld_fresh(pi + v);
+    u32 gp = ld_fresh(pi + p);
+    if (gp != p) {
+      pi[v] = gp;
+      ++steps;
+    }
+  }
+  if (__syncthreads_or(steps != 0) && threadIdx.x == 0) ctrl->jchanged = 1;
+  add_counter(&r->jump_steps, steps);
+  block_t1(&r->comp_t1);
+}
+
+// ---- loop-step kernels (single thread) ------------------------------------
+
+// Worklist pass finished: the output becomes the next input.
+__global__ void k_step_worklist(DevCtrl* c, DevRec* recs,
+                                cudaGraphConditionalHandle h, int use_cond) {
+  const u32 in = c->parity, out = in ^ 1u;
+  const u64 produced = c->wl_count[out];
+  c->parity = out;
+  c->wl_count[in] = 0;
+  c->passes += 1;
+  c->dirty = 0;
+  next_rec(c, recs);
+  const u32 cond = produced > 0 ? 1u : 0u;
+  c->cond = cond;
+  if (use_cond) cudaGraphSetConditional(h, cond);
+}
+
+// Segment finished (topology pass / adaptive segments).
+__global__ void k_step_segment(DevCtrl* c, DevRec* recs,
+                               cudaGraphConditionalHandle h, int use_cond) {
+  c->seg += 1;
+  c->passes += 1;
+  c->dirty = 0;
+  next_rec(c, recs);
+  const u32 cond = c->seg < c->nseg ? 1u : 0u;
+  c->cond = cond;
+  if (use_cond) cudaGraphSetConditional(h, cond);
+}
+
+// Baseline outer iteration finished: loop while some hook changed.
+__global__ void k_step_outer(DevCtrl* c, DevRec* recs,
+                             cudaGraphConditionalHandle h, int use_cond) {
+  const u32 cond = c->changed ? 1u : 0u;
+  c->changed = 0;
+  c->passes += 1;
+  c->dirty = 0;
+  next_rec(c, recs);
+  c->cond = cond;
+  if (use_cond) cudaGraphSetConditional(h, cond);
+}
+
+// Baseline inner jump loop: repeat while a jump changed a slot.
+__global__ void k_step_jump(DevCtrl* c, cudaGraphConditionalHandle h,
+                            int use_cond) {
+  const u32 cond = c->jchanged ? 1u : 0u;
+  c->jchanged = 0;
+  c->cond = cond;
+  if (use_cond) cudaGraphSetConditional(h, cond);
+}
+
+// ---- reductions -----------------------------------------------------------
+
+__global__ void k_count_roots(const u32* pi, u64 n, DevCtrl* ctrl) {
+  u64 cnt = 0;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 v = (u64)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride)
+    cnt += (pi[v] == (u32)v);
+  add_counter(&ctrl->components, cnt);
+}
+
+// flag != 0 iff some v has pi(pi(v)) != pi(v).
+__global__ void k_is_star(const u32* pi, u64 n, DevCtrl* ctrl) {
+  u32 bad = 0;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 v = (u64)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+    u32 p = pi[v];
+    bad |= (pi[p] != p);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) ctrl->flag = 1;
+}
+
+// flag != 0 iff some v has pi(v) > v.
+__global__ void k_check_bound(const u32* pi, u64 n, DevCtrl* ctrl) {
+  u32 bad = 0;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 v = (u64)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride)
+    bad |= (pi[v] > (u32)v);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) ctrl->flag = 1;
+}
+
+// ---- element kernels for the ParentForest API ------------------------------
+// One device thread; results in res[0..3]: res[0] = value / changed / steps,
+// res[1] = ok / cas failures, res[2] = jump steps.
+__global__ void k_elem(u32* pi, int op, u64 a, u64 b, u64 c, u64* res) {
+  volatile u32* vp = pi;
+  u64 r0 = 0, r1 = 0, r2 = 0;
+  switch (op) {
+    case kOpLoad:
+      r0 = vp[a];
+      break;
+    case kOpStore:
+      vp[a] = (u32)b;
+      break;
+    case kOpCas: {
+      u32 old = atomicCAS(pi + a, (u32)b, (u32)c);
+      r0 = old;
+      r1 = old == (u32)b;
+      break;
+    }
+    case kOpHook: {  // forest.hpp:83-89
+      u32 pu = vp[a], pv = vp[b];
+      if (pu != pv) {
+        vp[max(pu, pv)] = min(pu, pv);
+        r0 = 1;
+      }
+      break;
+    }
+    case kOpJump: {  // forest.hpp:93-99
+      u32 p = vp[a], gp = vp[p];
+      if (gp != p) {
+        vp[a] = gp;
+        r0 = 1;
+      }
+      break;
+    }
+    case kOpAtomicHook: {  // forest.hpp:107-122
+      u32 u = (u32)a, v = (u32)b;
+      for (;;) {
+        u32 pu = vp[u], pv = vp[v];
+        if (pu == pv) break;
+        ++r0;
+        u32 h = max(pu, pv), l = min(pu, pv);
+        u32 old = atomicCAS(pi + h, h, l);
+        if (old == h) break;
+        ++r1;
+        u = old;
+        v = l;
+      }
+      break;
+    }
+    case kOpMultiJump:
+    case kOpMultiJumpRange: {  // forest.hpp:127-136
+      u64 lo = a, hi = op == kOpMultiJump ? a + 1 : b;
+      const bool desc = op == kOpMultiJumpRange && c != 0;
+      for (u64 k = 0; k < hi - lo; ++k) {
+        u64 v = desc ? hi - 1 - k : lo + k;
+        u32 p = vp[v];
+        for (;;) {
+          u32 gp = vp[p];
+          if (gp == p) break;
+          vp[v] = gp;
+          ++r2;
+          p = gp;
+        }
+      }
+      break;
+    }
+    default:
+      break;
+  }
+  res[0] = r0;
+  res[1] = r1;
+  res[2] = r2;
+}
+
+}  // namespace hcc
