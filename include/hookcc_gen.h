@@ -10,7 +10,8 @@
 // (generators.hpp:14-26) — but draw each random word from a counter
 // (splitmix64 of seed and position), so edge i depends only on (seed, i)
 // and any range can be generated in parallel.  oracle/hookcc_oracle.c
-// restates them independently for the bit-exact parity tests.
+// restates them independently (this header is shared by the device kernels
+// and the host C++ API) for the bit-exact parity tests.
 //
 //   word(key, c)  = mix64(key + (c + 1) * 0x9E3779B97F4A7C15)
 //   key           = mix64(seed ^ 0x5851F42D4C957F2D)

@@ -136,7 +136,7 @@ int oracle_gen_grid(u64 rows, u64 cols, u64* uv) {
   return 0;
 }
 
-/* ---- counter-based twins (restating paper_1612_01178_b200/csrc/hcc_gen.h
+/* ---- counter-based twins (restating include/hookcc_gen.h
  * from its written specification, independently of that code) ----------- */
 
 static u64 sm_final(u64 z) {

@@ -31,7 +31,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 
-#include "hcc_gen.h"
+#include "hookcc_gen.h"
 #include "hcc_internal.cuh"
 #include "hookcc_c.h"
 
@@ -265,8 +265,13 @@ struct Seq {
     size_t nd = 0;
     HCC_CUDA(cudaStreamGetCaptureInfo(s(), &st, nullptr, &g, &deps, &nd));
     cudaGraphConditionalHandle h;
-    HCC_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1,
-                                              cudaGraphCondAssignDefault));
+    HCC_CUDA(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+    // An upstream kernel arms the condition on every entry, so a nested
+    // loop re-runs after an earlier pass left its condition at 0 (default
+    // values are only applied at top-level graph launch).
+    k_set_cond<<<1, 1, 0, s()>>>(h, 1u);
+    HCC_CUDA(cudaGetLastError());
+    HCC_CUDA(cudaStreamGetCaptureInfo(s(), &st, nullptr, &g, &deps, &nd));
     cudaGraphNodeParams p = {};
     p.type = cudaGraphNodeTypeConditional;
     p.conditional.handle = h;
@@ -1177,6 +1182,8 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   else
     out.outer_iterations = nrec;
   if (mx) *mx = out;
+  if (hc.err & 2u)
+    return fail(HCC_ECUDA, "device loop exceeded its step cap (runaway loop)");
   if ((o->flags & HCC_FLAG_CHECK_STAR) && hc.flag)
     return fail(HCC_ENOTSTAR, "extract_labels: forest is not star-shaped");
   return HCC_OK;

@@ -3,7 +3,7 @@
 // when a graph handle is created, never inside hcc_cc's timed region.
 #include <cuda_runtime.h>
 
-#include "hcc_gen.h"
+#include "hookcc_gen.h"
 #include "hcc_internal.cuh"
 
 namespace hcc {

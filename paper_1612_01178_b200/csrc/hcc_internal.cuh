@@ -50,7 +50,13 @@ struct DevCtrl {
   u32 cond;          // last loop condition (host-loop mode reads it)
   u32 err;           // sticky device error bits
   u32 flag;          // scratch result flag (is_star / bound checks)
+  u64 loop_steps;    // loop-step kernels executed (runaway guard)
 };
+
+// Device loops stop (and report HCC_ECUDA) after this many steps; the
+// reference's own bound is 4*ceil(log2(n+2))+2 outer iterations
+// (test_engines.cpp:179-187), so this only catches bugs.
+constexpr u64 kMaxLoopSteps = 1ull << 22;
 
 // Source of a hook phase.
 enum HookMode : int {
@@ -97,6 +103,7 @@ __global__ void k_step_outer(DevCtrl* ctrl, DevRec* recs,
                              cudaGraphConditionalHandle h, int use_cond);
 __global__ void k_step_jump(DevCtrl* ctrl, cudaGraphConditionalHandle h,
                             int use_cond);
+__global__ void k_set_cond(cudaGraphConditionalHandle h, u32 value);
 __global__ void k_count_roots(const u32* pi, u64 n, DevCtrl* ctrl);
 __global__ void k_is_star(const u32* pi, u64 n, DevCtrl* ctrl);
 __global__ void k_check_bound(const u32* pi, u64 n, DevCtrl* ctrl);

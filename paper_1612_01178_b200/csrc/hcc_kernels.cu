@@ -397,6 +397,18 @@ __global__ void __launch_bounds__(kVertThreads)
 
 // ---- loop-step kernels (single thread) ------------------------------------
 
+__device__ __forceinline__ u32 guard(DevCtrl* c, u32 cond) {
+  if (++c->loop_steps > kMaxLoopSteps) {
+    c->err |= 2u;
+    return 0u;
+  }
+  return cond;
+}
+
+__global__ void k_set_cond(cudaGraphConditionalHandle h, u32 value) {
+  cudaGraphSetConditional(h, value);
+}
+
 // Worklist pass finished: the output becomes the next input.
 __global__ void k_step_worklist(DevCtrl* c, DevRec* recs,
                                 cudaGraphConditionalHandle h, int use_cond) {
@@ -407,7 +419,7 @@ __global__ void k_step_worklist(DevCtrl* c, DevRec* recs,
   c->passes += 1;
   c->dirty = 0;
   next_rec(c, recs);
-  const u32 cond = produced > 0 ? 1u : 0u;
+  const u32 cond = guard(c, produced > 0 ? 1u : 0u);
   c->cond = cond;
   if (use_cond) cudaGraphSetConditional(h, cond);
 }
@@ -419,7 +431,7 @@ __global__ void k_step_segment(DevCtrl* c, DevRec* recs,
   c->passes += 1;
   c->dirty = 0;
   next_rec(c, recs);
-  const u32 cond = c->seg < c->nseg ? 1u : 0u;
+  const u32 cond = guard(c, c->seg < c->nseg ? 1u : 0u);
   c->cond = cond;
   if (use_cond) cudaGraphSetConditional(h, cond);
 }
@@ -427,7 +439,7 @@ __global__ void k_step_segment(DevCtrl* c, DevRec* recs,
 // Baseline outer iteration finished: loop while some hook changed.
 __global__ void k_step_outer(DevCtrl* c, DevRec* recs,
                              cudaGraphConditionalHandle h, int use_cond) {
-  const u32 cond = c->changed ? 1u : 0u;
+  const u32 cond = guard(c, c->changed ? 1u : 0u);
   c->changed = 0;
   c->passes += 1;
   c->dirty = 0;
@@ -439,7 +451,7 @@ __global__ void k_step_outer(DevCtrl* c, DevRec* recs,
 // Baseline inner jump loop: repeat while a jump changed a slot.
 __global__ void k_step_jump(DevCtrl* c, cudaGraphConditionalHandle h,
                             int use_cond) {
-  const u32 cond = c->jchanged ? 1u : 0u;
+  const u32 cond = guard(c, c->jchanged ? 1u : 0u);
   c->jchanged = 0;
   c->cond = cond;
   if (use_cond) cudaGraphSetConditional(h, cond);

@@ -42,6 +42,7 @@ def parity(ctx):
                     if mt == 1 and algo == "baseline":
                         continue
                     t = time.time()
+                    print(f"# start {name} {algo} {fl} mt={mt}", file=sys.stderr, flush=True)
                     lab, mx = ctx.cc(g, algo, segments=8, max_threads=mt, flags=FLAGS[fl])
                     ok = bool(np.array_equal(lab, want))
                     emit(kind="parity", case=name, algo=algo, flags=fl, max_threads=mt, ok=ok,
