@@ -80,6 +80,9 @@ struct CudaFail {
 constexpr u64 kMaxN = 0xffffffffull;
 // Topology segments unrolled into the root graph (with per-launch events).
 constexpr u64 kMaxUnrolledSegments = 64;
+// Root-walk steps of the atomic-free hook before an unconditional store
+// (HCC_WALK overrides, for tuning).
+constexpr int kDefaultWalk = 32;
 
 int usable_devices() {
   int count = 0;
@@ -108,10 +111,13 @@ struct GraphKey {
   const void* wl0 = nullptr;
   u64 n = 0, m = 0, nseg = 0, max_threads = 0;
   u32 flags = 0;
+  int walk = 0;
+  u64 plan = 0;
   bool operator==(const GraphKey& o) const {
     return algo == o.algo && edges == o.edges && pi == o.pi && wl0 == o.wl0 &&
            n == o.n && m == o.m && nseg == o.nseg &&
-           max_threads == o.max_threads && flags == o.flags;
+           max_threads == o.max_threads && flags == o.flags && walk == o.walk &&
+           plan == o.plan;
   }
 };
 
@@ -306,6 +312,8 @@ struct Plan {
   uint2* wl0;
   uint2* wl1;
   u64 nseg;
+  std::vector<u64> bounds;  // unrolled topology segment boundaries (nseg+1)
+  int walk;
   unsigned grid_hook, block_hook, grid_vert, block_vert;
 };
 
@@ -317,6 +325,7 @@ HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
   a.e = P.m;
   a.mode = mode;
   a.append = append;
+  a.walk = append ? P.walk : 0;  // the literal full-pass loops keep Fig. 2
   a.pi = P.pi;
   a.wl0 = P.wl0;
   a.wl1 = P.wl1;
@@ -373,9 +382,11 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           c->seg_ev.push_back(ev);
         }
         for (u64 sgi = 0; sgi < P.nseg; ++sgi) {
+          HookArgs ha = hook_args(c, P, kSrcRange, 1);
+          ha.b = P.bounds[sgi];
+          ha.e = P.bounds[sgi + 1];
           q.record(c->seg_ev[2 * sgi]);
-          k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(
-              hook_args(c, P, kSrcSegment, 1));
+          k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(ha);
           q.record(c->seg_ev[2 * sgi + 1]);
           q.phase_done(HCC_PHASE_HOOK);
           k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
@@ -968,6 +979,41 @@ uint64_t hcc_choose_segment_count(const hcc_graph_stats* st) {
 
 // ---- the CC engine -----------------------------------------------------------
 
+// partition_edges(m, s) boundaries (engines.hpp:43-58).
+static std::vector<u64> uniform_bounds(u64 m, u64 s) {
+  std::vector<u64> b(s + 1, 0);
+  const u64 q = m / s, r = m % s;
+  for (u64 i = 0; i < s; ++i) b[i + 1] = b[i] + q + (i < r ? 1 : 0);
+  return b;
+}
+
+// Auto plan for the topology pass: a short first segment
+// builds the hub structure while trees are still forming (the expensive,
+// walk-heavy regime), then each boundary grows by `growth` so the bulk of the
+// edges streams in the cheap regime where both endpoints already share a
+// star.  Every segment costs one compress over n, so few segments are used.
+// HCC_PLAN="geo:<k>:<growth>" overrides (first boundary m / 2^k).
+static std::vector<u64> geometric_bounds(u64 m) {
+  int k = 7, growth = 8;
+  if (const char* e = std::getenv("HCC_PLAN")) {
+    int kk = 0, gg = 0;
+    if (std::sscanf(e, "geo:%d:%d", &kk, &gg) == 2 && kk >= 0 && gg >= 2) {
+      k = kk;
+      growth = gg;
+    }
+  }
+  std::vector<u64> b{0};
+  u64 cur = k >= 63 ? 0 : (m >> k);
+  if (cur == 0) cur = std::min<u64>(m, 1);
+  while (cur < m && b.size() < kMaxUnrolledSegments) {
+    if (cur > b.back()) b.push_back(cur);
+    const u64 next = cur * (u64)growth;
+    cur = next / (u64)growth == cur ? next : m;  // overflow guard
+  }
+  if (b.back() != m || b.size() == 1) b.push_back(m);
+  return b;
+}
+
 static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
                   hcc_forest* f, hcc_metrics* mx) {
   const hcc_opts defaults = {HCC_ALGO_BASELINE_MJ, 0, 0, 0, 0, nullptr, nullptr};
@@ -987,6 +1033,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
 
   // segments (engines.hpp:243-247 and partition_edges 43-62)
   u64 requested = 1;
+  bool geo_plan = false;
   if (o->algo == HCC_ALGO_ADAPTIVE) {
     requested = o->segments;
     if (requested == 0) {
@@ -997,16 +1044,17 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   } else if (o->algo == HCC_ALGO_BASELINE_MJ &&
              !(o->flags & HCC_FLAG_FULL_PASSES)) {
     requested = o->first_pass_segments;
-    if (requested == 0) {
-      // cost model: the first segment's hooks all land in
-      // the worklist (m/s records) while every segment costs one compress
-      // over n; s ~ sqrt(m/n) balances the two.
-      double r = n ? std::sqrt((double)m / (double)n) : 1.0;
-      requested = (u64)std::max(1.0, std::floor(r + 0.5));
-    }
+    if (requested == 0) geo_plan = true;
   }
   if (requested < 1) requested = 1;
   u64 nseg = std::max<u64>(1, std::min(requested, std::max<u64>(m, 1)));
+  std::vector<u64> bounds;
+  if (geo_plan) {
+    bounds = geometric_bounds(m);
+    nseg = bounds.size() - 1;
+  } else if (nseg <= kMaxUnrolledSegments) {
+    bounds = uniform_bounds(m, nseg);
+  }
   out.s = nseg;
   out.segments_clamped = requested > m && m > 0;
 
@@ -1037,11 +1085,17 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   P.wl0 = uses_wl ? c->wl[0] : nullptr;
   P.wl1 = uses_wl ? c->wl[1] : nullptr;
   P.nseg = nseg;
+  P.bounds = bounds;
+  {
+    const char* w = std::getenv("HCC_WALK");
+    P.walk = w ? std::atoi(w) : kDefaultWalk;
+  }
   if (o->max_threads == 0) {
     P.block_hook = kHookThreads;
     P.grid_hook = (unsigned)(c->sms * c->occ_hook);
     P.block_vert = kVertThreads;
-    P.grid_vert = grid_for(n, kVertThreads, 0x7fffffffull);
+    // k_compress / k_init_pi take four vertices per thread
+    P.grid_vert = grid_for((n + 3) / 4, kVertThreads, 0x7fffffffull);
   } else {
     u64 t = o->max_threads;
     unsigned blk = (unsigned)std::min<u64>(t, 256);
@@ -1082,6 +1136,8 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   key.nseg = nseg;
   key.max_threads = o->max_threads;
   key.flags = o->flags;
+  key.walk = P.walk;
+  for (u64 x : P.bounds) key.plan = key.plan * 1000003ull + x;
 
   if (graph_mode) {
     if (!(c->exec && c->key == key)) {

@@ -71,6 +71,7 @@ struct HookArgs {
   u64 b, e;
   int mode;
   int append;        // append (H, L) of every write to the next worklist
+  int walk;          // max root-walk steps before a store (0 = Fig. 2 hook)
   u32* pi;
   uint2* wl0;
   uint2* wl1;

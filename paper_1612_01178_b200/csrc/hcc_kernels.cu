@@ -227,6 +227,44 @@ __global__ void __launch_bounds__(kHookThreads) k_hook(HookArgs a) {
   uint2* wl_out = out ? a.wl1 : a.wl0;
   u64* cnt_out = &ctrl->wl_count[out];
 
+  // One-thread launch (max_threads = 1): strictly sequential ascending edge
+  // order with read-after-write between edges, i.e. exactly the reference's
+  // workers = 1 schedule (parallel.hpp:29, 52-55).
+  if (gridDim.x * blockDim.x == 1) {
+    u32 wrote = 0;
+    for (u64 i = b; i < e; ++i) {
+      const uint2 ed = src[i];
+      u32 x = ld_fresh(pi + ed.x), y = ld_fresh(pi + ed.y);
+      if (x == y) continue;
+      u32 h = max(x, y), l = min(x, y);
+      bool store = true;
+      for (int step = 0; step < a.walk; ++step) {
+        const u32 ph = ld_fresh(pi + h);
+        if (ph == h) break;
+        if (ph == l) {
+          store = false;
+          break;
+        }
+        h = max(ph, l);
+        l = min(ph, l);
+      }
+      if (!store) continue;
+      pi[h] = l;
+      wrote = 1;
+      if (a.append) {
+        const u64 pos = atomicAdd(cnt_out, 1ull);
+        wl_out[pos] = make_uint2(h, l);
+        atomicAdd(&r->edges_out, 1ull);
+      }
+    }
+    if (wrote) {
+      ctrl->dirty = 1;
+      if (!a.append) ctrl->changed = 1;
+    }
+    block_t1(&r->hook_t1);
+    return;
+  }
+
   // Head / tail edges that do not fill a 16-byte pair: thread 0 of block 0.
   u64 b2 = b + (b & 1ull);
   if (b2 > e) b2 = e;
@@ -279,11 +317,41 @@ __global__ void __launch_bounds__(kHookThreads) k_hook(HookArgs a) {
       pu[k] = ld_pi(pi + ed[k].x);
       pv[k] = ld_pi(pi + ed[k].y);
     }
+    // Candidates (pu != pv) walk down like Fig. 3's atomic hook, but with a
+    // plain load in place of the CAS: read pi[h]; already linked -> drop;
+    // h still a root -> plain store; otherwise continue from (pi[h], l).
+    // Every value met is a root of the forest at the start of the pass, so
+    // only pass-start roots are ever stored to, and every store is recorded
+    // in the worklist.  After `walk` steps the store is
+    // made regardless (it may overwrite a transient link; the worklist
+    // records it).  This removes the redundant stores that single-level
+    // reads make to hub slots while the hub structure forms.
     u32 act = 0;
 #pragma unroll
     for (int k = 0; k < kHookEPT; ++k) {
-      if (pu[k] != pv[k]) {
-        const u32 h = max(pu[k], pv[k]), l = min(pu[k], pv[k]);
+      if (pu[k] == pv[k]) continue;
+      u32 x = pu[k], y = pv[k];
+      u32 h = max(x, y), l = min(x, y);
+      bool store = true;
+      for (int step = 0; step < a.walk; ++step) {
+        // L1-cached read: any value the slot ever held is a recorded link
+        // (pass-start star link or a worklist pair), so a stale value is a
+        // safe basis for both "drop" and "descend"; reading through L1
+        // keeps the hub slots every edge touches off the L2 slices.
+        const u32 ph = ld_pi(pi + h);
+        if (ph == h) break;             // root: store below
+        if (ph == l) {                  // already linked
+          store = false;
+          break;
+        }
+        h = max(ph, l);
+        l = min(ph, l);
+        if (h == l) {
+          store = false;
+          break;
+        }
+      }
+      if (store) {
         pi[h] = l;
         pu[k] = h;
         pv[k] = l;
@@ -360,15 +428,46 @@ __global__ void __launch_bounds__(kVertThreads)
   block_t0(&r->comp_t0);
   u64 steps = 0;
   const u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 v = (u64)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
-    u32 p = ld_fresh(pi + v);
-    if (p == (u32)v) continue;
-    u32 gp = ld_fresh(pi + p);
-    while (gp != p) {
-      pi[v] = gp;
+  const u64 tid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  // Four consecutive vertices per thread: one 16-byte coalesced read, then
+  // up to four independent parent gathers in flight before any chase.
+  const u64 n4 = n >> 2;
+  const uint4* p4 = reinterpret_cast<const uint4*>(pi);
+  for (u64 q = tid; q < n4; q += stride) {
+    const uint4 pp = __ldcg(p4 + q);
+    const u32 v0 = (u32)(q << 2);
+    u32 p[4] = {pp.x, pp.y, pp.z, pp.w};
+    u32 gp[4];
+#pragma unroll
+    // First parent read through L1: during a compress no root changes and
+    // non-root slots only move to other ancestors, so a stale value is safe
+    // (it just lengthens the chase), while a fresh read would send every
+    // warp to the one L2 sector holding the giant component's root.
+    for (int j = 0; j < 4; ++j) gp[j] = p[j] != v0 + j ? ld_pi(pi + p[j]) : p[j];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      u32 a = p[j], b = gp[j];
+      // parent inside this group: re-read after the earlier chases wrote it
+      // (keeps the one-thread schedule identical to the reference's
+      // sequential ascending pass, forest.hpp:127-136 / parallel.hpp:52-55)
+      if (j > 0 && a >= v0 && a != v0 + j) b = ld_fresh(pi + a);
+      while (b != a) {  // eager writes: every step is visible to other chasers
+        pi[v0 + j] = b;
+        ++steps;
+        a = b;
+        b = ld_fresh(pi + a);
+      }
+    }
+  }
+  for (u64 v = (n4 << 2) + tid; v < n; v += stride) {
+    u32 a = ld_fresh(pi + v);
+    if (a == (u32)v) continue;
+    u32 b = ld_fresh(pi + a);
+    while (b != a) {
+      pi[v] = b;
       ++steps;
-      p = gp;
-      gp = ld_fresh(pi + p);
+      a = b;
+      b = ld_fresh(pi + a);
     }
   }
   add_counter(&r->jump_steps, steps);

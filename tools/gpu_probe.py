@@ -36,8 +36,8 @@ def parity(ctx):
     for name, g in cases.items():
         ed = g.edges()
         want = O.cc(g.n, ed)
-        for algo in ["baseline", "baseline-mj", "atomic", "adaptive"]:
-            for fl in (["default", "full", "hostloop"] if algo == "baseline-mj" else ["default"]):
+        for algo in ["baseline-mj", "adaptive", "atomic", "baseline"]:
+            for fl in (["hostloop", "default", "full"] if algo == "baseline-mj" else ["default"]):
                 for mt in [0, 1] if g.m <= 1 << 20 else [0]:
                     if mt == 1 and algo == "baseline":
                         continue
@@ -85,12 +85,39 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--big", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--specs", default="")
+    ap.add_argument("--segs", default="1,2,4,8")
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--walks", default="")
+    ap.add_argument("--envs", default="", help="';'-separated K=V settings, one sweep each")
     args = ap.parse_args()
     emit(kind="env", devices=capi.device_count())
     ctx = capi.Context(0)
     emit(kind="ctx", sms=ctx.sm_count)
-    parity(ctx)
+    if not args.no_parity:
+        parity(ctx)
     if args.quick:
+        return
+    if args.specs:
+        import os
+        segs = [int(x) for x in args.segs.split(",")]
+        walks = args.walks.split(",") if args.walks else [None]
+        envs = args.envs.split(";") if args.envs else [None]
+        for spec in args.specs.split(";"):
+            for w in walks:
+              for ev in envs:
+                if w is not None:
+                    os.environ["HCC_WALK"] = w
+                    emit(kind="walk", walk=int(w))
+                if ev is not None:
+                    k, v = ev.split("=", 1)
+                    os.environ[k] = v
+                    emit(kind="env", env=ev)
+                timing(ctx, spec, reps=args.reps,
+                       variants=[("baseline-mj", dict(first_pass_segments=s)) for s in segs],
+                       check=not args.no_check)
         return
     timing(ctx, "rmatx:scale=20,ef=16,seed=1")
     timing(ctx, "rmatx:scale=24,ef=16,seed=1")
