@@ -1106,8 +1106,12 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   }
 
   const bool observer = o->observer != nullptr;
-  const bool graph_mode =
-      !observer && !(o->flags & (HCC_FLAG_HOST_LOOP | HCC_FLAG_NO_GRAPH));
+  // HCC_LAUNCH=eager: launch every kernel directly (host-driven loops) so a
+  // profiler that cannot see inside conditional graphs (ncu) lists them.
+  const char* launch_env = std::getenv("HCC_LAUNCH");
+  const bool eager_env = launch_env && std::strcmp(launch_env, "eager") == 0;
+  const bool graph_mode = !observer && !eager_env &&
+                          !(o->flags & (HCC_FLAG_HOST_LOOP | HCC_FLAG_NO_GRAPH));
   out.used_device_loop = graph_mode ? 1 : 0;
 
   Seq q;
