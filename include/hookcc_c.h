@@ -125,6 +125,9 @@ typedef struct hcc_metrics {
   uint64_t edges_processed; /* edge records streamed by hook kernels       */
   uint64_t records;         /* per-phase records available (hcc_ctx_segments)*/
   int used_device_loop;     /* 1 = CUDA-graph conditional loop             */
+  uint64_t kernels;         /* kernels this run launched (pi init through
+                               convergence)                                */
+  int star0_bitmap;         /* 1 = the star-0 bitmap fast path was used    */
 } hcc_metrics;
 
 /* One record per segment / outer iteration / worklist pass

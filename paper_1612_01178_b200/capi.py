@@ -43,7 +43,7 @@ class Metrics(C.Structure):
                 ("s", u64), ("segments_clamped", i32), ("outer_iterations", u64),
                 ("counters", Counters), ("components", u64), ("n", u64), ("m", u64),
                 ("passes", u64), ("edges_processed", u64), ("records", u64),
-                ("used_device_loop", i32)]
+                ("used_device_loop", i32), ("kernels", u64), ("star0_bitmap", i32)]
 
 
 class SegmentRec(C.Structure):
@@ -248,7 +248,8 @@ def metrics_dict(mx: Metrics) -> dict:
                 cas_failures=mx.counters.cas_failures, jump_steps=mx.counters.jump_steps,
                 components=mx.components, n=mx.n, m=mx.m, passes=mx.passes,
                 edges_processed=mx.edges_processed, records=mx.records,
-                used_device_loop=bool(mx.used_device_loop))
+                used_device_loop=bool(mx.used_device_loop), kernels=mx.kernels,
+                star0_bitmap=bool(mx.star0_bitmap))
 
 
 class Graph:

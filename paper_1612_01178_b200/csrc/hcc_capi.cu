@@ -113,11 +113,12 @@ struct GraphKey {
   u32 flags = 0;
   int walk = 0;
   u64 plan = 0;
+  bool s0b = false;
   bool operator==(const GraphKey& o) const {
     return algo == o.algo && edges == o.edges && pi == o.pi && wl0 == o.wl0 &&
            n == o.n && m == o.m && nseg == o.nseg &&
            max_threads == o.max_threads && flags == o.flags && walk == o.walk &&
-           plan == o.plan;
+           plan == o.plan && s0b == o.s0b;
   }
 };
 
@@ -143,6 +144,8 @@ struct hcc_ctx {
   std::vector<cudaEvent_t> seg_ev;   // 2 per segment
   u64 seg_ev_used = 0;
   u64 exec_seg_ev = 0;  // seg_ev_used of the cached executable graph
+  u32* s0b = nullptr;  // star-0 bitmap
+  u64 s0b_words = 0;
   // multi-GPU
   void* comm = nullptr;
   int world = 1, rank = 0;
@@ -212,6 +215,15 @@ void ensure_wl(hcc_ctx* c, u64 cap) {
   c->wl_cap = 0;
   for (int i = 0; i < 2; ++i) HCC_CUDA(cudaMalloc(&c->wl[i], cap * sizeof(uint2)));
   c->wl_cap = cap;
+}
+
+void ensure_s0b(hcc_ctx* c, u64 nwords) {
+  if (c->s0b_words >= nwords) return;
+  if (c->s0b) HCC_CUDA(cudaFree(c->s0b));
+  c->s0b = nullptr;
+  c->s0b_words = 0;
+  HCC_CUDA(cudaMalloc(&c->s0b, std::max<u64>(nwords, 1) * sizeof(u32)));
+  c->s0b_words = nwords;
 }
 
 void drop_exec(hcc_ctx* c) {
@@ -314,6 +326,7 @@ struct Plan {
   u64 nseg;
   std::vector<u64> bounds;  // unrolled topology segment boundaries (nseg+1)
   int walk;
+  bool s0b;                 // star-0 bitmap for hook passes after a compress
   unsigned grid_hook, block_hook, grid_vert, block_vert;
 };
 
@@ -326,6 +339,7 @@ HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
   a.mode = mode;
   a.append = append;
   a.walk = append ? P.walk : 0;  // the literal full-pass loops keep Fig. 2
+  a.s0b = nullptr;
   a.pi = P.pi;
   a.wl0 = P.wl0;
   a.wl1 = P.wl1;
@@ -338,7 +352,8 @@ HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
 void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
   c->seg_ev_used = 0;
   k_begin<<<1, 1, 0, q.s()>>>(c->d_ctrl, c->d_recs, P.nseg);
-  k_init_pi<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n);
+  k_init_pi<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n,
+                                                      P.s0b ? c->s0b : nullptr);
   HCC_CUDA(cudaGetLastError());
   DevCtrl* ctrl = c->d_ctrl;
   DevRec* recs = c->d_recs;
@@ -385,12 +400,25 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           HookArgs ha = hook_args(c, P, kSrcRange, 1);
           ha.b = P.bounds[sgi];
           ha.e = P.bounds[sgi + 1];
+          if (P.s0b && sgi >= 1) ha.s0b = c->s0b;
           q.record(c->seg_ev[2 * sgi]);
-          k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(ha);
+          const u64 seg_edges = ha.e - ha.b;
+          if (P.block_hook == kHookThreads &&
+              seg_edges < (u64)P.grid_hook * kHookThreads * kHookEPT * 2) {
+            // forming-regime segment: EPT 2 over a full grid
+            k_hook_small<<<grid_for((seg_edges + 1) / 2 + 1, kHookThreads, 0x7fffffffull),
+                           kHookThreads, 0, q.s()>>>(ha);
+          } else {
+            k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(ha);
+          }
           q.record(c->seg_ev[2 * sgi + 1]);
           q.phase_done(HCC_PHASE_HOOK);
-          k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
-                                                              recs, 1);
+          if (P.s0b)  // compress + star-0 bitmap (bitmap initialised by k_init_pi)
+            k_compress_s0b<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
+                                                                    recs, c->s0b, 1);
+          else
+            k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
+                                                                recs, 1);
           q.phase_done(HCC_PHASE_COMPRESS);
           k_step_segment<<<1, 1, 0, q.s()>>>(ctrl, recs, 0, 0);
         }
@@ -408,11 +436,16 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
       }
       // data-driven passes over the compacted worklist
       q.loop([&](cudaGraphConditionalHandle h, int u) {
-        k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(
-            hook_args(c, P, kSrcWorklist, 1));
+        HookArgs wa = hook_args(c, P, kSrcWorklist, 1);
+        if (P.s0b && !P.bounds.empty()) wa.s0b = c->s0b;
+        k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(wa);
         q.phase_done(HCC_PHASE_HOOK);
-        k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
-                                                            recs, 1);
+        if (P.s0b && !P.bounds.empty())
+          k_compress_s0b<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
+                                                                  recs, c->s0b, 1);
+        else
+          k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
+                                                              recs, 1);
         q.phase_done(HCC_PHASE_COMPRESS);
         k_step_worklist<<<1, 1, 0, q.s()>>>(ctrl, recs, h, u);
       });
@@ -639,6 +672,7 @@ int hcc_destroy(hcc_ctx* c) {
   cudaFree(c->scratch_pi);
   cudaFree(c->wl[0]);
   cudaFree(c->wl[1]);
+  cudaFree(c->s0b);
   for (cudaEvent_t ev : c->seg_ev) cudaEventDestroy(ev);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -1074,6 +1108,8 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   const bool uses_wl =
       o->algo == HCC_ALGO_BASELINE_MJ && !(o->flags & HCC_FLAG_FULL_PASSES);
   if (uses_wl) ensure_wl(c, m);
+  bool s0b = uses_wl && o->max_threads == 0 && n >= (1ull << 16);
+  if (const char* e = std::getenv("HCC_S0B")) s0b = s0b && std::atoi(e) != 0;
 
   Plan P;
   P.algo = o->algo;
@@ -1086,6 +1122,8 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   P.wl1 = uses_wl ? c->wl[1] : nullptr;
   P.nseg = nseg;
   P.bounds = bounds;
+  P.s0b = s0b && !bounds.empty();
+  if (P.s0b) ensure_s0b(c, (n + 31) / 32);
   {
     const char* w = std::getenv("HCC_WALK");
     P.walk = w ? std::atoi(w) : kDefaultWalk;
@@ -1094,7 +1132,11 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
     P.block_hook = kHookThreads;
     P.grid_hook = (unsigned)(c->sms * c->occ_hook);
     P.block_vert = kVertThreads;
-    // k_compress / k_init_pi take four vertices per thread
+    // k_compress / k_init_pi take four vertices per thread.  The grid covers
+    // n exactly: blocks start in ascending order and a new block starts as
+    // soon as any finishes, so the compress front stays ascending even when
+    // some chases are long (a persistent grid-stride loop lets fast blocks
+    // overtake stalled ancestors: grid 4096^2 compress went 0.5 -> 28 ms).
     P.grid_vert = grid_for((n + 3) / 4, kVertThreads, 0x7fffffffull);
   } else {
     u64 t = o->max_threads;
@@ -1141,6 +1183,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   key.max_threads = o->max_threads;
   key.flags = o->flags;
   key.walk = P.walk;
+  key.s0b = P.s0b;
   for (u64 x : P.bounds) key.plan = key.plan * 1000003ull + x;
 
   if (graph_mode) {
@@ -1234,6 +1277,19 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
     out.counters.hook_traversal_steps += r.traversal;
     out.counters.cas_failures += r.cas_fail;
     out.counters.jump_steps += r.jump_steps;
+  }
+  out.star0_bitmap = P.s0b ? 1 : 0;
+  {
+    // kernels launched by the run (loop iterations from the device records)
+    const u64 iters = nrec;
+    u64 k = 2;  // k_begin, k_init_pi
+    if (o->algo == HCC_ALGO_BASELINE_MJ && !P.full_passes && !P.bounds.empty()) {
+      const u64 wl = nrec > nseg ? nrec - nseg : 0;
+      k += 3 * nseg + 1 + 3 * wl;  // hook+compress+step; k_set_cond; wl passes
+    } else {
+      k += 1 + 3 * iters;  // k_set_cond + hook/compress(or jump)/step per record
+    }
+    out.kernels = k;
   }
   if (o->algo == HCC_ALGO_BASELINE_MJ && !P.full_passes)
     out.outer_iterations = 1 + (nrec > nseg ? nrec - nseg : 0);
@@ -1331,7 +1387,7 @@ int hcc_forest_reset(hcc_forest* f) {
   HCC_CUDA(cudaSetDevice(f->dev));
   if (f->n) {
     k_init_pi<<<grid_for(f->n, 256, 65536), 256, 0, cudaStreamPerThread>>>(
-        f->d_pi, f->n);
+        f->d_pi, f->n, nullptr);
     HCC_CUDA(cudaGetLastError());
   }
   HCC_CUDA(cudaStreamSynchronize(cudaStreamPerThread));

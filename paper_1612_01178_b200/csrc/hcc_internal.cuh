@@ -72,6 +72,8 @@ struct HookArgs {
   int mode;
   int append;        // append (H, L) of every write to the next worklist
   int walk;          // max root-walk steps before a store (0 = Fig. 2 hook)
+  const u32* s0b;    // star-0 bitmap (bit v = pi(v) == 0 after the last
+                     // compress), or null
   u32* pi;
   uint2* wl0;
   uint2* wl1;
@@ -90,11 +92,14 @@ struct Launch {
 
 // ---- kernels (hcc_kernels.cu) -------------------------------------------
 __global__ void k_begin(DevCtrl* ctrl, DevRec* recs, u64 nseg);
-__global__ void k_init_pi(u32* pi, u64 n);
+__global__ void k_init_pi(u32* pi, u64 n, u32* bits);
 __global__ void k_hook(HookArgs a);
+__global__ void k_hook_small(HookArgs a);
 __global__ void k_cas_hook(HookArgs a);
 __global__ void k_compress(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
                            int skip_if_clean);
+__global__ void k_compress_s0b(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
+                               u32* bits, int skip_if_clean);
 __global__ void k_jump(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs);
 __global__ void k_step_worklist(DevCtrl* ctrl, DevRec* recs,
                                 cudaGraphConditionalHandle h, int use_cond);

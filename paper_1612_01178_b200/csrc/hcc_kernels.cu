@@ -84,13 +84,20 @@ __device__ __forceinline__ void next_rec(DevCtrl* c, DevRec* recs) {
   }
 }
 
+// Phase spans: sampled blocks only (every 32nd block plus the last 32), so
+// a kernel with tens of thousands of blocks does not serialize on two L2
+// atomics per block.  Block 0 starts first and the tail blocks finish last.
+__device__ __forceinline__ bool timer_block() {
+  return (blockIdx.x & 31u) == 0 || blockIdx.x + 32u >= gridDim.x;
+}
+
 __device__ __forceinline__ void block_t0(u64* t0) {
-  if (threadIdx.x == 0) atomicMin(t0, gtime());
+  if (threadIdx.x == 0 && timer_block()) atomicMin(t0, gtime());
 }
 
 __device__ __forceinline__ void block_t1(u64* t1) {
   __syncthreads();
-  if (threadIdx.x == 0) atomicMax(t1, gtime());
+  if (threadIdx.x == 0 && timer_block()) atomicMax(t1, gtime());
 }
 
 // Adds a per-thread counter into a global u64.  Must be reached by every
@@ -196,10 +203,13 @@ __global__ void k_begin(DevCtrl* ctrl, DevRec* recs, u64 nseg) {
   }
 }
 
-// pi(v) = v (ParentForest::reset, forest.hpp:25-28), 16-byte stores.
-__global__ void k_init_pi(u32* pi, u64 n) {
+// pi(v) = v (ParentForest::reset, forest.hpp:25-28), 16-byte stores.  With
+// a star-0 bitmap, also its initial state (only vertex 0 is in star 0).
+__global__ void k_init_pi(u32* pi, u64 n, u32* bits) {
   const u64 tid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   const u64 stride = (u64)gridDim.x * blockDim.x;
+  if (bits)
+    for (u64 w = tid; w < ((n + 31) >> 5); w += stride) bits[w] = w == 0 ? 1u : 0u;
   const u64 n4 = n >> 2;
   uint4* p4 = reinterpret_cast<uint4*>(pi);
   for (u64 i = tid; i < n4; i += stride) {
@@ -210,8 +220,11 @@ __global__ void k_init_pi(u32* pi, u64 n) {
 }
 
 // Atomic-free Hook (forest.hpp:83-89) over an edge range, a segment or the
-// current worklist.  See the file comment for the design.
-__global__ void __launch_bounds__(kHookThreads) k_hook(HookArgs a) {
+// current worklist.  See the file comment for the design.  EPT edges per
+// thread per tile; the next tile's edge loads are issued before the current
+// tile's dependent gathers (software pipelining).
+template <int EPT>
+__device__ __forceinline__ void hook_impl(const HookArgs& a) {
   const uint2* src;
   u64 b, e;
   u32 out;
@@ -294,28 +307,47 @@ __global__ void __launch_bounds__(kHookThreads) k_hook(HookArgs a) {
 
   const uint4* s4 = reinterpret_cast<const uint4*>(src + b2);
   const u64 pol = policy_evict_first();
-  const u64 tile = (u64)blockDim.x * (kHookEPT / 2);
+  const u64 tile = (u64)blockDim.x * (EPT / 2);
   const u64 ntiles = (n4 + tile - 1) / tile;
-  for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    uint2 ed[kHookEPT];
+  // Out-of-range slots become the self-loop (0,0): a no-op hook.
+  auto load_tile = [&](u64 t, uint4* q) {
 #pragma unroll
-    for (int j = 0; j < kHookEPT / 2; ++j) {
+    for (int j = 0; j < EPT / 2; ++j) {
       const u64 i = t * tile + (u64)j * blockDim.x + threadIdx.x;
-      if (i < n4) {
-        uint4 q = ld_stream16(s4 + i, pol);
-        ed[2 * j] = make_uint2(q.x, q.y);
-        ed[2 * j + 1] = make_uint2(q.z, q.w);
-      } else {
-        // Out-of-range slots become the self-loop (0,0): a no-op hook.
-        ed[2 * j] = make_uint2(0u, 0u);
-        ed[2 * j + 1] = make_uint2(0u, 0u);
-      }
+      q[j] = i < n4 ? ld_stream16(s4 + i, pol) : make_uint4(0u, 0u, 0u, 0u);
     }
-    u32 pu[kHookEPT], pv[kHookEPT];
+  };
+  uint4 nq[EPT / 2];
+  if ((u64)blockIdx.x < ntiles) load_tile(blockIdx.x, nq);
+  for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    uint2 ed[EPT];
 #pragma unroll
-    for (int k = 0; k < kHookEPT; ++k) {
-      pu[k] = ld_pi(pi + ed[k].x);
-      pv[k] = ld_pi(pi + ed[k].y);
+    for (int j = 0; j < EPT / 2; ++j) {
+      ed[2 * j] = make_uint2(nq[j].x, nq[j].y);
+      ed[2 * j + 1] = make_uint2(nq[j].z, nq[j].w);
+    }
+    if (t + gridDim.x < ntiles) load_tile(t + gridDim.x, nq);
+    u32 pu[EPT], pv[EPT];
+    if (a.s0b) {
+      // Star-0 bitmap: one L1-friendly word read answers pi(x) == 0 for
+      // the giant component's vertices; only the rest gather pi.
+      u32 wu[EPT], wv[EPT];
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        wu[k] = ld_pi(a.s0b + (ed[k].x >> 5));
+        wv[k] = ld_pi(a.s0b + (ed[k].y >> 5));
+      }
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        pu[k] = (wu[k] >> (ed[k].x & 31u)) & 1u ? 0u : ld_pi(pi + ed[k].x);
+        pv[k] = (wv[k] >> (ed[k].y & 31u)) & 1u ? 0u : ld_pi(pi + ed[k].y);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        pu[k] = ld_pi(pi + ed[k].x);
+        pv[k] = ld_pi(pi + ed[k].y);
+      }
     }
     // Candidates (pu != pv) walk down like Fig. 3's atomic hook, but with a
     // plain load in place of the CAS: read pi[h]; already linked -> drop;
@@ -328,7 +360,7 @@ __global__ void __launch_bounds__(kHookThreads) k_hook(HookArgs a) {
     // reads make to hub slots while the hub structure forms.
     u32 act = 0;
 #pragma unroll
-    for (int k = 0; k < kHookEPT; ++k) {
+    for (int k = 0; k < EPT; ++k) {
       if (pu[k] == pv[k]) continue;
       u32 x = pu[k], y = pv[k];
       u32 h = max(x, y), l = min(x, y);
@@ -362,7 +394,7 @@ __global__ void __launch_bounds__(kHookThreads) k_hook(HookArgs a) {
       u64 pos;
       if (block_reserve(__popc(act), cnt_out, r, ctrl, pos)) {
 #pragma unroll
-        for (int k = 0; k < kHookEPT; ++k)
+        for (int k = 0; k < EPT; ++k)
           if (act & (1u << k)) wl_out[pos++] = make_uint2(pu[k], pv[k]);
       }
     } else {
@@ -376,6 +408,17 @@ __global__ void __launch_bounds__(kHookThreads) k_hook(HookArgs a) {
     }
   }
   block_t1(&r->hook_t1);
+}
+
+__global__ void __launch_bounds__(kHookThreads, 4) k_hook(HookArgs a) {
+  hook_impl<kHookEPT>(a);
+}
+
+// Small segments (the forming regime): two edges per thread, one tile per
+// block over a full grid, so long root walks run side by side instead of
+// eight deep per thread.
+__global__ void __launch_bounds__(kHookThreads) k_hook_small(HookArgs a) {
+  hook_impl<2>(a);
 }
 
 // CAS-verified hook (forest.hpp:107-122): walks down until it acquires a
@@ -470,6 +513,64 @@ __global__ void __launch_bounds__(kVertThreads)
       b = ld_fresh(pi + a);
     }
   }
+  add_counter(&r->jump_steps, steps);
+  block_t1(&r->comp_t1);
+}
+
+// Multi-Jump compress fused with the star-0 bitmap build (HC engine, full
+// grid): thread q owns vertices [4q, 4q+4); after the chases every thread
+// knows its vertices' roots, so bit v = (root(v) == 0) is assembled with
+// three warp shuffles (8 lanes = one 32-vertex word) and stored once.
+__global__ void __launch_bounds__(kVertThreads)
+    k_compress_s0b(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs, u32* bits,
+                   int skip_if_clean) {
+  if (skip_if_clean && *(volatile u32*)&ctrl->dirty == 0) return;
+  DevRec* r = cur_rec(ctrl, recs);
+  block_t0(&r->comp_t0);
+  u64 steps = 0;
+  const u64 q = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 v0 = q << 2;
+  u32 nib = 0;
+  if (v0 + 4 <= n) {
+    const uint4 pp = __ldcg(reinterpret_cast<const uint4*>(pi) + q);
+    u32 p[4] = {pp.x, pp.y, pp.z, pp.w};
+    u32 gp[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) gp[j] = p[j] != (u32)v0 + j ? ld_pi(pi + p[j]) : p[j];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      u32 a = p[j], b = gp[j];
+      if (j > 0 && a >= (u32)v0 && a != (u32)v0 + j) b = ld_fresh(pi + a);
+      while (b != a) {
+        pi[v0 + j] = b;
+        ++steps;
+        a = b;
+        b = ld_fresh(pi + a);
+      }
+      nib |= (a == 0u) ? 1u << j : 0u;
+    }
+  } else if (v0 < n) {
+    for (u64 v = v0; v < n; ++v) {
+      u32 a = ld_fresh(pi + v);
+      if (a != (u32)v) {
+        u32 b = ld_fresh(pi + a);
+        while (b != a) {
+          pi[v] = b;
+          ++steps;
+          a = b;
+          b = ld_fresh(pi + a);
+        }
+      }
+      nib |= (a == 0u) ? 1u << (u32)(v - v0) : 0u;
+    }
+  }
+  const u32 lane = threadIdx.x & 31u;
+  u32 w = nib << (4u * (lane & 7u));
+  w |= __shfl_xor_sync(0xffffffffu, w, 1);
+  w |= __shfl_xor_sync(0xffffffffu, w, 2);
+  w |= __shfl_xor_sync(0xffffffffu, w, 4);
+  const u64 word = (v0 >> 5);  // lanes 8i..8i+7 share word (v0 of lane 8i) >> 5
+  if ((lane & 7u) == 0 && v0 < n) bits[word] = w;
   add_counter(&r->jump_steps, steps);
   block_t1(&r->comp_t1);
 }

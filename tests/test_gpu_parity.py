@@ -456,3 +456,23 @@ def test_in_place_forest(ctx, oracle):  # *_cc_into contract (engines.hpp:183-23
         lab, _ = ctx.cc(g, algo, forest=f)
         assert np.array_equal(f.snapshot(), oracle.cc(n, e))
         assert f.is_star()
+
+
+@pytest.mark.parametrize("spec", ["rmatx:scale=20,ef=16,seed=7", "erx:n=1100000,m=9000000,seed=3",
+                                  "erx:n=1048579,m=8000000,seed=5", "erx:n=70001,m=40000,seed=9",
+                                  "grid:1100x1000"])
+def test_star0_bitmap_paths(ctx, oracle, spec):
+    """The star-0 bitmap fast path (n >= 2^16) and the plain gather path give
+    identical labels under every topology plan."""
+    import os
+    g = ctx.generate(spec)
+    want = oracle.cc(g.n, g.edges())
+    for s0b in ["1", "0"]:
+        os.environ["HCC_S0B"] = s0b
+        try:
+            for fps in [0, 1, 3]:
+                lab, mx = ctx.cc(g, "baseline-mj", first_pass_segments=fps)
+                assert np.array_equal(lab, want), (spec, s0b, fps)
+                assert mx["star0_bitmap"] == (s0b == "1")
+        finally:
+            os.environ.pop("HCC_S0B", None)

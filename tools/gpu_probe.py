@@ -112,8 +112,9 @@ def main():
                     os.environ["HCC_WALK"] = w
                     emit(kind="walk", walk=int(w))
                 if ev is not None:
-                    k, v = ev.split("=", 1)
-                    os.environ[k] = v
+                    for kv in ev.split(","):
+                        k, v = kv.split("=", 1)
+                        os.environ[k] = v
                     emit(kind="env", env=ev)
                 timing(ctx, spec, reps=args.reps,
                        variants=[("baseline-mj", dict(first_pass_segments=s)) for s in segs],
