@@ -1,0 +1,53 @@
+"""The reference's OWN test sources, compiled unchanged against this repo's
+headers and run on the B200.
+
+`make reftests` (run by __graft_entry__.build where /root/reference exists)
+compiles /root/reference/proj/tests/test_*.cpp with a Catch2 shim
+(tests/cpp/shim) into tests/cpp/_bin/unit_tests, and acceptance.cpp into
+tests/cpp/_bin/acceptance.  The binaries travel to the GPU box with the repo.
+
+Reference status for comparison (proj/test_output.txt:1-34): unit_tests pass;
+acceptance passes every criterion except 5, whose expectation (k = 1000
+ascending jump steps) contradicts the reference's own unit test
+(test_forest.cpp:159, k - 1 = 999).  The B200 build reproduces exactly that:
+999 steps, so criterion 5 fails with the reference's own message.
+"""
+from __future__ import annotations
+
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+BIN = Path(__file__).resolve().parent / "cpp" / "_bin"
+
+pytestmark = pytest.mark.gpu
+
+
+def _need(name: str) -> Path:
+    p = BIN / name
+    if not p.exists():
+        pytest.skip(f"{p} not built (make reftests needs /root/reference at build time)")
+    return p
+
+
+def test_reference_unit_tests_pass_on_b200(ctx):
+    exe = _need("unit_tests")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    m = re.search(r"(\d+) test cases, 0 failed", r.stdout)
+    assert m and int(m.group(1)) >= 70
+
+
+def test_reference_acceptance_on_b200(ctx):
+    exe = _need("acceptance")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=1800)
+    lines = {int(m.group(1)): m.group(2)
+             for m in re.finditer(r"\[criterion (\d+)\] (PASS|FAIL)", r.stdout)}
+    assert sorted(lines) == list(range(1, 9)), r.stdout
+    for c in (1, 2, 3, 4, 6, 7, 8):
+        assert lines[c] == "PASS", (c, r.stdout)
+    # criterion 5: the reference's own test bug, reproduced bit-for-bit
+    assert lines[5] == "FAIL"
+    assert "ascending pass recorded 999 jump steps, expected exactly 1000" in r.stdout
