@@ -241,19 +241,26 @@ int hcc_forest_is_star(hcc_forest* f, int* out);           /* 140-146 */
 /* max over v of (pi(v) > v): the bound invariant (SPEC: pi(v) <= v). */
 int hcc_forest_check_bound(hcc_forest* f, int* ok);
 
-/* ---- multi-GPU edge-partitioned CC (north-star (5)) ----------
- * One process per GPU. Rank r runs the local CC on its shard of the edge
- * list (partition_edges(m, world) semantics, engines.hpp:43-58), then the
- * forests are merged over NVLink with NCCL and re-hooked as
- * (v, pi_remote(v)) pairs until global convergence. */
-int hcc_nccl_unique_id_size(void);
-int hcc_nccl_get_unique_id(void* id_out);
-int hcc_comm_init(hcc_ctx* ctx, int world, int rank, const void* id);
-int hcc_comm_destroy(hcc_ctx* ctx);
-/* Shard [first, first+count) of a host edge array, uploaded as a graph. */
-int hcc_cc_distributed(hcc_ctx* ctx, const hcc_graph* shard, uint64_t n,
-                       const hcc_opts* opts, uint32_t* labels_out,
-                       hcc_metrics* out);
+/* ---- multi-GPU merge primitives (north-star (5), SURVEY 8e shape 3) ------
+ * After a local CC on an edge shard, a rank exports its star forest as
+ *   bits  : uint32[ceil(n/32)], bit v = (pi(v) == 0 && v != 0)
+ *   pairs : uint32[2*cap], (v, pi(v)) for every v with pi(v) not in {v, 0}
+ * into DEVICE buffers (e.g. torch CUDA tensors), so the payload goes to NCCL
+ * without a host hop.  After the exchange, hcc_rehook re-hooks the OR of
+ * the remote bitmaps (as (v, 0) edges) and the concatenated remote pairs as
+ * edges into the local forest with the worklist engine, until convergence.
+ * The union of all shards' relations is then in every rank's forest, so the
+ * labels are the global min-canonical labels. */
+int hcc_forest_export(hcc_ctx* ctx, hcc_forest* f, uint32_t* dev_bits,
+                      uint32_t* dev_pairs, uint64_t cap, uint64_t* count);
+/* dev_bits_or may be NULL; dev_pairs holds `count` (v, parent) u32 pairs. */
+int hcc_rehook(hcc_ctx* ctx, hcc_forest* f, const uint32_t* dev_bits_or,
+               const uint32_t* dev_pairs, uint64_t count, hcc_metrics* out);
+/* Device generator of one shard: edges [first, first+count) of `spec`
+ * (partition_edges(m, world) gives the rank's range). */
+int hcc_graph_generate_range(hcc_ctx* ctx, const char* spec,
+                             uint64_t default_seed, uint64_t first,
+                             uint64_t count, hcc_graph** out);
 
 #ifdef __cplusplus
 }  /* extern "C" */

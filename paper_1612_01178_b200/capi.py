@@ -102,11 +102,9 @@ _SIGS = {
     "hcc_forest_multi_jump_range": (i32, [vp, u64, u64, i32, C.POINTER(Counters)]),
     "hcc_forest_is_star": (i32, [vp, C.POINTER(i32)]),
     "hcc_forest_check_bound": (i32, [vp, C.POINTER(i32)]),
-    "hcc_nccl_unique_id_size": (i32, []),
-    "hcc_nccl_get_unique_id": (i32, [vp]),
-    "hcc_comm_init": (i32, [vp, i32, i32, vp]),
-    "hcc_comm_destroy": (i32, [vp]),
-    "hcc_cc_distributed": (i32, [vp, vp, u64, C.POINTER(Opts), vp, C.POINTER(Metrics)]),
+    "hcc_forest_export": (i32, [vp, vp, vp, vp, u64, C.POINTER(u64)]),
+    "hcc_rehook": (i32, [vp, vp, vp, vp, u64, C.POINTER(Metrics)]),
+    "hcc_graph_generate_range": (i32, [vp, C.c_char_p, u64, u64, u64, C.POINTER(vp)]),
 }
 
 
@@ -212,6 +210,26 @@ class Context:
         h = vp()
         check(lib().hcc_graph_generate(self.h, spec.encode(), default_seed, C.byref(h)))
         return Graph(self, h)
+
+    def generate_range(self, spec: str, first: int, count: int, default_seed: int = 1) -> "Graph":
+        """Edges [first, first+count) of a device generator spec (one shard)."""
+        h = vp()
+        check(lib().hcc_graph_generate_range(self.h, spec.encode(), default_seed, first, count,
+                                             C.byref(h)))
+        return Graph(self, h)
+
+    def export(self, forest: "Forest", dev_bits: int, dev_pairs: int, cap: int) -> int:
+        """hcc_forest_export into caller device buffers; returns the pair count
+        (may exceed cap: then retry with a larger buffer)."""
+        cnt = u64()
+        check(lib().hcc_forest_export(self.h, forest.h, dev_bits, dev_pairs, cap, C.byref(cnt)))
+        return cnt.value
+
+    def rehook(self, forest: "Forest", dev_bits_or: int | None, dev_pairs: int | None,
+               count: int) -> dict:
+        mx = Metrics()
+        check(lib().hcc_rehook(self.h, forest.h, dev_bits_or, dev_pairs, count, C.byref(mx)))
+        return metrics_dict(mx)
 
     def forest(self, n: int) -> "Forest":
         h = vp()

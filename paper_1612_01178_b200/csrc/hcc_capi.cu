@@ -854,8 +854,8 @@ int hcc_graph_from_csr(hcc_ctx* c, const uint64_t* row_ptr, const uint32_t* col,
   }
 }
 
-int hcc_graph_generate(hcc_ctx* c, const char* spec_c, uint64_t default_seed,
-                       hcc_graph** out) {
+static int generate_impl(hcc_ctx* c, const char* spec_c, uint64_t default_seed,
+                         bool ranged, u64 first, u64 count, hcc_graph** out) {
   if (!out || !spec_c) return fail(HCC_EINVAL, "null argument");
   *out = nullptr;
   if (int r = ctx_enter(c)) return r;
@@ -904,22 +904,29 @@ int hcc_graph_generate(hcc_ctx* c, const char* spec_c, uint64_t default_seed,
     return fail(HCC_EINVAL, "vertex count >= 2^32");
   if (kind == "rmatx" && n > kMaxN)
     return fail(HCC_EINVAL, "rmatx: scale 32 needs 2^32 vertices (> u32)");
+  if (ranged) {
+    if (first > m || count > m - first)
+      return fail(HCC_EINVAL, "generator range out of bounds");
+  } else {
+    first = 0;
+    count = m;
+  }
   hcc_graph* g = new hcc_graph;
   g->ctx = c;
   g->n = n;
-  g->m = m;
+  g->m = count;
   HCC_GUARD_BEGIN
-  HCC_CUDA(cudaMalloc(&g->d_edges, std::max<u64>(m, 2) * sizeof(uint2)));
-  if (m > 0) {
-    unsigned grid = grid_for(m, 256, (u64)c->sms * 32);
+  HCC_CUDA(cudaMalloc(&g->d_edges, std::max<u64>(count, 2) * sizeof(uint2)));
+  if (count > 0) {
+    unsigned grid = grid_for(count, 256, (u64)c->sms * 32);
     if (kind == "grid") {
-      k_gen_grid<<<grid, 256, 0, c->stream>>>(g->d_edges, rows, cols);
+      k_gen_grid<<<grid, 256, 0, c->stream>>>(g->d_edges, rows, cols, first, count);
     } else if (kind == "rmatx") {
       k_gen_rmatx<<<grid, 256, 0, c->stream>>>(
-          g->d_edges, 0, m, (u32)scale, seed, prob_threshold(a),
+          g->d_edges, first, count, (u32)scale, seed, prob_threshold(a),
           prob_threshold(a + b), prob_threshold(a + b + cc));
     } else {
-      k_gen_erx<<<grid, 256, 0, c->stream>>>(g->d_edges, 0, m, n, seed);
+      k_gen_erx<<<grid, 256, 0, c->stream>>>(g->d_edges, first, count, n, seed);
     }
     HCC_CUDA(cudaGetLastError());
   }
@@ -931,6 +938,16 @@ int hcc_graph_generate(hcc_ctx* c, const char* spec_c, uint64_t default_seed,
     hcc_graph_free(g);
     return f.code;
   }
+}
+
+int hcc_graph_generate(hcc_ctx* c, const char* spec, uint64_t default_seed,
+                       hcc_graph** out) {
+  return generate_impl(c, spec, default_seed, false, 0, 0, out);
+}
+
+int hcc_graph_generate_range(hcc_ctx* c, const char* spec, uint64_t default_seed,
+                             uint64_t first, uint64_t count, hcc_graph** out) {
+  return generate_impl(c, spec, default_seed, true, first, count, out);
 }
 
 int hcc_graph_info(const hcc_graph* g, uint64_t* n, uint64_t* m) {
@@ -1582,6 +1599,97 @@ int hcc_forest_check_bound(hcc_forest* f, int* ok) {
   return forest_flag_kernel(f, false, ok);
 }
 
-// ---- multi-GPU (implemented in hcc_multi.cu when NCCL is linked) -------------
+// ---- multi-GPU merge primitives (kernels in hcc_multi.cu) ---------------------
+
+int hcc_forest_export(hcc_ctx* c, hcc_forest* f, uint32_t* dev_bits,
+                      uint32_t* dev_pairs, uint64_t cap, uint64_t* count) {
+  if (!f || !count || (!dev_bits && f->n)) return fail(HCC_EINVAL, "null argument");
+  if (cap && !dev_pairs) return fail(HCC_EINVAL, "null pair buffer");
+  if (int r = ctx_enter(c)) return r;
+  HCC_GUARD_BEGIN
+  u64* d_cnt = reinterpret_cast<u64*>(&c->d_ctrl->wl_count[0]);
+  HCC_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(u64), c->stream));
+  if (f->n) {
+    const u64 nwords = (f->n + 31) / 32;
+    k_export<<<grid_for(nwords * 32, 256, (u64)c->sms * 32), 256, 0, c->stream>>>(
+        f->d_pi, f->n, dev_bits, reinterpret_cast<uint2*>(dev_pairs), cap, d_cnt);
+    HCC_CUDA(cudaGetLastError());
+  }
+  u64 h = 0;
+  HCC_CUDA(cudaMemcpyAsync(&h, d_cnt, sizeof(u64), cudaMemcpyDeviceToHost, c->stream));
+  HCC_CUDA(cudaStreamSynchronize(c->stream));
+  *count = h;
+  return HCC_OK;
+  HCC_GUARD_END
+}
+
+// Re-hook remote relations into a star forest with the worklist engine
+// (host-driven passes: the merge needs only a few).
+int hcc_rehook(hcc_ctx* c, hcc_forest* f, const uint32_t* dev_bits_or,
+               const uint32_t* dev_pairs, uint64_t count, hcc_metrics* mx) {
+  if (!f) return fail(HCC_EINVAL, "null forest");
+  if (count && !dev_pairs) return fail(HCC_EINVAL, "null pair buffer");
+  if (int r = ctx_enter(c)) return r;
+  hcc_metrics out{};
+  out.n = f->n;
+  out.m = count;
+  HCC_GUARD_BEGIN
+  const u64 n = f->n;
+  ensure_wl(c, count + n + 1);
+  Plan P;
+  P.algo = HCC_ALGO_BASELINE_MJ;
+  P.full_passes = false;
+  P.n = n;
+  P.m = 0;
+  P.edges = nullptr;
+  P.pi = f->d_pi;
+  P.wl0 = c->wl[0];
+  P.wl1 = c->wl[1];
+  P.nseg = 1;
+  P.walk = kDefaultWalk;
+  P.s0b = false;
+  P.block_hook = kHookThreads;
+  P.grid_hook = (unsigned)(c->sms * c->occ_hook);
+  P.block_vert = kVertThreads;
+  P.grid_vert = grid_for((n + 3) / 4, kVertThreads, 0x7fffffffull);
+  HCC_CUDA(cudaEventRecord(c->ev0, c->stream));
+  k_begin<<<1, 1, 0, c->stream>>>(c->d_ctrl, c->d_recs, 1);
+  u64* d_cnt = reinterpret_cast<u64*>(&c->d_ctrl->wl_count[0]);
+  if (count) {
+    HCC_CUDA(cudaMemcpyAsync(c->wl[0], dev_pairs, count * sizeof(uint2),
+                             cudaMemcpyDeviceToDevice, c->stream));
+    c->h_ctrl->wl_count[0] = count;
+    HCC_CUDA(cudaMemcpyAsync(d_cnt, &c->h_ctrl->wl_count[0], sizeof(u64),
+                             cudaMemcpyHostToDevice, c->stream));
+  }
+  if (dev_bits_or && n)
+    k_decode_bits<<<grid_for((n + 31) / 32 * 32, 256, (u64)c->sms * 32), 256, 0,
+                    c->stream>>>(dev_bits_or, f->d_pi, n, c->wl[0], d_cnt);
+  HCC_CUDA(cudaGetLastError());
+  Seq q;
+  q.c = c;
+  q.graph_mode = false;
+  q.streams.push_back(c->stream);
+  DevCtrl* ctrl = c->d_ctrl;
+  DevRec* recs = c->d_recs;
+  q.loop([&](cudaGraphConditionalHandle h, int u) {
+    k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(hook_args(c, P, kSrcWorklist, 1));
+    k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl, recs, 1);
+    k_step_worklist<<<1, 1, 0, q.s()>>>(ctrl, recs, h, u);
+  });
+  HCC_CUDA(cudaEventRecord(c->ev1, c->stream));
+  HCC_CUDA(cudaEventSynchronize(c->ev1));
+  float ms = 0.f;
+  HCC_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  HCC_CUDA(cudaMemcpy(c->h_ctrl, c->d_ctrl, sizeof(DevCtrl), cudaMemcpyDeviceToHost));
+  out.total_ms = ms;
+  out.passes = c->h_ctrl->passes;
+  out.outer_iterations = c->h_ctrl->passes;
+  out.edges_processed = c->h_ctrl->edges_processed;
+  out.kernels = 3 + 3 * c->h_ctrl->passes;
+  if (mx) *mx = out;
+  return HCC_OK;
+  HCC_GUARD_END
+}
 
 }  // extern "C"

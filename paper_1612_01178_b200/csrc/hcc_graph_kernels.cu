@@ -52,12 +52,11 @@ __global__ void k_csr_expand(const u64* row_ptr, const u32* col, u64 n,
   if (bad) atomicOr(err, 1u);
 }
 
-__global__ void k_gen_grid(uint2* out, u64 rows, u64 cols) {
-  const u64 m = rows * (cols - 1) + (rows - 1) * cols;
+__global__ void k_gen_grid(uint2* out, u64 rows, u64 cols, u64 first, u64 count) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
     u32 u, v;
-    grid_edge(rows, cols, i, &u, &v);
+    grid_edge(rows, cols, first + i, &u, &v);
     out[i] = make_uint2(u, v);
   }
 }

@@ -127,10 +127,16 @@ __global__ void k_narrow_u64(const u64* uv, uint2* out, u64 m, u64 n,
 __global__ void k_check_u32(const uint2* e, u64 m, u64 n, u32* err);
 __global__ void k_csr_expand(const u64* row_ptr, const u32* col, u64 n,
                              uint2* out, u64 m, u32* err);
-__global__ void k_gen_grid(uint2* out, u64 rows, u64 cols);
+__global__ void k_gen_grid(uint2* out, u64 rows, u64 cols, u64 first, u64 count);
 __global__ void k_gen_rmatx(uint2* out, u64 first, u64 count, u32 scale,
                             u64 seed, u32 ta, u32 tab, u32 tabc);
 __global__ void k_gen_erx(uint2* out, u64 first, u64 count, u64 n, u64 seed);
 __global__ void k_checksum(const uint2* e, u64 m, u64* out);
+
+// Multi-GPU merge (hcc_multi.cu).
+__global__ void k_export(const u32* pi, u64 n, u32* bits, uint2* pairs, u64 cap,
+                         u64* count);
+__global__ void k_decode_bits(const u32* bits_or, const u32* pi, u64 n,
+                              uint2* wl, u64* count);
 
 }  // namespace hcc

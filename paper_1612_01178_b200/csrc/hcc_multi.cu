@@ -1,41 +1,71 @@
-// Multi-GPU edge-partitioned CC (north-star (5)).
-// Placeholder entry points until the NCCL merge lands; they fail loudly.
-#include <string>
+// Multi-GPU merge kernels (north-star (5); SURVEY.md §8e shape 3).
+//
+// Each rank runs the single-GPU engine on its partition_edges(m, world)
+// shard (engines.hpp:43-58 semantics) into a full local forest.  The forest
+// of a rank is a set of stars, so it is fully described by the pairs
+// (v, pi(v)) with pi(v) != v.  On skewed graphs almost all of those point at
+// vertex 0 (the giant component's minimum), so the export is split into
+//   bits  : bit v = (pi(v) == 0 && v != 0)          n/8 bytes, dense
+//   pairs : (v, pi(v)) for pi(v) not in {v, 0}      8 bytes each, sparse
+// The host exchanges the payloads (NCCL allgather through torch.distributed
+// in bench.py; any transport works) and hcc_rehook re-hooks the remote
+// relations into the local forest as edges, with the same worklist kernels
+// as the single-GPU engine.  One exchange round suffices: after it every
+// rank holds the union of all shards' relations.
+#include <cuda_runtime.h>
 
-#include "hookcc_c.h"
+#include "hcc_internal.cuh"
 
-extern "C" {
+namespace hcc {
 
-int hcc_nccl_unique_id_size(void) { return 128; }
+namespace {
 
-int hcc_nccl_get_unique_id(void* id_out) {
-  (void)id_out;
-  return HCC_ENCCL;
+// Warp-aggregated append of one pair per active lane; returns via `pos`.
+__device__ __forceinline__ void warp_append(bool want, uint2 pr, uint2* out, u64 cap,
+                                            u64* count) {
+  const u32 mask = __ballot_sync(0xffffffffu, want);
+  if (!mask) return;
+  const u32 lane = threadIdx.x & 31u;
+  u64 base = 0;
+  if (lane == 0) base = atomicAdd(count, (u64)__popc(mask));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (want) {
+    const u64 pos = base + __popc(mask & ((1u << lane) - 1u));
+    if (pos < cap) out[pos] = pr;
+  }
 }
 
-int hcc_comm_init(hcc_ctx* ctx, int world, int rank, const void* id) {
-  (void)ctx;
-  (void)world;
-  (void)rank;
-  (void)id;
-  return HCC_ENCCL;
+}  // namespace
+
+// One warp per 32-vertex word.  Requires blockDim.x % 32 == 0.
+__global__ void k_export(const u32* pi, u64 n, u32* bits, uint2* pairs, u64 cap,
+                         u64* count) {
+  const u32 lane = threadIdx.x & 31u;
+  const u64 nwords = (n + 31) >> 5;
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 w = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwords; w += warps) {
+    const u64 v = (w << 5) + lane;
+    const u32 p = v < n ? __ldcg(pi + v) : (u32)v;
+    const u32 b = __ballot_sync(0xffffffffu, v < n && v != 0 && p == 0u);
+    if (lane == 0) bits[w] = b;
+    warp_append(v < n && p != (u32)v && p != 0u, make_uint2((u32)v, p), pairs, cap, count);
+  }
 }
 
-int hcc_comm_destroy(hcc_ctx* ctx) {
-  (void)ctx;
-  return HCC_OK;
+// Append (v, 0) for every v set in the OR of the remote bitmaps that is not
+// already in the local star of 0.
+__global__ void k_decode_bits(const u32* bits_or, const u32* pi, u64 n, uint2* wl,
+                              u64* count) {
+  const u32 lane = threadIdx.x & 31u;
+  const u64 nwords = (n + 31) >> 5;
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 w = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwords; w += warps) {
+    const u32 b = bits_or[w];
+    if (b == 0u) continue;  // warp-uniform
+    const u64 v = (w << 5) + lane;
+    const bool want = ((b >> lane) & 1u) && v < n && __ldcg(pi + v) != 0u;
+    warp_append(want, make_uint2((u32)v, 0u), wl, ~0ull, count);
+  }
 }
 
-int hcc_cc_distributed(hcc_ctx* ctx, const hcc_graph* shard, uint64_t n,
-                       const hcc_opts* opts, uint32_t* labels_out,
-                       hcc_metrics* out) {
-  (void)ctx;
-  (void)shard;
-  (void)n;
-  (void)opts;
-  (void)labels_out;
-  (void)out;
-  return HCC_ENCCL;
-}
-
-}  // extern "C"
+}  // namespace hcc

@@ -1,0 +1,148 @@
+"""Edge-partitioned multi-GPU connected components (north-star (5)).
+
+One process per GPU.  Rank r owns the contiguous edge range
+partition_edges(m, world)[r] (engines.hpp:43-58: the first m % world ranks
+get one extra edge) and runs the single-GPU Hook-Compress engine on it into
+a full local forest (stars).  The merge is one exchange round (§8e shape 3):
+
+  1. export   each rank encodes its forest as a bitmap of {v : pi(v) == 0}
+              (the giant component's root on skewed graphs) plus sparse
+              (v, pi(v)) pairs for the remaining non-self entries;
+  2. exchange all-gather of the bitmaps (OR-combined) and of the pair lists
+              (sizes first, then the padded payloads) over the process group
+              (NCCL on GPUs, gloo in the CPU tests);
+  3. re-hook  each rank hooks the remote relations as (v, pi_remote(v)) edges
+              into its own forest with the worklist engine.
+
+After the round every rank holds the union of all shards' relations, i.e. the
+global min-canonical labels.  The exchange is written against a tiny backend
+interface so that the protocol itself is testable without a GPU.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+def edge_range(m: int, world: int, rank: int) -> tuple[int, int]:
+    """(first, count) of rank's shard under partition_edges(m, world)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    base, rem = divmod(m, world)
+    first = rank * base + min(rank, rem)
+    return first, base + (1 if rank < rem else 0)
+
+
+@dataclass
+class MergeTimes:
+    local_ms: float = 0.0
+    export_ms: float = 0.0
+    exchange_ms: float = 0.0
+    rehook_ms: float = 0.0
+    pairs_sent: int = 0
+    pairs_received: int = 0
+    bits_bytes: int = 0
+    rehook_passes: int = 0
+    extra: dict = field(default_factory=dict)
+
+
+def exchange(bits, pairs, group=None):
+    """All-gather the payloads.
+
+    bits  : int32 tensor [nwords] (bit patterns), this rank's bitmap
+    pairs : int32 tensor [k, 2], this rank's (v, parent) pairs
+    returns (bits_or over the OTHER ranks, remote pairs [K, 2]).
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = bits.device
+    # flat output buffers: the layout both NCCL and gloo accept
+    gathered = torch.empty(world * bits.numel(), dtype=bits.dtype, device=dev)
+    dist.all_gather_into_tensor(gathered, bits.contiguous(), group=group)
+    gathered = gathered.view(world, bits.numel())
+    others = torch.cat([gathered[:rank], gathered[rank + 1:]]) if world > 1 else gathered[:0]
+    bits_or = torch.zeros_like(bits)
+    for row in others:
+        bits_or.bitwise_or_(row)
+    k = torch.tensor([pairs.shape[0]], dtype=torch.int64, device=dev)
+    sizes = torch.empty(world, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(sizes, k, group=group)
+    sizes_h = sizes.cpu().tolist()
+    kmax = max(sizes_h) if sizes_h else 0
+    if kmax == 0:
+        return bits_or, torch.empty((0, 2), dtype=pairs.dtype, device=dev)
+    padded = torch.zeros((kmax, 2), dtype=pairs.dtype, device=dev)
+    padded[: pairs.shape[0]] = pairs
+    allp = torch.empty(world * kmax * 2, dtype=pairs.dtype, device=dev)
+    dist.all_gather_into_tensor(allp, padded.view(-1), group=group)
+    allp = allp.view(world * kmax, 2)
+    parts = [allp[r * kmax: r * kmax + sizes_h[r]] for r in range(world) if r != rank]
+    remote = torch.cat(parts) if parts else torch.empty((0, 2), dtype=pairs.dtype, device=dev)
+    return bits_or, remote
+
+
+def merge_round(backend, group=None, sync=None) -> MergeTimes:
+    """export -> exchange -> re-hook on this rank (local CC already done)."""
+    t = MergeTimes()
+    sync = sync or (lambda: None)
+    t0 = time.perf_counter()
+    bits, pairs = backend.export()
+    sync()
+    t1 = time.perf_counter()
+    bits_or, remote = exchange(bits, pairs, group)
+    sync()
+    t2 = time.perf_counter()
+    mx = backend.rehook(bits_or, remote)
+    sync()
+    t3 = time.perf_counter()
+    t.export_ms, t.exchange_ms, t.rehook_ms = 1e3 * (t1 - t0), 1e3 * (t2 - t1), 1e3 * (t3 - t2)
+    t.pairs_sent = int(pairs.shape[0])
+    t.pairs_received = int(remote.shape[0])
+    t.bits_bytes = int(bits.numel() * 4)
+    t.rehook_passes = int(mx.get("passes", 0)) if isinstance(mx, dict) else 0
+    return t
+
+
+class CudaBackend:
+    """The B200 path: libhookcc_cuda.so kernels on torch CUDA buffers."""
+
+    def __init__(self, ctx, n: int, device):
+        import torch
+        self.torch = torch
+        self.ctx = ctx
+        self.n = n
+        self.device = device
+        self.forest = ctx.forest(n)
+        self.nwords = (n + 31) // 32
+        self.bits = torch.empty(self.nwords, dtype=torch.int32, device=device)
+        self.cap = max(1 << 16, n // 64)
+        self.pairs = torch.empty((self.cap, 2), dtype=torch.int32, device=device)
+        self.local_metrics = None
+
+    def local_cc(self, graph, **kw):
+        _, self.local_metrics = self.ctx.cc(graph, "baseline-mj", forest=self.forest,
+                                            labels=False, **kw)
+        return self.local_metrics
+
+    def export(self):
+        k = self.ctx.export(self.forest, self.bits.data_ptr(), self.pairs.data_ptr(), self.cap)
+        if k > self.cap:
+            self.cap = k + (k >> 3)
+            self.pairs = self.torch.empty((self.cap, 2), dtype=self.torch.int32,
+                                          device=self.device)
+            k = self.ctx.export(self.forest, self.bits.data_ptr(), self.pairs.data_ptr(), self.cap)
+        return self.bits, self.pairs[:k]
+
+    def rehook(self, bits_or, remote):
+        remote = remote.contiguous()
+        return self.ctx.rehook(self.forest, bits_or.data_ptr(),
+                               remote.data_ptr() if remote.shape[0] else None,
+                               int(remote.shape[0]))
+
+    def labels(self) -> np.ndarray:
+        return self.forest.snapshot()

@@ -22,7 +22,7 @@ def test_header_declares_boundary():
     d = declared()
     for must in ["hcc_create", "hcc_destroy", "hcc_graph_from_edges_u64", "hcc_graph_from_edges_u32",
                  "hcc_graph_from_csr", "hcc_graph_free", "hcc_cc", "hcc_last_error",
-                 "hcc_forest_download_u64", "hcc_cc_distributed"]:
+                 "hcc_forest_download_u64", "hcc_forest_export", "hcc_rehook"]:
         assert must in d
 
 
