@@ -83,6 +83,8 @@ constexpr u64 kMaxUnrolledSegments = 64;
 // Root-walk steps of the atomic-free hook before an unconditional store
 // (HCC_WALK overrides, for tuning).
 constexpr int kDefaultWalk = 32;
+// First adaptive topology segment = m >> kAdaptShift (HCC_PLAN=adapt:<k>).
+constexpr u32 kAdaptShift = 7;
 
 int usable_devices() {
   int count = 0;
@@ -327,6 +329,8 @@ struct Plan {
   std::vector<u64> bounds;  // unrolled topology segment boundaries (nseg+1)
   int walk;
   bool s0b;                 // star-0 bitmap for hook passes after a compress
+  bool adapt;               // device-side adaptive topology plan
+  u32 adapt_shift;          // first adaptive segment = m >> adapt_shift
   unsigned grid_hook, block_hook, grid_vert, block_vert;
 };
 
@@ -396,13 +400,14 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           HCC_CUDA(cudaEventCreate(&ev));
           c->seg_ev.push_back(ev);
         }
+        if (P.adapt) k_plan_begin<<<1, 1, 0, q.s()>>>(ctrl, P.m, P.adapt_shift);
         for (u64 sgi = 0; sgi < P.nseg; ++sgi) {
-          HookArgs ha = hook_args(c, P, kSrcRange, 1);
+          HookArgs ha = hook_args(c, P, P.adapt ? kSrcCtrlRange : kSrcRange, 1);
           ha.b = P.bounds[sgi];
           ha.e = P.bounds[sgi + 1];
           if (P.s0b && sgi >= 1) ha.s0b = c->s0b;
           q.record(c->seg_ev[2 * sgi]);
-          const u64 seg_edges = ha.e - ha.b;
+          const u64 seg_edges = ha.e - ha.b;  // adaptive: the static estimate
           if (P.block_hook == kHookThreads &&
               seg_edges < (u64)P.grid_hook * kHookThreads * kHookEPT * 2) {
             // forming-regime segment: EPT 2 over a full grid
@@ -414,13 +419,16 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           q.record(c->seg_ev[2 * sgi + 1]);
           q.phase_done(HCC_PHASE_HOOK);
           if (P.s0b)  // compress + star-0 bitmap (bitmap initialised by k_init_pi)
-            k_compress_s0b<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
-                                                                    recs, c->s0b, 1);
+            k_compress_s0b<<<grid_for((P.n + 7) / 8, kVertThreads, 0x7fffffffull),
+                             kVertThreads, 0, q.s()>>>(P.pi, P.n, ctrl, recs, c->s0b, 1);
           else
             k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
                                                                 recs, 1);
           q.phase_done(HCC_PHASE_COMPRESS);
-          k_step_segment<<<1, 1, 0, q.s()>>>(ctrl, recs, 0, 0);
+          if (P.adapt)
+            k_step_adapt<<<1, 1, 0, q.s()>>>(ctrl, recs, P.m);
+          else
+            k_step_segment<<<1, 1, 0, q.s()>>>(ctrl, recs, 0, 0);
         }
         c->seg_ev_used = P.nseg;
       } else {
@@ -441,8 +449,8 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
         k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(wa);
         q.phase_done(HCC_PHASE_HOOK);
         if (P.s0b && !P.bounds.empty())
-          k_compress_s0b<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
-                                                                  recs, c->s0b, 1);
+          k_compress_s0b<<<grid_for((P.n + 7) / 8, kVertThreads, 0x7fffffffull),
+                           kVertThreads, 0, q.s()>>>(P.pi, P.n, ctrl, recs, c->s0b, 1);
         else
           k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
                                                               recs, 1);
@@ -1100,9 +1108,39 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   if (requested < 1) requested = 1;
   u64 nseg = std::max<u64>(1, std::min(requested, std::max<u64>(m, 1)));
   std::vector<u64> bounds;
+  bool adapt = false;
+  u32 adapt_shift = kAdaptShift;
   if (geo_plan) {
-    bounds = geometric_bounds(m);
-    nseg = bounds.size() - 1;
+    const char* pe = std::getenv("HCC_PLAN");
+    int sh = 0;
+    if (!pe || std::strncmp(pe, "adapt", 5) == 0) {
+      // device-side adaptive plan: launches are unrolled up to the number a
+      // x4-growth schedule can need; ranges past the end are empty no-ops
+      adapt = true;
+      if (pe && std::sscanf(pe, "adapt:%d", &sh) == 1 && sh >= 0 && sh < 40)
+        adapt_shift = (u32)sh;
+      u64 first = std::max<u64>(1, m >> adapt_shift), len = first, covered = first;
+      nseg = 1;
+      while (covered < m && nseg < kMaxUnrolledSegments) {
+        len = std::min<u64>(len * kAdaptGrowth, m - covered);
+        covered += len;
+        ++nseg;
+      }
+      // the static bounds only size the launch of each slot (small vs
+      // streaming hook kernel); the device decides the real ranges
+      bounds.assign(nseg + 1, 0);
+      u64 b = 0, l = first;
+      for (u64 i = 0; i < nseg; ++i) {
+        bounds[i] = b;
+        b = std::min<u64>(m, b + l);
+        l *= kAdaptGrowth;
+      }
+      bounds[nseg] = m;
+      if (nseg >= 2) bounds[nseg - 1] = std::min(bounds[nseg - 1], m);
+    } else {
+      bounds = geometric_bounds(m);
+      nseg = bounds.size() - 1;
+    }
   } else if (nseg <= kMaxUnrolledSegments) {
     bounds = uniform_bounds(m, nseg);
   }
@@ -1140,6 +1178,8 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   P.nseg = nseg;
   P.bounds = bounds;
   P.s0b = s0b && !bounds.empty();
+  P.adapt = adapt;
+  P.adapt_shift = adapt_shift;
   if (P.s0b) ensure_s0b(c, (n + 31) / 32);
   {
     const char* w = std::getenv("HCC_WALK");
@@ -1201,6 +1241,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   key.flags = o->flags;
   key.walk = P.walk;
   key.s0b = P.s0b;
+  key.plan = key.plan * 31 + (P.adapt ? 1000 + P.adapt_shift : 0);
   for (u64 x : P.bounds) key.plan = key.plan * 1000003ull + x;
 
   if (graph_mode) {

@@ -51,6 +51,7 @@ struct DevCtrl {
   u32 err;           // sticky device error bits
   u32 flag;          // scratch result flag (is_star / bound checks)
   u64 loop_steps;    // loop-step kernels executed (runaway guard)
+  u64 seg_b, seg_e;  // adaptive topology plan: current segment range
 };
 
 // Device loops stop (and report HCC_ECUDA) after this many steps; the
@@ -63,7 +64,15 @@ enum HookMode : int {
   kSrcRange = 0,     // edges[b, e)
   kSrcSegment = 1,   // segment ctrl->seg of partition_edges(m, ctrl->nseg)
   kSrcWorklist = 2,  // wl[ctrl->parity][0, wl_count[parity])
+  kSrcCtrlRange = 3, // edges[ctrl->seg_b, ctrl->seg_e) (adaptive plan)
 };
+
+// Adaptive topology plan: the first segment is m >> shift;
+// while a segment stores for more than kAdaptFormingPct% of its edges (trees
+// still forming) the next one is kAdaptGrowth times larger, otherwise the
+// next segment takes every remaining edge.
+constexpr u32 kAdaptGrowth = 4;
+constexpr u32 kAdaptFormingPct = 20;
 
 struct HookArgs {
   const uint2* edges;
@@ -105,6 +114,8 @@ __global__ void k_step_worklist(DevCtrl* ctrl, DevRec* recs,
                                 cudaGraphConditionalHandle h, int use_cond);
 __global__ void k_step_segment(DevCtrl* ctrl, DevRec* recs,
                                cudaGraphConditionalHandle h, int use_cond);
+__global__ void k_plan_begin(DevCtrl* ctrl, u64 m, u32 shift);
+__global__ void k_step_adapt(DevCtrl* ctrl, DevRec* recs, u64 m);
 __global__ void k_step_outer(DevCtrl* ctrl, DevRec* recs,
                              cudaGraphConditionalHandle h, int use_cond);
 __global__ void k_step_jump(DevCtrl* ctrl, cudaGraphConditionalHandle h,

@@ -131,6 +131,11 @@ __device__ __forceinline__ void resolve_src(const HookArgs& a, const uint2*& src
     if (b > e) b = e;
     src = a.edges;
     out = c->parity;
+  } else if (a.mode == kSrcCtrlRange) {
+    src = a.edges;
+    b = c->seg_b;
+    e = c->seg_e;
+    out = c->parity;
   } else {
     u32 p = c->parity;
     src = p ? a.wl1 : a.wl0;
@@ -528,17 +533,21 @@ __global__ void __launch_bounds__(kVertThreads)
   DevRec* r = cur_rec(ctrl, recs);
   block_t0(&r->comp_t0);
   u64 steps = 0;
+  // Thread q owns vertices [8q, 8q+8): two 16-byte reads and eight parent
+  // gathers in flight before any chase (ascending order is kept: a thread's
+  // vertices are consecutive and blocks start in ascending order).
   const u64 q = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  const u64 v0 = q << 2;
-  u32 nib = 0;
-  if (v0 + 4 <= n) {
-    const uint4 pp = __ldcg(reinterpret_cast<const uint4*>(pi) + q);
-    u32 p[4] = {pp.x, pp.y, pp.z, pp.w};
-    u32 gp[4];
+  const u64 v0 = q << 3;
+  u32 byte = 0;  // bit j = (root(v0 + j) == 0)
+  if (v0 + 8 <= n) {
+    const uint4* p4 = reinterpret_cast<const uint4*>(pi) + (q << 1);
+    const uint4 pa = __ldcg(p4), pb = __ldcg(p4 + 1);
+    u32 p[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+    u32 gp[8];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) gp[j] = p[j] != (u32)v0 + j ? ld_pi(pi + p[j]) : p[j];
+    for (int j = 0; j < 8; ++j) gp[j] = p[j] != (u32)v0 + j ? ld_pi(pi + p[j]) : p[j];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < 8; ++j) {
       u32 a = p[j], b = gp[j];
       if (j > 0 && a >= (u32)v0 && a != (u32)v0 + j) b = ld_fresh(pi + a);
       while (b != a) {
@@ -547,7 +556,7 @@ __global__ void __launch_bounds__(kVertThreads)
         a = b;
         b = ld_fresh(pi + a);
       }
-      nib |= (a == 0u) ? 1u << j : 0u;
+      byte |= (a == 0u) ? 1u << j : 0u;
     }
   } else if (v0 < n) {
     for (u64 v = v0; v < n; ++v) {
@@ -561,16 +570,15 @@ __global__ void __launch_bounds__(kVertThreads)
           b = ld_fresh(pi + a);
         }
       }
-      nib |= (a == 0u) ? 1u << (u32)(v - v0) : 0u;
+      byte |= (a == 0u) ? 1u << (u32)(v - v0) : 0u;
     }
   }
+  // four lanes = one 32-vertex word
   const u32 lane = threadIdx.x & 31u;
-  u32 w = nib << (4u * (lane & 7u));
+  u32 w = byte << (8u * (lane & 3u));
   w |= __shfl_xor_sync(0xffffffffu, w, 1);
   w |= __shfl_xor_sync(0xffffffffu, w, 2);
-  w |= __shfl_xor_sync(0xffffffffu, w, 4);
-  const u64 word = (v0 >> 5);  // lanes 8i..8i+7 share word (v0 of lane 8i) >> 5
-  if ((lane & 7u) == 0 && v0 < n) bits[word] = w;
+  if ((lane & 3u) == 0 && v0 < n) bits[v0 >> 5] = w;
   add_counter(&r->jump_steps, steps);
   block_t1(&r->comp_t1);
 }
@@ -634,6 +642,29 @@ __global__ void k_step_segment(DevCtrl* c, DevRec* recs,
   const u32 cond = guard(c, c->seg < c->nseg ? 1u : 0u);
   c->cond = cond;
   if (use_cond) cudaGraphSetConditional(h, cond);
+}
+
+__global__ void k_plan_begin(DevCtrl* c, u64 m, u32 shift) {
+  u64 first = shift >= 63 ? 0 : (m >> shift);
+  if (first == 0) first = m < 1 ? m : 1;
+  c->seg_b = 0;
+  c->seg_e = first;
+}
+
+// Adaptive segment finished: choose the next range from this segment's
+// store ratio (records are per segment).
+__global__ void k_step_adapt(DevCtrl* c, DevRec* recs, u64 m) {
+  const DevRec& r = recs[c->rec < (u32)kMaxRecs ? c->rec : (u32)kMaxRecs - 1];
+  const u64 len = c->seg_e - c->seg_b;
+  const bool forming = r.edges_in > 0 && r.edges_out * 100 > r.edges_in * kAdaptFormingPct;
+  c->seg_b = c->seg_e;
+  u64 next = forming ? len * kAdaptGrowth : m;
+  if (next < 1) next = 1;
+  c->seg_e = (m - c->seg_b) <= next ? m : c->seg_b + next;
+  c->seg += 1;
+  c->passes += (len > 0);
+  c->dirty = 0;
+  next_rec(c, recs);
 }
 
 // Baseline outer iteration finished: loop while some hook changed.
