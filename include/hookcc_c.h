@@ -177,6 +177,11 @@ int hcc_graph_from_edges_u32(hcc_ctx* ctx, const uint32_t* uv, uint64_t m,
  * is internal to bfs_cc, oracle.hpp:68-83.) */
 int hcc_graph_from_csr(hcc_ctx* ctx, const uint64_t* row_ptr,
                        const uint32_t* col, uint64_t n, hcc_graph** out);
+/* Overwrite edges [first, first+count) of an existing graph from host u32
+ * pairs (endpoint-checked).  Reusing one handle for successive inputs of the
+ * same size keeps its device buffer and the cached executable CUDA graph. */
+int hcc_graph_assign_edges_u32(hcc_ctx* ctx, hcc_graph* g, const uint32_t* uv,
+                               uint64_t first, uint64_t count);
 /* Device generators. spec: "grid:RxC" (identical to generators.hpp:71-87),
  * "rmatx:scale=K,ef=F[,seed=S][,a=..,b=..,c=..,d=..]" and
  * "erx:n=N,m=M[,seed=S]" (counter-based twins of generators.hpp:14-62,

@@ -76,6 +76,7 @@ _SIGS = {
     "hcc_graph_from_edges_u64": (i32, [vp, vp, u64, u64, C.POINTER(vp)]),
     "hcc_graph_from_edges_u32": (i32, [vp, vp, u64, u64, C.POINTER(vp)]),
     "hcc_graph_from_csr": (i32, [vp, vp, vp, u64, C.POINTER(vp)]),
+    "hcc_graph_assign_edges_u32": (i32, [vp, vp, vp, u64, u64]),
     "hcc_graph_generate": (i32, [vp, C.c_char_p, u64, C.POINTER(vp)]),
     "hcc_graph_info": (i32, [vp, C.POINTER(u64), C.POINTER(u64)]),
     "hcc_graph_download_u32": (i32, [vp, vp, vp, u64, u64]),
@@ -294,6 +295,13 @@ class Graph:
         check(lib().hcc_graph_download_u32(self.ctx.h, self.h, _ptr(out) if count else None,
                                            first, count))
         return out
+
+    def assign(self, edges: np.ndarray, first: int = 0) -> None:
+        """Overwrite edges [first, first+len) from host u32 pairs (pinned memory
+        gives full PCIe bandwidth)."""
+        e = np.ascontiguousarray(edges, dtype=np.uint32).reshape(-1, 2)
+        check(lib().hcc_graph_assign_edges_u32(self.ctx.h, self.h, _ptr(e) if e.size else None,
+                                               first, e.shape[0]))
 
     def checksum(self) -> int:
         out = u64()

@@ -420,7 +420,8 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           q.phase_done(HCC_PHASE_HOOK);
           if (P.s0b)  // compress + star-0 bitmap (bitmap initialised by k_init_pi)
             k_compress_s0b<<<grid_for((P.n + 7) / 8, kVertThreads, 0x7fffffffull),
-                             kVertThreads, 0, q.s()>>>(P.pi, P.n, ctrl, recs, c->s0b, 1);
+                             kVertThreads, 0, q.s()>>>(P.pi, P.n, ctrl, recs, c->s0b,
+                                                       kCompressIfDirty);
           else
             k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
                                                                 recs, 1);
@@ -450,7 +451,8 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
         q.phase_done(HCC_PHASE_HOOK);
         if (P.s0b && !P.bounds.empty())
           k_compress_s0b<<<grid_for((P.n + 7) / 8, kVertThreads, 0x7fffffffull),
-                           kVertThreads, 0, q.s()>>>(P.pi, P.n, ctrl, recs, c->s0b, 1);
+                           kVertThreads, 0, q.s()>>>(P.pi, P.n, ctrl, recs, c->s0b,
+                                                     kCompressIfDirty);
         else
           k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
                                                               recs, 1);
@@ -800,6 +802,31 @@ int hcc_graph_from_edges_u32(hcc_ctx* c, const uint32_t* uv, uint64_t m,
     hcc_graph_free(g);
     return f.code;
   }
+}
+
+int hcc_graph_assign_edges_u32(hcc_ctx* c, hcc_graph* g, const uint32_t* uv,
+                               uint64_t first, uint64_t count) {
+  if (!g || (count && !uv)) return fail(HCC_EINVAL, "null argument");
+  if (first > g->m || count > g->m - first)
+    return fail(HCC_EINVAL, "range out of bounds");
+  if (int r = ctx_enter(c)) return r;
+  HCC_GUARD_BEGIN
+  u32* d_err = reinterpret_cast<u32*>(&c->d_ctrl->err);
+  HCC_CUDA(cudaMemsetAsync(d_err, 0, sizeof(u32), c->stream));
+  if (count) {
+    HCC_CUDA(cudaMemcpyAsync(g->d_edges + first, uv, count * sizeof(uint2),
+                             cudaMemcpyHostToDevice, c->stream));
+    k_check_u32<<<grid_for(count, 256, 65536), 256, 0, c->stream>>>(g->d_edges + first,
+                                                                    count, g->n, d_err);
+    HCC_CUDA(cudaGetLastError());
+  }
+  u32 err = 0;
+  HCC_CUDA(cudaMemcpyAsync(&err, d_err, sizeof(u32), cudaMemcpyDeviceToHost, c->stream));
+  HCC_CUDA(cudaStreamSynchronize(c->stream));
+  g->has_stats = false;
+  if (err) return fail(HCC_ERANGE, "edge endpoint out of range");
+  return HCC_OK;
+  HCC_GUARD_END
 }
 
 int hcc_graph_from_csr(hcc_ctx* c, const uint64_t* row_ptr, const uint32_t* col,

@@ -54,6 +54,12 @@ struct DevCtrl {
   u64 seg_b, seg_e;  // adaptive topology plan: current segment range
 };
 
+// k_compress_s0b modes.
+enum CompressMode : int {
+  kCompressAlways = 0,
+  kCompressIfDirty = 1,
+};
+
 // Device loops stop (and report HCC_ECUDA) after this many steps; the
 // reference's own bound is 4*ceil(log2(n+2))+2 outer iterations
 // (test_engines.cpp:179-187), so this only catches bugs.

@@ -60,6 +60,23 @@ __device__ __forceinline__ uint4 ld_stream16(const uint4* p, u64 pol) {
 // (any value ever held by the slot is a valid ancestor).
 __device__ __forceinline__ u32 ld_pi(const u32* p) { return *p; }
 
+// Star-0 bitmap read: the bitmap is written only by the compress kernel,
+// never during a hook launch, so the read-only path is legal; evict-last
+// keeps hot words resident against the pi gathers.  HCC_BITLOAD selects the
+// variant at compile time for experiments (0 = plain, 1 = nc + evict_last).
+#ifndef HCC_BITLOAD
+#define HCC_BITLOAD 0
+#endif
+__device__ __forceinline__ u32 ld_bits(const u32* p) {
+#if HCC_BITLOAD == 1
+  u32 r;
+  asm volatile("ld.global.nc.L1::evict_last.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+#else
+  return *p;
+#endif
+}
+
 // Coherent (L2) read: sees other threads' stores made during this kernel.
 __device__ __forceinline__ u32 ld_fresh(const u32* p) { return __ldcg(p); }
 
@@ -147,8 +164,12 @@ __device__ __forceinline__ void resolve_src(const HookArgs& a, const uint2*& src
 
 // Reserve space for `c` entries of this thread in the output worklist with
 // one global atomic per block; returns this thread's first slot.
-__device__ __forceinline__ bool block_reserve(u32 c, u64* cnt, DevRec* r,
-                                              DevCtrl* ctrl, u64& pos) {
+// `appended` (meaningful in the thread that reserves: warp 0 lane 31, or
+// each thread of a tiny launch) accumulates this block's appends; the block
+// publishes it once per launch (block_publish), so a launch costs one
+// counter atomic and one dirty store per block instead of one per tile.
+__device__ __forceinline__ bool block_reserve(u32 c, u64* cnt, u64& pos,
+                                              u64& appended) {
   __shared__ u32 s_w[32];
   __shared__ u64 s_base;
   if (!__syncthreads_or(c != 0)) return false;
@@ -158,8 +179,7 @@ __device__ __forceinline__ bool block_reserve(u32 c, u64* cnt, DevRec* r,
     for (u32 t = 0; t < blockDim.x; ++t) {
       if (t == threadIdx.x && c) {
         pos = atomicAdd(cnt, (u64)c);
-        atomicAdd(&r->edges_out, (u64)c);
-        ctrl->dirty = 1;
+        appended += c;
       }
       __syncthreads();
     }
@@ -186,13 +206,19 @@ __device__ __forceinline__ bool block_reserve(u32 c, u64* cnt, DevRec* r,
     if (lane < nw) s_w[lane] = inc - w;
     if (lane == 31) {
       s_base = atomicAdd(cnt, (u64)inc);
-      atomicAdd(&r->edges_out, (u64)inc);
-      ctrl->dirty = 1;
+      appended += inc;
     }
   }
   __syncthreads();
   pos = s_base + s_w[warp] + (x - c);
   return c != 0;
+}
+
+__device__ __forceinline__ void block_publish(u64 appended, DevRec* r, DevCtrl* ctrl) {
+  if (appended) {
+    atomicAdd(&r->edges_out, appended);
+    ctrl->dirty = 1;
+  }
 }
 
 }  // namespace
@@ -255,10 +281,13 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
       u32 x = ld_fresh(pi + ed.x), y = ld_fresh(pi + ed.y);
       if (x == y) continue;
       u32 h = max(x, y), l = min(x, y);
-      bool store = true;
+      bool store = true, at_root = a.walk == 0;
       for (int step = 0; step < a.walk; ++step) {
         const u32 ph = ld_fresh(pi + h);
-        if (ph == h) break;
+        if (ph == h) {
+          at_root = true;
+          break;
+        }
         if (ph == l) {
           store = false;
           break;
@@ -267,8 +296,10 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
         l = min(ph, l);
       }
       if (!store) continue;
-      pi[h] = l;
-      wrote = 1;
+      if (at_root) {
+        pi[h] = l;
+        wrote = 1;
+      }
       if (a.append) {
         const u64 pos = atomicAdd(cnt_out, 1ull);
         wl_out[pos] = make_uint2(h, l);
@@ -288,6 +319,7 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
   if (b2 > e) b2 = e;
   const u64 n4 = (e - b2) >> 1;
   u32 any_change = 0;
+  u64 appended = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     u64 idx[2];
     int k = 0;
@@ -339,8 +371,8 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
       u32 wu[EPT], wv[EPT];
 #pragma unroll
       for (int k = 0; k < EPT; ++k) {
-        wu[k] = ld_pi(a.s0b + (ed[k].x >> 5));
-        wv[k] = ld_pi(a.s0b + (ed[k].y >> 5));
+        wu[k] = ld_bits(a.s0b + (ed[k].x >> 5));
+        wv[k] = ld_bits(a.s0b + (ed[k].y >> 5));
       }
 #pragma unroll
       for (int k = 0; k < EPT; ++k) {
@@ -369,27 +401,30 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
       if (pu[k] == pv[k]) continue;
       u32 x = pu[k], y = pv[k];
       u32 h = max(x, y), l = min(x, y);
-      bool store = true;
+      bool store = true, at_root = a.walk == 0;
       for (int step = 0; step < a.walk; ++step) {
         // L1-cached read: any value the slot ever held is a recorded link
-        // (pass-start star link or a worklist pair), so a stale value is a
-        // safe basis for both "drop" and "descend"; reading through L1
-        // keeps the hub slots every edge touches off the L2 slices.
+        // (pass-start link or a worklist pair), so a stale value is a safe
+        // basis for both "drop" and "descend"; reading through L1 keeps the
+        // hub slots every edge touches off the L2 slices.
         const u32 ph = ld_pi(pi + h);
-        if (ph == h) break;             // root: store below
+        if (ph == h) {                  // root: store below
+          at_root = true;
+          break;
+        }
         if (ph == l) {                  // already linked
           store = false;
           break;
         }
         h = max(ph, l);
         l = min(ph, l);
-        if (h == l) {
-          store = false;
-          break;
-        }
       }
       if (store) {
-        pi[h] = l;
+        // A walk that ran out of steps defers the pair to the worklist
+        // without storing: h may be an interior vertex whose link existed
+        // at pass start (the forest need not be a star), and only slots
+        // observed as roots may be written.
+        if (at_root) pi[h] = l;
         pu[k] = h;
         pv[k] = l;
         act |= 1u << k;
@@ -397,7 +432,7 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
     }
     if (a.append) {
       u64 pos;
-      if (block_reserve(__popc(act), cnt_out, r, ctrl, pos)) {
+      if (block_reserve(__popc(act), cnt_out, pos, appended)) {
 #pragma unroll
         for (int k = 0; k < EPT; ++k)
           if (act & (1u << k)) wl_out[pos++] = make_uint2(pu[k], pv[k]);
@@ -411,6 +446,8 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
       ctrl->changed = 1;
       ctrl->dirty = 1;
     }
+  } else {
+    block_publish(appended, r, ctrl);
   }
   block_t1(&r->hook_t1);
 }
@@ -528,8 +565,8 @@ __global__ void __launch_bounds__(kVertThreads)
 // three warp shuffles (8 lanes = one 32-vertex word) and stored once.
 __global__ void __launch_bounds__(kVertThreads)
     k_compress_s0b(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs, u32* bits,
-                   int skip_if_clean) {
-  if (skip_if_clean && *(volatile u32*)&ctrl->dirty == 0) return;
+                   int mode) {
+  if (mode && *(volatile u32*)&ctrl->dirty == 0) return;
   DevRec* r = cur_rec(ctrl, recs);
   block_t0(&r->comp_t0);
   u64 steps = 0;

@@ -467,12 +467,33 @@ def test_star0_bitmap_paths(ctx, oracle, spec):
     import os
     g = ctx.generate(spec)
     want = oracle.cc(g.n, g.edges())
-    for s0b in ["1", "0"]:
-        os.environ["HCC_S0B"] = s0b
+    for s0b, walk in [("1", "32"), ("0", "32"), ("1", "2"), ("1", "1"), ("0", "1")]:
+        os.environ.update(HCC_S0B=s0b, HCC_WALK=walk)
         try:
             for fps in [0, 1, 3]:
                 lab, mx = ctx.cc(g, "baseline-mj", first_pass_segments=fps)
-                assert np.array_equal(lab, want), (spec, s0b, fps)
+                assert np.array_equal(lab, want), (spec, s0b, walk, fps)
                 assert mx["star0_bitmap"] == (s0b == "1")
         finally:
-            os.environ.pop("HCC_S0B", None)
+            for k in ("HCC_S0B", "HCC_WALK"):
+                os.environ.pop(k, None)
+
+
+def test_graph_assign_reuses_handle(ctx, oracle):
+    """hcc_graph_assign_edges_u32 refills a handle; results track the new edges
+    and the out-of-range check still applies."""
+    a = oracle.gen_rmat(12, 8, 1).astype(np.uint32)
+    b = oracle.gen_rmat(12, 8, 2).astype(np.uint32)
+    g = ctx.graph_from_edges(a, 4096)
+    assert np.array_equal(ctx.cc(g)[0], oracle.cc(4096, a))
+    g.assign(b)
+    assert np.array_equal(ctx.cc(g)[0], oracle.cc(4096, b))
+    g.assign(a[:100], first=5)
+    want = b.copy()
+    want[5:105] = a[:100]
+    assert np.array_equal(g.edges(), want)
+    assert np.array_equal(ctx.cc(g)[0], oracle.cc(4096, want))
+    import paper_1612_01178_b200.capi as C
+    with pytest.raises(C.HccError) as ei:
+        g.assign(np.array([[0, 4096]], dtype=np.uint32))
+    assert ei.value.code == C.HCC_ERANGE
