@@ -17,7 +17,7 @@ LDLIBS := -L$(LIBDIR) -lhookcc_cuda -Wl,-rpath,$(LIBDIR) -pthread
 HDRS := $(wildcard $(ROOT)include/hookcc/*.hpp) $(ROOT)include/hookcc_c.h
 LIBSO := $(LIBDIR)/libhookcc_cuda.so
 
-all: lib cc reftests oracle
+all: lib cc reftests apitests oracle
 
 lib:
 	python3 -m paper_1612_01178_b200.build
@@ -46,7 +46,13 @@ $(BIN)/acceptance: $(REF_TESTS)/acceptance.cpp $(HDRS) | $(LIBSO)
 	@mkdir -p $(BIN)
 	$(CXX) $(CXXFLAGS) $(INC) -DFIXTURE_DIR=\"$(ROOT)tests/golden/fixtures\" -o $@ $< $(LDLIBS)
 
+# B200-only API additions (own sources, no reference needed)
+apitests: $(BIN)/api_extras
+$(BIN)/api_extras: $(ROOT)tests/cpp/test_api_extras.cpp $(ROOT)tests/cpp/shim/catch_main.cpp $(HDRS) $(ROOT)include/hookcc/verify.hpp | $(LIBSO)
+	@mkdir -p $(BIN)
+	$(CXX) $(CXXFLAGS) $(INC) $(SHIM) -o $@ $(ROOT)tests/cpp/test_api_extras.cpp $(ROOT)tests/cpp/shim/catch_main.cpp $(LDLIBS)
+
 oracle:
 	$(MAKE) -C $(ROOT)oracle
 
-.PHONY: all lib cc reftests oracle
+.PHONY: all lib cc reftests apitests oracle

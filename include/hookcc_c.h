@@ -246,6 +246,20 @@ int hcc_forest_is_star(hcc_forest* f, int* out);           /* 140-146 */
 /* max over v of (pi(v) > v): the bound invariant (SPEC: pi(v) <= v). */
 int hcc_forest_check_bound(hcc_forest* f, int* ok);
 
+/* ---- device-side verification -------------------------------
+ * Size-independent checks of a finished forest against its graph:
+ *   bad_edges    = #edges (u, v) with pi(u) != pi(v)   (labels split an edge)
+ *   bad_vertices = #v with pi(v) > v or pi(pi(v)) != pi(v)  (not canonical
+ *                  min-rooted stars)
+ * Both are 0 for a correct min-canonical labeling. */
+int hcc_forest_verify(hcc_ctx* ctx, const hcc_graph* g, hcc_forest* f,
+                      uint64_t* bad_edges, uint64_t* bad_vertices);
+/* partitions_equal (oracle.hpp:112-126) on the device: host label arrays a, b
+ * of n entries induce the same partition (radix sort of (a, b) pairs, then
+ * #distinct pairs == #distinct a == #distinct b).  exact = (a == b). */
+int hcc_labels_compare(hcc_ctx* ctx, const uint32_t* a, const uint32_t* b,
+                       uint64_t n, int* partition_equal, int* exact);
+
 /* ---- multi-GPU merge primitives (north-star (5), SURVEY 8e shape 3) ------
  * After a local CC on an edge shard, a rank exports its star forest as
  *   bits  : uint32[ceil(n/32)], bit v = (pi(v) == 0 && v != 0)

@@ -104,6 +104,8 @@ _SIGS = {
     "hcc_forest_is_star": (i32, [vp, C.POINTER(i32)]),
     "hcc_forest_check_bound": (i32, [vp, C.POINTER(i32)]),
     "hcc_forest_export": (i32, [vp, vp, vp, vp, u64, C.POINTER(u64)]),
+    "hcc_forest_verify": (i32, [vp, vp, vp, C.POINTER(u64), C.POINTER(u64)]),
+    "hcc_labels_compare": (i32, [vp, vp, vp, u64, C.POINTER(i32), C.POINTER(i32)]),
     "hcc_rehook": (i32, [vp, vp, vp, vp, u64, C.POINTER(Metrics)]),
     "hcc_graph_generate_range": (i32, [vp, C.c_char_p, u64, u64, u64, C.POINTER(vp)]),
 }
@@ -231,6 +233,24 @@ class Context:
         mx = Metrics()
         check(lib().hcc_rehook(self.h, forest.h, dev_bits_or, dev_pairs, count, C.byref(mx)))
         return metrics_dict(mx)
+
+    def verify(self, graph: "Graph", forest: "Forest") -> tuple[int, int]:
+        """(edges split by the labels, non-canonical vertices); (0, 0) when correct."""
+        be, bv = u64(), u64()
+        check(lib().hcc_forest_verify(self.h, graph.h, forest.h, C.byref(be), C.byref(bv)))
+        return be.value, bv.value
+
+    def labels_compare(self, a: np.ndarray, b: np.ndarray) -> tuple[bool, bool]:
+        """(partitions equal, arrays equal) computed on the device."""
+        x = np.ascontiguousarray(a, dtype=np.uint32)
+        y = np.ascontiguousarray(b, dtype=np.uint32)
+        if x.shape != y.shape:
+            raise ValueError("partitions_equal: length mismatch")
+        pe, ex = i32(), i32()
+        check(lib().hcc_labels_compare(self.h, _ptr(x) if x.size else None,
+                                       _ptr(y) if y.size else None, x.size,
+                                       C.byref(pe), C.byref(ex)))
+        return bool(pe.value), bool(ex.value)
 
     def forest(self, n: int) -> "Forest":
         h = vp()

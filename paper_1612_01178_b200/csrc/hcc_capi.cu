@@ -331,6 +331,7 @@ struct Plan {
   bool s0b;                 // star-0 bitmap for hook passes after a compress
   bool adapt;               // device-side adaptive topology plan
   u32 adapt_shift;          // first adaptive segment = m >> adapt_shift
+  u32 forming_pct;          // store ratio (%) above which a segment is forming
   unsigned grid_hook, block_hook, grid_vert, block_vert;
 };
 
@@ -427,7 +428,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
                                                                 recs, 1);
           q.phase_done(HCC_PHASE_COMPRESS);
           if (P.adapt)
-            k_step_adapt<<<1, 1, 0, q.s()>>>(ctrl, recs, P.m);
+            k_step_adapt<<<1, 1, 0, q.s()>>>(ctrl, recs, P.m, P.forming_pct);
           else
             k_step_segment<<<1, 1, 0, q.s()>>>(ctrl, recs, 0, 0);
         }
@@ -1207,6 +1208,8 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   P.s0b = s0b && !bounds.empty();
   P.adapt = adapt;
   P.adapt_shift = adapt_shift;
+  P.forming_pct = std::getenv("HCC_FORMING_PCT") ? (u32)std::atoi(std::getenv("HCC_FORMING_PCT"))
+                                                  : kAdaptFormingPct;
   if (P.s0b) ensure_s0b(c, (n + 31) / 32);
   {
     const char* w = std::getenv("HCC_WALK");
@@ -1268,7 +1271,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   key.flags = o->flags;
   key.walk = P.walk;
   key.s0b = P.s0b;
-  key.plan = key.plan * 31 + (P.adapt ? 1000 + P.adapt_shift : 0);
+  key.plan = key.plan * 31 + (P.adapt ? 1000 + P.adapt_shift + 100000ull * P.forming_pct : 0);
   for (u64 x : P.bounds) key.plan = key.plan * 1000003ull + x;
 
   if (graph_mode) {
@@ -1665,6 +1668,83 @@ int hcc_forest_is_star(hcc_forest* f, int* out) {
 
 int hcc_forest_check_bound(hcc_forest* f, int* ok) {
   return forest_flag_kernel(f, false, ok);
+}
+
+// ---- device-side verification ----------------------------------------------------
+
+int hcc_forest_verify(hcc_ctx* c, const hcc_graph* g, hcc_forest* f,
+                      uint64_t* bad_edges, uint64_t* bad_vertices) {
+  if (!g || !f || !bad_edges || !bad_vertices) return fail(HCC_EINVAL, "null argument");
+  if (f->n != g->n) return fail(HCC_EINVAL, "forest size does not match the graph");
+  if (int r = ctx_enter(c)) return r;
+  HCC_GUARD_BEGIN
+  u64* d = reinterpret_cast<u64*>(&c->d_ctrl->wl_count[0]);  // two u64 scratch slots
+  HCC_CUDA(cudaMemsetAsync(d, 0, 2 * sizeof(u64), c->stream));
+  if (g->m)
+    k_verify_edges<<<grid_for(g->m, 256, (u64)c->sms * 32), 256, 0, c->stream>>>(
+        g->d_edges, g->m, f->d_pi, d);
+  if (f->n)
+    k_verify_canonical<<<grid_for(f->n, 256, (u64)c->sms * 32), 256, 0, c->stream>>>(
+        f->d_pi, f->n, d + 1);
+  HCC_CUDA(cudaGetLastError());
+  u64 h[2] = {0, 0};
+  HCC_CUDA(cudaMemcpyAsync(h, d, 2 * sizeof(u64), cudaMemcpyDeviceToHost, c->stream));
+  HCC_CUDA(cudaStreamSynchronize(c->stream));
+  *bad_edges = h[0];
+  *bad_vertices = h[1];
+  return HCC_OK;
+  HCC_GUARD_END
+}
+
+int hcc_labels_compare(hcc_ctx* c, const uint32_t* a, const uint32_t* b, uint64_t n,
+                       int* partition_equal, int* exact) {
+  if (!partition_equal || !exact || (n && (!a || !b))) return fail(HCC_EINVAL, "null argument");
+  if (int r = ctx_enter(c)) return r;
+  if (n == 0) {
+    *partition_equal = *exact = 1;
+    return HCC_OK;
+  }
+  u32 *da = nullptr, *db = nullptr;
+  u64 *k1 = nullptr, *k2 = nullptr, *cnt = nullptr;
+  void* tmp = nullptr;
+  auto cleanup = [&] {
+    cudaFree(da); cudaFree(db); cudaFree(k1); cudaFree(k2); cudaFree(cnt); cudaFree(tmp);
+  };
+  try {
+    cudaStream_t s = c->stream;
+    HCC_CUDA(cudaMalloc(&da, n * sizeof(u32)));
+    HCC_CUDA(cudaMalloc(&db, n * sizeof(u32)));
+    HCC_CUDA(cudaMalloc(&k1, n * sizeof(u64)));
+    HCC_CUDA(cudaMalloc(&k2, n * sizeof(u64)));
+    HCC_CUDA(cudaMalloc(&cnt, 4 * sizeof(u64)));
+    HCC_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(u64), s));
+    HCC_CUDA(cudaMemcpyAsync(da, a, n * sizeof(u32), cudaMemcpyHostToDevice, s));
+    HCC_CUDA(cudaMemcpyAsync(db, b, n * sizeof(u32), cudaMemcpyHostToDevice, s));
+    const unsigned grid = grid_for(n, 256, (u64)c->sms * 32);
+    size_t tb = 0;
+    // pairs (a, b): distinct pairs and distinct a
+    k_pair_keys<<<grid, 256, 0, s>>>(da, db, n, k1, cnt + 3);
+    HCC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, k1, k2, (int64_t)n, 0, 64, s));
+    HCC_CUDA(cudaMalloc(&tmp, tb));
+    HCC_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, k1, k2, (int64_t)n, 0, 64, s));
+    k_count_distinct<<<grid, 256, 0, s>>>(k2, n, 0, cnt + 0);
+    k_count_distinct<<<grid, 256, 0, s>>>(k2, n, 32, cnt + 1);
+    // pairs (b, a): distinct b
+    k_pair_keys<<<grid, 256, 0, s>>>(db, da, n, k1, cnt + 3);
+    HCC_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, k1, k2, (int64_t)n, 0, 64, s));
+    k_count_distinct<<<grid, 256, 0, s>>>(k2, n, 32, cnt + 2);
+    HCC_CUDA(cudaGetLastError());
+    u64 h[4];
+    HCC_CUDA(cudaMemcpyAsync(h, cnt, 4 * sizeof(u64), cudaMemcpyDeviceToHost, s));
+    HCC_CUDA(cudaStreamSynchronize(s));
+    *partition_equal = h[0] == h[1] && h[0] == h[2];
+    *exact = h[3] == 0;
+  } catch (const CudaFail& f) {
+    cleanup();
+    return f.code;
+  }
+  cleanup();
+  return HCC_OK;
 }
 
 // ---- multi-GPU merge primitives (kernels in hcc_multi.cu) ---------------------

@@ -96,4 +96,46 @@ __global__ void k_checksum(const uint2* e, u64 m, u64* out) {
   if ((threadIdx.x & 31u) == 0) atomicAdd(out, s);
 }
 
+__global__ void k_verify_edges(const uint2* e, u64 m, const u32* pi, u64* bad) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  u64 cnt = 0;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const uint2 x = e[i];
+    cnt += __ldcg(pi + x.x) != __ldcg(pi + x.y);
+  }
+  if (cnt) atomicAdd(bad, cnt);
+}
+
+__global__ void k_verify_canonical(const u32* pi, u64 n, u64* bad) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  u64 cnt = 0;
+  for (u64 v = (u64)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+    const u32 l = __ldcg(pi + v);
+    cnt += (l > (u32)v) || (__ldcg(pi + l) != l);
+  }
+  if (cnt) atomicAdd(bad, cnt);
+}
+
+// keys[i] = a[i] << 32 | b[i]; diff counts label mismatches (exactness)
+__global__ void k_pair_keys(const u32* a, const u32* b, u64 n, u64* keys, u64* diff) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  u64 cnt = 0;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    keys[i] = ((u64)a[i] << 32) | b[i];
+    cnt += a[i] != b[i];
+  }
+  if (cnt) atomicAdd(diff, cnt);
+}
+
+// distinct counts over sorted keys: [0] pairs, [1] first components
+__global__ void k_count_distinct(const u64* k, u64 n, int shift, u64* out) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  u64 cnt = 0;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const u64 x = shift ? (k[i] >> shift) : k[i];
+    cnt += i == 0 || (shift ? (k[i - 1] >> shift) : k[i - 1]) != x;
+  }
+  if (cnt) atomicAdd(out, cnt);
+}
+
 }  // namespace hcc

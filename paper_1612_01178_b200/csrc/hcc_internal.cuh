@@ -121,7 +121,7 @@ __global__ void k_step_worklist(DevCtrl* ctrl, DevRec* recs,
 __global__ void k_step_segment(DevCtrl* ctrl, DevRec* recs,
                                cudaGraphConditionalHandle h, int use_cond);
 __global__ void k_plan_begin(DevCtrl* ctrl, u64 m, u32 shift);
-__global__ void k_step_adapt(DevCtrl* ctrl, DevRec* recs, u64 m);
+__global__ void k_step_adapt(DevCtrl* ctrl, DevRec* recs, u64 m, u32 forming_pct);
 __global__ void k_step_outer(DevCtrl* ctrl, DevRec* recs,
                              cudaGraphConditionalHandle h, int use_cond);
 __global__ void k_step_jump(DevCtrl* ctrl, cudaGraphConditionalHandle h,
@@ -149,6 +149,12 @@ __global__ void k_gen_rmatx(uint2* out, u64 first, u64 count, u32 scale,
                             u64 seed, u32 ta, u32 tab, u32 tabc);
 __global__ void k_gen_erx(uint2* out, u64 first, u64 count, u64 n, u64 seed);
 __global__ void k_checksum(const uint2* e, u64 m, u64* out);
+
+// Verification (hcc_graph_kernels.cu).
+__global__ void k_verify_edges(const uint2* e, u64 m, const u32* pi, u64* bad);
+__global__ void k_verify_canonical(const u32* pi, u64 n, u64* bad);
+__global__ void k_pair_keys(const u32* a, const u32* b, u64 n, u64* keys, u64* diff);
+__global__ void k_count_distinct(const u64* k, u64 n, int shift, u64* out);
 
 // Multi-GPU merge (hcc_multi.cu).
 __global__ void k_export(const u32* pi, u64 n, u32* bits, uint2* pairs, u64 cap,

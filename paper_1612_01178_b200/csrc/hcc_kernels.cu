@@ -690,10 +690,10 @@ __global__ void k_plan_begin(DevCtrl* c, u64 m, u32 shift) {
 
 // Adaptive segment finished: choose the next range from this segment's
 // store ratio (records are per segment).
-__global__ void k_step_adapt(DevCtrl* c, DevRec* recs, u64 m) {
+__global__ void k_step_adapt(DevCtrl* c, DevRec* recs, u64 m, u32 forming_pct) {
   const DevRec& r = recs[c->rec < (u32)kMaxRecs ? c->rec : (u32)kMaxRecs - 1];
   const u64 len = c->seg_e - c->seg_b;
-  const bool forming = r.edges_in > 0 && r.edges_out * 100 > r.edges_in * kAdaptFormingPct;
+  const bool forming = r.edges_in > 0 && r.edges_out * 100 > r.edges_in * forming_pct;
   c->seg_b = c->seg_e;
   u64 next = forming ? len * kAdaptGrowth : m;
   if (next < 1) next = 1;

@@ -51,3 +51,9 @@ def test_reference_acceptance_on_b200(ctx):
     # criterion 5: the reference's own test bug, reproduced bit-for-bit
     assert lines[5] == "FAIL"
     assert "ascending pass recorded 999 jump steps, expected exactly 1000" in r.stdout
+
+
+def test_api_extras_on_b200(ctx):
+    exe = _need("api_extras")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
