@@ -1322,7 +1322,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
       pi, n, c->d_ctrl);
   if (o->flags & HCC_FLAG_CHECK_STAR)
     k_is_star<<<grid_for(n, 256, (u64)c->sms * 16), 256, 0, c->stream>>>(
-        pi, n, c->d_ctrl);
+        pi, n, &c->d_ctrl->flag);
   HCC_CUDA(cudaGetLastError());
   HCC_CUDA(cudaMemcpyAsync(c->h_ctrl, c->d_ctrl, sizeof(DevCtrl),
                            cudaMemcpyDeviceToHost, c->stream));
@@ -1638,26 +1638,19 @@ static int forest_flag_kernel(hcc_forest* f, bool star, int* out) {
   HCC_GUARD_BEGIN
   HCC_CUDA(cudaSetDevice(f->dev));
   u64* h = nullptr;
-  u64* d = thread_scratch(f->dev, &h);
-  // reuse the scratch as a DevCtrl-shaped flag holder: only ->flag is used
-  DevCtrl* dc = nullptr;
-  HCC_CUDA(cudaMalloc(&dc, sizeof(DevCtrl)));
-  HCC_CUDA(cudaMemsetAsync(dc, 0, sizeof(DevCtrl), cudaStreamPerThread));
-  unsigned grid = grid_for(f->n, 256, 4096);
+  u64* d = thread_scratch(f->dev, &h);  // per-thread device scratch word
+  u32* flag = reinterpret_cast<u32*>(d + 3);
+  HCC_CUDA(cudaMemsetAsync(flag, 0, sizeof(u32), cudaStreamPerThread));
+  const unsigned grid = grid_for(f->n, 256, 4096);
   if (star)
-    k_is_star<<<grid, 256, 0, cudaStreamPerThread>>>(f->d_pi, f->n, dc);
+    k_is_star<<<grid, 256, 0, cudaStreamPerThread>>>(f->d_pi, f->n, flag);
   else
-    k_check_bound<<<grid, 256, 0, cudaStreamPerThread>>>(f->d_pi, f->n, dc);
-  cudaError_t le = cudaGetLastError();
-  u32 flag = 0;
-  cudaError_t ce = cudaMemcpyAsync(&flag, &dc->flag, sizeof(u32),
-                                   cudaMemcpyDeviceToHost, cudaStreamPerThread);
-  cudaError_t se = cudaStreamSynchronize(cudaStreamPerThread);
-  cudaFree(dc);
-  (void)d;
-  if (le != cudaSuccess || ce != cudaSuccess || se != cudaSuccess)
-    return fail(HCC_ECUDA, "flag kernel failed");
-  *out = flag ? 0 : 1;
+    k_check_bound<<<grid, 256, 0, cudaStreamPerThread>>>(f->d_pi, f->n, flag);
+  HCC_CUDA(cudaGetLastError());
+  HCC_CUDA(cudaMemcpyAsync(h + 3, flag, sizeof(u32), cudaMemcpyDeviceToHost,
+                           cudaStreamPerThread));
+  HCC_CUDA(cudaStreamSynchronize(cudaStreamPerThread));
+  *out = (*reinterpret_cast<u32*>(h + 3)) ? 0 : 1;
   return HCC_OK;
   HCC_GUARD_END
 }

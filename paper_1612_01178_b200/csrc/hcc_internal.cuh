@@ -128,8 +128,8 @@ __global__ void k_step_jump(DevCtrl* ctrl, cudaGraphConditionalHandle h,
                             int use_cond);
 __global__ void k_set_cond(cudaGraphConditionalHandle h, u32 value);
 __global__ void k_count_roots(const u32* pi, u64 n, DevCtrl* ctrl);
-__global__ void k_is_star(const u32* pi, u64 n, DevCtrl* ctrl);
-__global__ void k_check_bound(const u32* pi, u64 n, DevCtrl* ctrl);
+__global__ void k_is_star(const u32* pi, u64 n, u32* flag);
+__global__ void k_check_bound(const u32* pi, u64 n, u32* flag);
 
 // Element kernels (single thread) for the ParentForest API.
 enum ElemOp : int {

@@ -735,24 +735,24 @@ __global__ void k_count_roots(const u32* pi, u64 n, DevCtrl* ctrl) {
   add_counter(&ctrl->components, cnt);
 }
 
-// flag != 0 iff some v has pi(pi(v)) != pi(v).
-__global__ void k_is_star(const u32* pi, u64 n, DevCtrl* ctrl) {
+// *flag != 0 iff some v has pi(pi(v)) != pi(v).
+__global__ void k_is_star(const u32* pi, u64 n, u32* flag) {
   u32 bad = 0;
   const u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 v = (u64)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
     u32 p = pi[v];
     bad |= (pi[p] != p);
   }
-  if (__syncthreads_or(bad) && threadIdx.x == 0) ctrl->flag = 1;
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
 }
 
-// flag != 0 iff some v has pi(v) > v.
-__global__ void k_check_bound(const u32* pi, u64 n, DevCtrl* ctrl) {
+// *flag != 0 iff some v has pi(v) > v.
+__global__ void k_check_bound(const u32* pi, u64 n, u32* flag) {
   u32 bad = 0;
   const u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 v = (u64)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride)
     bad |= (pi[v] > (u32)v);
-  if (__syncthreads_or(bad) && threadIdx.x == 0) ctrl->flag = 1;
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
 }
 
 // ---- element kernels for the ParentForest API ------------------------------
