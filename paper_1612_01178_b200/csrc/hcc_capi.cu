@@ -356,9 +356,9 @@ HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
 // Enqueue one full CC run (pi init through convergence) on seq.
 void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
   c->seg_ev_used = 0;
-  k_begin<<<1, 1, 0, q.s()>>>(c->d_ctrl, c->d_recs, P.nseg);
-  k_init_pi<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n,
-                                                      P.s0b ? c->s0b : nullptr);
+  k_start<<<P.grid_vert, P.block_vert, 0, q.s()>>>(
+      P.pi, P.n, P.s0b ? c->s0b : nullptr, c->d_ctrl, c->d_recs, P.nseg, P.m,
+      P.adapt ? P.adapt_shift : 64u);
   HCC_CUDA(cudaGetLastError());
   DevCtrl* ctrl = c->d_ctrl;
   DevRec* recs = c->d_recs;
@@ -401,7 +401,6 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           HCC_CUDA(cudaEventCreate(&ev));
           c->seg_ev.push_back(ev);
         }
-        if (P.adapt) k_plan_begin<<<1, 1, 0, q.s()>>>(ctrl, P.m, P.adapt_shift);
         for (u64 sgi = 0; sgi < P.nseg; ++sgi) {
           HookArgs ha = hook_args(c, P, P.adapt ? kSrcCtrlRange : kSrcRange, 1);
           ha.b = P.bounds[sgi];
@@ -419,7 +418,8 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           }
           q.record(c->seg_ev[2 * sgi + 1]);
           q.phase_done(HCC_PHASE_HOOK);
-          if (P.s0b)  // compress + star-0 bitmap (bitmap initialised by k_init_pi)
+          // compress (+ star-0 bitmap, initialised by k_start)
+          if (P.s0b)
             k_compress_s0b<<<grid_for((P.n + 7) / 8, kVertThreads, 0x7fffffffull),
                              kVertThreads, 0, q.s()>>>(P.pi, P.n, ctrl, recs, c->s0b,
                                                        kCompressIfDirty);
@@ -427,6 +427,8 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
             k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
                                                                 recs, 1);
           q.phase_done(HCC_PHASE_COMPRESS);
+          // (a step folded into the compress's last block costs one
+          // single-address atomic per compress block: slower than a launch)
           if (P.adapt)
             k_step_adapt<<<1, 1, 0, q.s()>>>(ctrl, recs, P.m, P.forming_pct);
           else
@@ -1370,10 +1372,10 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   {
     // kernels launched by the run (loop iterations from the device records)
     const u64 iters = nrec;
-    u64 k = 2;  // k_begin, k_init_pi
+    u64 k = 1;  // k_start
     if (o->algo == HCC_ALGO_BASELINE_MJ && !P.full_passes && !P.bounds.empty()) {
       const u64 wl = nrec > nseg ? nrec - nseg : 0;
-      k += 3 * nseg + 1 + 3 * wl;  // hook+compress+step; k_set_cond; wl passes
+      k += 3 * nseg + 1 + 3 * wl;  // hook+compress+step per slot; k_set_cond; wl passes
     } else {
       k += 1 + 3 * iters;  // k_set_cond + hook/compress(or jump)/step per record
     }
@@ -1827,7 +1829,7 @@ int hcc_rehook(hcc_ctx* c, hcc_forest* f, const uint32_t* dev_bits_or,
   out.passes = c->h_ctrl->passes;
   out.outer_iterations = c->h_ctrl->passes;
   out.edges_processed = c->h_ctrl->edges_processed;
-  out.kernels = 3 + 3 * c->h_ctrl->passes;
+  out.kernels = 2 + 3 * c->h_ctrl->passes;
   if (mx) *mx = out;
   return HCC_OK;
   HCC_GUARD_END

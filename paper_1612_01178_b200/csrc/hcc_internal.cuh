@@ -115,12 +115,13 @@ __global__ void k_compress(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
                            int skip_if_clean);
 __global__ void k_compress_s0b(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
                                u32* bits, int skip_if_clean);
+__global__ void k_start(u32* pi, u64 n, u32* bits, DevCtrl* ctrl, DevRec* recs, u64 nseg,
+                        u64 m, u32 plan_shift);
 __global__ void k_jump(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs);
 __global__ void k_step_worklist(DevCtrl* ctrl, DevRec* recs,
                                 cudaGraphConditionalHandle h, int use_cond);
 __global__ void k_step_segment(DevCtrl* ctrl, DevRec* recs,
                                cudaGraphConditionalHandle h, int use_cond);
-__global__ void k_plan_begin(DevCtrl* ctrl, u64 m, u32 shift);
 __global__ void k_step_adapt(DevCtrl* ctrl, DevRec* recs, u64 m, u32 forming_pct);
 __global__ void k_step_outer(DevCtrl* ctrl, DevRec* recs,
                              cudaGraphConditionalHandle h, int use_cond);

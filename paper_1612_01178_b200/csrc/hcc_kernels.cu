@@ -234,6 +234,35 @@ __global__ void k_begin(DevCtrl* ctrl, DevRec* recs, u64 nseg) {
   }
 }
 
+// Run start: control block + first record (k_begin), the adaptive plan's
+// first range (plan_shift < 64), and pi(v) = v + the star-0 bitmap
+// (k_init_pi), in one launch.
+__global__ void k_start(u32* pi, u64 n, u32* bits, DevCtrl* ctrl, DevRec* recs, u64 nseg,
+                        u64 m, u32 plan_shift) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    DevCtrl c = {};
+    c.nseg = nseg ? nseg : 1;
+    if (plan_shift < 64) {
+      u64 first = m >> plan_shift;
+      if (first == 0) first = m < 1 ? m : 1;
+      c.seg_e = first;
+    }
+    *ctrl = c;
+    rec_clear(recs[0]);
+  }
+  const u64 tid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  if (bits)
+    for (u64 w = tid; w < ((n + 31) >> 5); w += stride) bits[w] = w == 0 ? 1u : 0u;
+  const u64 n4 = n >> 2;
+  uint4* p4 = reinterpret_cast<uint4*>(pi);
+  for (u64 i = tid; i < n4; i += stride) {
+    const u32 v = (u32)(i << 2);
+    p4[i] = make_uint4(v, v + 1, v + 2, v + 3);
+  }
+  for (u64 v = (n4 << 2) + tid; v < n; v += stride) pi[v] = (u32)v;
+}
+
 // pi(v) = v (ParentForest::reset, forest.hpp:25-28), 16-byte stores.  With
 // a star-0 bitmap, also its initial state (only vertex 0 is in star 0).
 __global__ void k_init_pi(u32* pi, u64 n, u32* bits) {
@@ -679,13 +708,6 @@ __global__ void k_step_segment(DevCtrl* c, DevRec* recs,
   const u32 cond = guard(c, c->seg < c->nseg ? 1u : 0u);
   c->cond = cond;
   if (use_cond) cudaGraphSetConditional(h, cond);
-}
-
-__global__ void k_plan_begin(DevCtrl* c, u64 m, u32 shift) {
-  u64 first = shift >= 63 ? 0 : (m >> shift);
-  if (first == 0) first = m < 1 ? m : 1;
-  c->seg_b = 0;
-  c->seg_e = first;
 }
 
 // Adaptive segment finished: choose the next range from this segment's
