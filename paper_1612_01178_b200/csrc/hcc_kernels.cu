@@ -608,22 +608,56 @@ __global__ void __launch_bounds__(kVertThreads)
   if (v0 + 8 <= n) {
     const uint4* p4 = reinterpret_cast<const uint4*>(pi) + (q << 1);
     const uint4 pa = __ldcg(p4), pb = __ldcg(p4 + 1);
-    u32 p[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
-    u32 gp[8];
+    u32 a[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+    // pi(v) <= v, so a parent inside this group is an earlier vertex of it:
+    // those vertices take their parent's root after the chases (ascending,
+    // as the reference's sequential pass would; grid rows chain this way).
+    u32 dep = 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) gp[j] = p[j] != (u32)v0 + j ? ld_pi(pi + p[j]) : p[j];
+    for (int j = 1; j < 8; ++j)
+      dep |= (a[j] >= (u32)v0 && a[j] < (u32)v0 + j) ? 1u << j : 0u;
+    u32 b[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      u32 a = p[j], b = gp[j];
-      if (j > 0 && a >= (u32)v0 && a != (u32)v0 + j) b = ld_fresh(pi + a);
-      while (b != a) {
-        pi[v0 + j] = b;
-        ++steps;
-        a = b;
-        b = ld_fresh(pi + a);
-      }
-      byte |= (a == 0u) ? 1u << j : 0u;
+    for (int j = 0; j < 8; ++j)
+      b[j] = (a[j] != (u32)v0 + j && !(dep & (1u << j))) ? ld_pi(pi + a[j]) : a[j];
+    // The remaining chases advance in lockstep (one level per round, up to
+    // eight independent loads in flight) instead of one after another: in
+    // the forming segments the trees are deep and a serial chase is one
+    // dependent L2 round trip per level.  Each level is still written
+    // eagerly; values read from other chasers' slots are ancestors, so a
+    // stale read only costs an extra round.
+    u32 act = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) act |= (b[j] != a[j]) ? 1u << j : 0u;
+    while (act) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (act & (1u << j)) {
+          pi[v0 + j] = b[j];
+          ++steps;
+          a[j] = b[j];
+          b[j] = ld_fresh(pi + a[j]);
+        }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (b[j] == a[j]) act &= ~(1u << j);
     }
+#pragma unroll
+    for (int j = 1; j < 8; ++j) {
+      if (dep & (1u << j)) {
+        u32 root = a[0];
+#pragma unroll
+        for (int k = 1; k < j; ++k)
+          if (a[j] == (u32)v0 + k) root = a[k];
+        if (root != a[j]) {
+          pi[v0 + j] = root;
+          ++steps;
+          a[j] = root;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) byte |= (a[j] == 0u) ? 1u << j : 0u;
   } else if (v0 < n) {
     for (u64 v = v0; v < n; ++v) {
       u32 a = ld_fresh(pi + v);
