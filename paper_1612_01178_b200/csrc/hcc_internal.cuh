@@ -23,7 +23,10 @@ typedef unsigned int u32;
 
 constexpr int kMaxRecs = 4096;    // per-run phase records kept on device
 constexpr int kHookThreads = 256;
-constexpr int kHookEPT = 8;       // edges per thread per tile (4 x uint4)
+#ifndef HCC_HOOK_EPT
+#define HCC_HOOK_EPT 8
+#endif
+constexpr int kHookEPT = HCC_HOOK_EPT;  // edges per thread per tile (4 x uint4)
 constexpr int kVertThreads = 256;
 
 // One record per hook+compress phase pair (segment, outer iteration or

@@ -77,6 +77,11 @@ __device__ __forceinline__ u32 ld_bits(const u32* p) {
 #endif
 }
 
+// Same-round store visibility between a thread's walks (see hook_impl).
+#ifndef HCC_HOOK_DEDUP
+#define HCC_HOOK_DEDUP 0
+#endif
+
 // Coherent (L2) read: sees other threads' stores made during this kernel.
 __device__ __forceinline__ u32 ld_fresh(const u32* p) { return __ldcg(p); }
 
@@ -424,41 +429,60 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
     // made regardless (it may overwrite a transient link; the worklist
     // records it).  This removes the redundant stores that single-level
     // reads make to hub slots while the hub structure forms.
-    u32 act = 0;
+    // The EPT walks of a thread advance in lockstep, one level per round
+    // with all their loads in flight (in the forming segments a walk is
+    // several dependent round trips).
+    u32 walking = 0;
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
-      if (pu[k] == pv[k]) continue;
-      u32 x = pu[k], y = pv[k];
-      u32 h = max(x, y), l = min(x, y);
-      bool store = true, at_root = a.walk == 0;
-      for (int step = 0; step < a.walk; ++step) {
-        // L1-cached read: any value the slot ever held is a recorded link
-        // (pass-start link or a worklist pair), so a stale value is a safe
-        // basis for both "drop" and "descend"; reading through L1 keeps the
-        // hub slots every edge touches off the L2 slices.
-        const u32 ph = ld_pi(pi + h);
-        if (ph == h) {                  // root: store below
-          at_root = true;
-          break;
+      const u32 x = pu[k], y = pv[k];
+      pu[k] = max(x, y);  // h
+      pv[k] = min(x, y);  // l
+      walking |= x != y ? 1u << k : 0u;
+    }
+    u32 act = walking, roots = a.walk == 0 ? walking : 0u;
+    for (int step = 0; step < a.walk && walking; ++step) {
+      // L1-cached read: any value the slot ever held is a recorded link
+      // (pass-start link or a worklist pair), so a stale value is a safe
+      // basis for both "drop" and "descend"; reading through L1 keeps the
+      // hub slots every edge touches off the L2 slices.
+      u32 ph[EPT];
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) ph[k] = walking & (1u << k) ? ld_pi(pi + pu[k]) : 0u;
+      u32 fresh = 0;  // edges that stored in this round
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        if (!(walking & (1u << k))) continue;
+        // A root this thread linked earlier in the round: see that store,
+        // as a one-edge-at-a-time walk would (stores of earlier rounds are
+        // seen through memory).
+        u32 p = ph[k];
+#if HCC_HOOK_DEDUP
+#pragma unroll
+        for (int k2 = 0; k2 < k; ++k2)
+          if ((fresh & (1u << k2)) && pu[k2] == pu[k]) p = pv[k2];
+#endif
+        if (p == pu[k]) {               // root: store now
+          pi[pu[k]] = pv[k];
+          fresh |= 1u << k;
+          walking &= ~(1u << k);
+        } else if (p == pv[k]) {        // already linked
+          act &= ~(1u << k);
+          walking &= ~(1u << k);
+        } else {
+          const u32 l = pv[k];
+          pu[k] = max(p, l);
+          pv[k] = min(p, l);
         }
-        if (ph == l) {                  // already linked
-          store = false;
-          break;
-        }
-        h = max(ph, l);
-        l = min(ph, l);
-      }
-      if (store) {
-        // A walk that ran out of steps defers the pair to the worklist
-        // without storing: h may be an interior vertex whose link existed
-        // at pass start (the forest need not be a star), and only slots
-        // observed as roots may be written.
-        if (at_root) pi[h] = l;
-        pu[k] = h;
-        pv[k] = l;
-        act |= 1u << k;
       }
     }
+    // A walk that ran out of steps defers the pair to the worklist without
+    // storing: h may be an interior vertex whose link existed at pass start
+    // (the forest need not be a star), and only slots observed as roots may
+    // be written.
+#pragma unroll
+    for (int k = 0; k < EPT; ++k)
+      if (roots & (1u << k)) pi[pu[k]] = pv[k];
     if (a.append) {
       u64 pos;
       if (block_reserve(__popc(act), cnt_out, pos, appended)) {
@@ -481,7 +505,10 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
   block_t1(&r->hook_t1);
 }
 
-__global__ void __launch_bounds__(kHookThreads, 4) k_hook(HookArgs a) {
+#ifndef HCC_HOOK_MINB
+#define HCC_HOOK_MINB 4
+#endif
+__global__ void __launch_bounds__(kHookThreads, HCC_HOOK_MINB) k_hook(HookArgs a) {
   hook_impl<kHookEPT>(a);
 }
 
