@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define HCC_ABI_VERSION 1
+#define HCC_ABI_VERSION 2
 
 typedef enum hcc_status {
   HCC_OK = 0,
@@ -70,6 +70,11 @@ typedef enum hcc_algo {
 #define HCC_FLAG_NO_GRAPH      0x4u /* launch kernels directly, no CUDA graph*/
 #define HCC_FLAG_CHECK_STAR    0x8u /* verify the final forest is a star
                                        (extract_labels' debug check)        */
+#define HCC_FLAG_HOOK_EVENTS   0x10u /* record CUDA events around every
+                                       unrolled topology hook launch
+                                       (hcc_segment_rec.hook_event_ms; each
+                                       event node costs ~5 us of graph
+                                       latency, so it is off by default)    */
 
 /* Phase identifiers passed to the observer; reference Phase enum
  * (engines.hpp:84). */
@@ -141,6 +146,10 @@ typedef struct hcc_segment_rec {
   double hook_event_ms;     /* hook kernel time from CUDA events recorded
                                around the launch on the launch stream (the
                                unrolled topology segments); -1 if not taken */
+  /* Device timeline (globaltimer, ms since the run's first kernel started):
+     first sampled block start / last block end of the hook and compress
+     launches of this record; -1 if the phase did not run. */
+  double hook_start_ms, hook_end_ms, compress_start_ms, compress_end_ms;
 } hcc_segment_rec;
 
 /* Reference GraphStats (graph.hpp:33-40), computed on the device. */

@@ -20,6 +20,7 @@ ALGO_BASELINE, ALGO_BASELINE_MJ, ALGO_ATOMIC, ALGO_ADAPTIVE = range(4)
 ALGOS = {"baseline": ALGO_BASELINE, "baseline-mj": ALGO_BASELINE_MJ,
          "atomic": ALGO_ATOMIC, "adaptive": ALGO_ADAPTIVE}
 FLAG_FULL_PASSES, FLAG_HOST_LOOP, FLAG_NO_GRAPH, FLAG_CHECK_STAR = 0x1, 0x2, 0x4, 0x8
+FLAG_HOOK_EVENTS = 0x10
 PHASE_HOOK, PHASE_COMPRESS = 0, 1
 
 u64, u32, i32 = C.c_uint64, C.c_uint32, C.c_int
@@ -48,7 +49,9 @@ class Metrics(C.Structure):
 
 class SegmentRec(C.Structure):
     _fields_ = [("hook_ms", C.c_double), ("compress_ms", C.c_double), ("counters", Counters),
-                ("edges_in", u64), ("edges_out", u64), ("hook_event_ms", C.c_double)]
+                ("edges_in", u64), ("edges_out", u64), ("hook_event_ms", C.c_double),
+                ("hook_start_ms", C.c_double), ("hook_end_ms", C.c_double),
+                ("compress_start_ms", C.c_double), ("compress_end_ms", C.c_double)]
 
 
 class GraphStats(C.Structure):
@@ -183,7 +186,10 @@ class Context:
                             cas_failures=r.counters.cas_failures,
                             jump_steps=r.counters.jump_steps,
                             edges_in=r.edges_in, edges_out=r.edges_out,
-                            hook_event_ms=r.hook_event_ms))
+                            hook_event_ms=r.hook_event_ms,
+                            hook_start_ms=r.hook_start_ms, hook_end_ms=r.hook_end_ms,
+                            compress_start_ms=r.compress_start_ms,
+                            compress_end_ms=r.compress_end_ms))
         return out
 
     # -- graphs --

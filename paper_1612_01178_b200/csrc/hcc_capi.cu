@@ -85,6 +85,9 @@ constexpr u64 kMaxUnrolledSegments = 64;
 constexpr int kDefaultWalk = 32;
 // First adaptive topology segment = m >> kAdaptShift (HCC_PLAN=adapt:<k>).
 constexpr u32 kAdaptShift = 7;
+// Unrolled adaptive slots (HCC_PLAN=adapt:<k>:<slots>); the last takes every
+// remaining edge, so a plan never needs an empty trailing launch.
+constexpr int kAdaptSlots = 4;
 
 int usable_devices() {
   int count = 0;
@@ -285,13 +288,19 @@ struct Seq {
     size_t nd = 0;
     HCC_CUDA(cudaStreamGetCaptureInfo(s(), &st, nullptr, &g, &deps, &nd));
     cudaGraphConditionalHandle h;
-    HCC_CUDA(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
-    // An upstream kernel arms the condition on every entry, so a nested
-    // loop re-runs after an earlier pass left its condition at 0 (default
-    // values are only applied at top-level graph launch).
-    k_set_cond<<<1, 1, 0, s()>>>(h, 1u);
-    HCC_CUDA(cudaGetLastError());
-    HCC_CUDA(cudaStreamGetCaptureInfo(s(), &st, nullptr, &g, &deps, &nd));
+    if (depth == 0) {
+      // top-level loop: the default value 1 is applied at every launch of
+      // the root graph, so the body runs at least once without a kernel
+      HCC_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    } else {
+      // An upstream kernel arms the condition on every entry, so a nested
+      // loop re-runs after an earlier pass left its condition at 0 (default
+      // values are only applied at top-level graph launch).
+      HCC_CUDA(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+      k_set_cond<<<1, 1, 0, s()>>>(h, 1u);
+      HCC_CUDA(cudaGetLastError());
+      HCC_CUDA(cudaStreamGetCaptureInfo(s(), &st, nullptr, &g, &deps, &nd));
+    }
     cudaGraphNodeParams p = {};
     p.type = cudaGraphNodeTypeConditional;
     p.conditional.handle = h;
@@ -329,6 +338,7 @@ struct Plan {
   std::vector<u64> bounds;  // unrolled topology segment boundaries (nseg+1)
   int walk;
   bool s0b;                 // star-0 bitmap for hook passes after a compress
+  bool hook_events = false;  // CUDA events around unrolled hook launches
   bool adapt;               // device-side adaptive topology plan
   u32 adapt_shift;          // first adaptive segment = m >> adapt_shift
   u32 forming_pct;          // store ratio (%) above which a segment is forming
@@ -406,7 +416,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           ha.b = P.bounds[sgi];
           ha.e = P.bounds[sgi + 1];
           if (P.s0b && sgi >= 1) ha.s0b = c->s0b;
-          q.record(c->seg_ev[2 * sgi]);
+          if (P.hook_events) q.record(c->seg_ev[2 * sgi]);
           const u64 seg_edges = ha.e - ha.b;  // adaptive: the static estimate
           if (P.block_hook == kHookThreads &&
               seg_edges < (u64)P.grid_hook * kHookThreads * kHookEPT * 2) {
@@ -416,7 +426,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           } else {
             k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(ha);
           }
-          q.record(c->seg_ev[2 * sgi + 1]);
+          if (P.hook_events) q.record(c->seg_ev[2 * sgi + 1]);
           q.phase_done(HCC_PHASE_HOOK);
           // compress (+ star-0 bitmap, initialised by k_start)
           if (P.s0b)
@@ -434,7 +444,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           else
             k_step_segment<<<1, 1, 0, q.s()>>>(ctrl, recs, 0, 0);
         }
-        c->seg_ev_used = P.nseg;
+        c->seg_ev_used = P.hook_events ? P.nseg : 0;
       } else {
         q.loop([&](cudaGraphConditionalHandle h, int u) {
           k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(
@@ -1147,11 +1157,18 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
       // device-side adaptive plan: launches are unrolled up to the number a
       // x4-growth schedule can need; ranges past the end are empty no-ops
       adapt = true;
-      if (pe && std::sscanf(pe, "adapt:%d", &sh) == 1 && sh >= 0 && sh < 40)
-        adapt_shift = (u32)sh;
+      int slots = kAdaptSlots;
+      if (pe) {
+        int sl = 0;
+        const int got = std::sscanf(pe, "adapt:%d:%d", &sh, &sl);
+        if (got >= 1 && sh >= 0 && sh < 40) adapt_shift = (u32)sh;
+        if (got == 2 && sl >= 1 && sl <= (int)kMaxUnrolledSegments) slots = sl;
+      }
+      // at most `slots` launches; the device gives the last one every
+      // remaining edge (k_step_adapt)
       u64 first = std::max<u64>(1, m >> adapt_shift), len = first, covered = first;
       nseg = 1;
-      while (covered < m && nseg < kMaxUnrolledSegments) {
+      while (covered < m && nseg < (u64)slots) {
         len = std::min<u64>(len * kAdaptGrowth, m - covered);
         covered += len;
         ++nseg;
@@ -1210,6 +1227,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   P.s0b = s0b && !bounds.empty();
   P.adapt = adapt;
   P.adapt_shift = adapt_shift;
+  P.hook_events = (o->flags & HCC_FLAG_HOOK_EVENTS) != 0;
   P.forming_pct = std::getenv("HCC_FORMING_PCT") ? (u32)std::atoi(std::getenv("HCC_FORMING_PCT"))
                                                   : kAdaptFormingPct;
   if (P.s0b) ensure_s0b(c, (n + 31) / 32);
@@ -1352,6 +1370,16 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
     sr.counters.jump_steps = r.jump_steps;
     sr.edges_in = r.edges_in;
     sr.edges_out = r.edges_out;
+    auto rel = [&](u64 t) {
+      return (t == 0 || t == ~0ull || hc.t_start == 0) ? -1.0
+                                                       : (double)(int64_t)(t - hc.t_start) * 1e-6;
+    };
+    const bool hk = r.hook_t1 > r.hook_t0 && r.hook_t0 != ~0ull;
+    const bool cp = r.comp_t1 > r.comp_t0 && r.comp_t0 != ~0ull;
+    sr.hook_start_ms = hk ? rel(r.hook_t0) : -1.0;
+    sr.hook_end_ms = hk ? rel(r.hook_t1) : -1.0;
+    sr.compress_start_ms = cp ? rel(r.comp_t0) : -1.0;
+    sr.compress_end_ms = cp ? rel(r.comp_t1) : -1.0;
     sr.hook_event_ms = -1.0;
     if (i < c->seg_ev_used) {
       float ems = 0.f;
@@ -1375,9 +1403,9 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
     u64 k = 1;  // k_start
     if (o->algo == HCC_ALGO_BASELINE_MJ && !P.full_passes && !P.bounds.empty()) {
       const u64 wl = nrec > nseg ? nrec - nseg : 0;
-      k += 3 * nseg + 1 + 3 * wl;  // hook+compress+step per slot; k_set_cond; wl passes
+      k += 3 * nseg + 3 * wl;  // hook+compress+step per slot and per wl pass
     } else {
-      k += 1 + 3 * iters;  // k_set_cond + hook/compress(or jump)/step per record
+      k += 3 * iters;  // hook/compress(or jump)/step per record
     }
     out.kernels = k;
   }

@@ -55,6 +55,7 @@ struct DevCtrl {
   u32 flag;          // scratch result flag (is_star / bound checks)
   u64 loop_steps;    // loop-step kernels executed (runaway guard)
   u64 seg_b, seg_e;  // adaptive topology plan: current segment range
+  u64 t_start;       // globaltimer at k_start (span timeline origin)
 };
 
 // k_compress_s0b modes.

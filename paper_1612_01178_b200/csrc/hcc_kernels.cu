@@ -247,9 +247,11 @@ __global__ void k_start(u32* pi, u64 n, u32* bits, DevCtrl* ctrl, DevRec* recs, 
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     DevCtrl c = {};
     c.nseg = nseg ? nseg : 1;
+    c.t_start = gtime();
     if (plan_shift < 64) {
       u64 first = m >> plan_shift;
       if (first == 0) first = m < 1 ? m : 1;
+      if (c.nseg <= 1) first = m;  // a single slot takes every edge
       c.seg_e = first;
     }
     *ctrl = c;
@@ -780,6 +782,7 @@ __global__ void k_step_adapt(DevCtrl* c, DevRec* recs, u64 m, u32 forming_pct) {
   c->seg_b = c->seg_e;
   u64 next = forming ? len * kAdaptGrowth : m;
   if (next < 1) next = 1;
+  if (c->seg + 2 >= c->nseg) next = m;  // the next slot is the last one
   c->seg_e = (m - c->seg_b) <= next ? m : c->seg_b + next;
   c->seg += 1;
   c->passes += (len > 0);

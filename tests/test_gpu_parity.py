@@ -479,6 +479,32 @@ def test_star0_bitmap_paths(ctx, oracle, spec):
                 os.environ.pop(k, None)
 
 
+def test_hook_events_flag_and_timeline(ctx, oracle, capi):
+    """HCC_FLAG_HOOK_EVENTS adds per-launch CUDA events (bench roofline) without
+    changing results; the device timeline is ordered hook -> compress -> next."""
+    g = ctx.generate("rmatx:scale=20,ef=16,seed=3")
+    want = oracle.cc(g.n, g.edges())
+    for flags in (0, capi.FLAG_HOOK_EVENTS):
+        lab, mx = ctx.cc(g, "baseline-mj", flags=flags)
+        assert np.array_equal(lab, want)
+        segs = ctx.segments()
+        used = [s for s in segs[:mx["s"]] if s["edges_in"] > 0]
+        assert used
+        for s in used:
+            assert (s["hook_event_ms"] >= 0) == bool(flags)
+        prev = 0.0
+        for s in segs:
+            if s["hook_start_ms"] < 0:
+                continue
+            assert prev <= s["hook_start_ms"] <= s["hook_end_ms"], segs
+            prev = s["hook_end_ms"]
+            if s["compress_start_ms"] >= 0:
+                assert s["hook_end_ms"] <= s["compress_start_ms"] <= s["compress_end_ms"]
+                prev = s["compress_end_ms"]
+        assert prev <= mx["total_ms"] + 0.05
+    g.close()
+
+
 def test_graph_assign_reuses_handle(ctx, oracle):
     """hcc_graph_assign_edges_u32 refills a handle; results track the new edges
     and the out-of-range check still applies."""

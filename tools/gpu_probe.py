@@ -77,7 +77,10 @@ def timing(ctx, spec, reps=5, check=True, variants=None):
              gteps=m / best["total_ms"] / 1e6, alg_gbs=(16 * m + 12 * g.n) / best["total_ms"] / 1e6,
              outer=best["outer_iterations"], s=best["s"], edges_processed=best["edges_processed"],
              segs=[(round(s["hook_ms"], 4), round(s["compress_ms"], 4), s["edges_in"], s["edges_out"],
-                    s["jump_steps"]) for s in best["segs"]][:24])
+                    s["jump_steps"]) for s in best["segs"]][:24],
+             timeline=[tuple(round(s[k], 4) for k in ("hook_start_ms", "hook_end_ms",
+                                                      "compress_start_ms", "compress_end_ms"))
+                       for s in best["segs"]][:24])
     g.close()
 
 
