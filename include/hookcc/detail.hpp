@@ -63,7 +63,15 @@ inline hcc_ctx* ctx() {
     }
   };
   thread_local Holder h;
-  if (!h.c) check(hcc_create(default_device(), &h.c));
+  if (!h.c) {
+    // structs cross the boundary by value: refuse a library built against
+    // another revision of hookcc_c.h
+    if (hcc_abi_version() != HCC_ABI_VERSION)
+      throw std::runtime_error("libhookcc_cuda.so ABI " + std::to_string(hcc_abi_version()) +
+                               " != header ABI " + std::to_string(HCC_ABI_VERSION) +
+                               " (rebuild the binary)");
+    check(hcc_create(default_device(), &h.c));
+  }
   return h.c;
 }
 

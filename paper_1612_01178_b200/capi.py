@@ -21,6 +21,7 @@ ALGOS = {"baseline": ALGO_BASELINE, "baseline-mj": ALGO_BASELINE_MJ,
          "atomic": ALGO_ATOMIC, "adaptive": ALGO_ADAPTIVE}
 FLAG_FULL_PASSES, FLAG_HOST_LOOP, FLAG_NO_GRAPH, FLAG_CHECK_STAR = 0x1, 0x2, 0x4, 0x8
 FLAG_HOOK_EVENTS = 0x10
+ABI_VERSION = 2  # HCC_ABI_VERSION of include/hookcc_c.h
 PHASE_HOOK, PHASE_COMPRESS = 0, 1
 
 u64, u32, i32 = C.c_uint64, C.c_uint32, C.c_int
@@ -130,6 +131,8 @@ def lib() -> C.CDLL:
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
+        if L.hcc_abi_version() != ABI_VERSION:  # structs are mirrored below
+            raise ImportError(f"{path}: ABI {L.hcc_abi_version()} != binding ABI {ABI_VERSION}")
         _lib = L
     return _lib
 

@@ -119,11 +119,12 @@ struct GraphKey {
   int walk = 0;
   u64 plan = 0;
   bool s0b = false;
+  bool sum = false;
   bool operator==(const GraphKey& o) const {
     return algo == o.algo && edges == o.edges && pi == o.pi && wl0 == o.wl0 &&
            n == o.n && m == o.m && nseg == o.nseg &&
            max_threads == o.max_threads && flags == o.flags && walk == o.walk &&
-           plan == o.plan && s0b == o.s0b;
+           plan == o.plan && s0b == o.s0b && sum == o.sum;
   }
 };
 
@@ -140,7 +141,7 @@ struct hcc_ctx {
   uint2* wl[2] = {nullptr, nullptr};
   u64 wl_cap = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  int occ_hook = 1, occ_vert = 1;
+  int occ_hook = 1, occ_vert = 1, occ_hook_sum = 1;
   // cached executable graph for repeated calls with identical arguments
   cudaGraphExec_t exec = nullptr;
   GraphKey key;
@@ -151,6 +152,8 @@ struct hcc_ctx {
   u64 exec_seg_ev = 0;  // seg_ev_used of the cached executable graph
   u32* s0b = nullptr;  // star-0 bitmap
   u64 s0b_words = 0;
+  u32* s0f = nullptr;  // star-0 summary (one bit per group of bitmap words)
+  u64 s0f_words = 0;
   // multi-GPU
   void* comm = nullptr;
   int world = 1, rank = 0;
@@ -229,6 +232,15 @@ void ensure_s0b(hcc_ctx* c, u64 nwords) {
   c->s0b_words = 0;
   HCC_CUDA(cudaMalloc(&c->s0b, std::max<u64>(nwords, 1) * sizeof(u32)));
   c->s0b_words = nwords;
+}
+
+void ensure_s0f(hcc_ctx* c, u64 nwords) {
+  if (c->s0f_words >= nwords) return;
+  if (c->s0f) HCC_CUDA(cudaFree(c->s0f));
+  c->s0f = nullptr;
+  c->s0f_words = 0;
+  HCC_CUDA(cudaMalloc(&c->s0f, std::max<u64>(nwords, 1) * sizeof(u32)));
+  c->s0f_words = nwords;
 }
 
 void drop_exec(hcc_ctx* c) {
@@ -338,6 +350,9 @@ struct Plan {
   std::vector<u64> bounds;  // unrolled topology segment boundaries (nseg+1)
   int walk;
   bool s0b;                 // star-0 bitmap for hook passes after a compress
+  bool sum = false;         // star-0 summary staged in the hook's shared memory
+  bool chunked = false;     // streaming hooks with per-warp chunked appends
+  u32 sum_words = 0, sum_shift = 0;
   bool hook_events = false;  // CUDA events around unrolled hook launches
   bool adapt;               // device-side adaptive topology plan
   u32 adapt_shift;          // first adaptive segment = m >> adapt_shift
@@ -355,12 +370,43 @@ HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
   a.append = append;
   a.walk = append ? P.walk : 0;  // the literal full-pass loops keep Fig. 2
   a.s0b = nullptr;
+  a.s0f = nullptr;
+  a.s0f_words = a.s0f_shift = 0;
   a.pi = P.pi;
   a.wl0 = P.wl0;
   a.wl1 = P.wl1;
+  a.wl_cap = c->wl_cap;
+  a.chunked = 0;
+  a.gate = kGateAlways;
   a.ctrl = c->d_ctrl;
   a.recs = c->d_recs;
   return a;
+}
+
+// Star-0 lookups for a hook launch (bitmap, plus the summary table when the
+// plan has one).
+void use_s0b(hcc_ctx* c, const Plan& P, HookArgs& a) {
+  a.s0b = c->s0b;
+  if (P.sum) {
+    a.s0f = c->s0f;
+    a.s0f_words = P.sum_words;
+    a.s0f_shift = P.sum_shift;
+  }
+}
+
+// k_hook dynamic shared memory: the summary table, then one slow-path queue
+// of 32 * kHookEPT edges per warp (hook_stream).
+size_t hook_smem(const HookArgs& a, unsigned block) {
+  if (!a.s0f) return 0;
+  return (size_t)((a.s0f_words + 3u) & ~3u) * 4 + (size_t)((block + 31) / 32) * 32 * kHookEPT * 8;
+}
+constexpr size_t kHookSmemMax = kS0fMaxBytes + (size_t)kHookSumCta * kHookEPT * 8;
+
+// Unrolled topology slot that runs the small-segment hook (forming regime).
+bool slot_small(const Plan& P, u64 sgi) {
+  const u64 seg_edges = P.bounds[sgi + 1] - P.bounds[sgi];  // adaptive: estimate
+  return P.block_hook == kHookCta &&
+         seg_edges < (u64)P.grid_hook * P.block_hook * kHookEPT * 2;
 }
 
 // Enqueue one full CC run (pi init through convergence) on seq.
@@ -368,7 +414,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
   c->seg_ev_used = 0;
   k_start<<<P.grid_vert, P.block_vert, 0, q.s()>>>(
       P.pi, P.n, P.s0b ? c->s0b : nullptr, c->d_ctrl, c->d_recs, P.nseg, P.m,
-      P.adapt ? P.adapt_shift : 64u);
+      P.adapt ? P.adapt_shift : 64u, P.sum ? c->s0f : nullptr, P.sum_words);
   HCC_CUDA(cudaGetLastError());
   DevCtrl* ctrl = c->d_ctrl;
   DevRec* recs = c->d_recs;
@@ -415,16 +461,30 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           HookArgs ha = hook_args(c, P, P.adapt ? kSrcCtrlRange : kSrcRange, 1);
           ha.b = P.bounds[sgi];
           ha.e = P.bounds[sgi + 1];
-          if (P.s0b && sgi >= 1) ha.s0b = c->s0b;
+          if (P.s0b && sgi >= 1) use_s0b(c, P, ha);
           if (P.hook_events) q.record(c->seg_ev[2 * sgi]);
-          const u64 seg_edges = ha.e - ha.b;  // adaptive: the static estimate
-          if (P.block_hook == kHookThreads &&
-              seg_edges < (u64)P.grid_hook * kHookThreads * kHookEPT * 2) {
+          if (slot_small(P, sgi)) {
             // forming-regime segment: EPT 2 over a full grid
+            ha.s0f = nullptr;
+            const u64 seg_edges = ha.e - ha.b;  // adaptive: the static estimate
             k_hook_small<<<grid_for((seg_edges + 1) / 2 + 1, kHookThreads, 0x7fffffffull),
                            kHookThreads, 0, q.s()>>>(ha);
           } else {
-            k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(ha);
+            ha.chunked = P.chunked ? 1 : 0;
+            HookArgs hp = ha;  // plain streaming hook: bitmap only, full L1
+            hp.s0f = nullptr;
+            if (P.sum && sgi >= 1 && P.adapt) {
+              // the previous step's device vote picks the summary hook or
+              // the plain one; the other launch exits at entry (cheaper
+              // than an IF/ELSE graph node, measured ~20 us per slot)
+              ha.gate = kGateIfSum;
+              hp.gate = kGateIfPlain;
+              k_hook_sum<<<c->sms * c->occ_hook_sum, kHookSumCta, hook_smem(ha, kHookSumCta),
+                           q.s()>>>(ha);
+              k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(hp);
+            } else {
+              k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(hp);
+            }
           }
           if (P.hook_events) q.record(c->seg_ev[2 * sgi + 1]);
           q.phase_done(HCC_PHASE_HOOK);
@@ -432,16 +492,25 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           if (P.s0b)
             k_compress_s0b<<<grid_for((P.n + 7) / 8, kVertThreads, 0x7fffffffull),
                              kVertThreads, 0, q.s()>>>(P.pi, P.n, ctrl, recs, c->s0b,
-                                                       kCompressIfDirty);
+                                                       kCompressIfDirty,
+                                                       P.sum ? c->s0f : nullptr,
+                                                       P.sum_words, P.sum_shift);
           else
             k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
                                                                 recs, 1);
           q.phase_done(HCC_PHASE_COMPRESS);
           // (a step folded into the compress's last block costs one
           // single-address atomic per compress block: slower than a launch)
-          if (P.adapt)
-            k_step_adapt<<<1, 1, 0, q.s()>>>(ctrl, recs, P.m, P.forming_pct);
-          else
+          if (P.adapt) {
+            // the next hook's summary vote rides on the step kernel (the
+            // worklist passes reuse the last one: coverage only grows)
+            const bool vote = P.sum && sgi + 1 < P.nseg && !slot_small(P, sgi + 1);
+            if (vote)
+              k_step_adapt<<<1, 1024, 0, q.s()>>>(ctrl, recs, P.m, P.forming_pct, c->s0f,
+                                                 P.sum_words);
+            else
+              k_step_adapt<<<1, 1, 0, q.s()>>>(ctrl, recs, P.m, P.forming_pct, nullptr, 0);
+          } else
             k_step_segment<<<1, 1, 0, q.s()>>>(ctrl, recs, 0, 0);
         }
         c->seg_ev_used = P.hook_events ? P.nseg : 0;
@@ -459,13 +528,27 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
       // data-driven passes over the compacted worklist
       q.loop([&](cudaGraphConditionalHandle h, int u) {
         HookArgs wa = hook_args(c, P, kSrcWorklist, 1);
-        if (P.s0b && !P.bounds.empty()) wa.s0b = c->s0b;
-        k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(wa);
+        if (P.s0b && !P.bounds.empty()) use_s0b(c, P, wa);
+        wa.chunked = P.chunked ? 1 : 0;
+        if (wa.s0f && P.adapt) {
+          HookArgs wp = wa;
+          wa.gate = kGateIfSum;
+          wp.gate = kGateIfPlain;
+          wp.s0f = nullptr;
+          k_hook_sum<<<c->sms * c->occ_hook_sum, kHookSumCta, hook_smem(wa, kHookSumCta),
+                       q.s()>>>(wa);
+          k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(wp);
+        } else {
+          wa.s0f = nullptr;
+          k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(wa);
+        }
         q.phase_done(HCC_PHASE_HOOK);
         if (P.s0b && !P.bounds.empty())
           k_compress_s0b<<<grid_for((P.n + 7) / 8, kVertThreads, 0x7fffffffull),
                            kVertThreads, 0, q.s()>>>(P.pi, P.n, ctrl, recs, c->s0b,
-                                                     kCompressIfDirty);
+                                                     kCompressIfDirty,
+                                                     P.sum ? c->s0f : nullptr,
+                                                     P.sum_words, P.sum_shift);
         else
           k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
                                                               recs, 1);
@@ -668,9 +751,14 @@ int hcc_create(int device, hcc_ctx** out) {
   HCC_CUDA(cudaEventCreate(&c->ev0));
   HCC_CUDA(cudaEventCreate(&c->ev1));
   int occ = 0;
-  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook,
-                                                          kHookThreads, 0));
+  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook, kHookCta, 0));
   c->occ_hook = std::max(occ, 1);
+  // the summary hook stages the star-0 summary and its slow-path queues
+  HCC_CUDA(cudaFuncSetAttribute(k_hook_sum, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kHookSmemMax));
+  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_sum, kHookSumCta,
+                                                          kHookSmemMax));
+  c->occ_hook_sum = std::max(occ, 1);
   HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_compress,
                                                           kVertThreads, 0));
   c->occ_vert = std::max(occ, 1);
@@ -696,6 +784,7 @@ int hcc_destroy(hcc_ctx* c) {
   cudaFree(c->wl[0]);
   cudaFree(c->wl[1]);
   cudaFree(c->s0b);
+  cudaFree(c->s0f);
   for (cudaEvent_t ev : c->seg_ev) cudaEventDestroy(ev);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -1230,13 +1319,29 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   P.hook_events = (o->flags & HCC_FLAG_HOOK_EVENTS) != 0;
   P.forming_pct = std::getenv("HCC_FORMING_PCT") ? (u32)std::atoi(std::getenv("HCC_FORMING_PCT"))
                                                   : kAdaptFormingPct;
-  if (P.s0b) ensure_s0b(c, (n + 31) / 32);
+  if (P.s0b) {
+    ensure_s0b(c, (n + 31) / 32);
+    // star-0 summary: the smallest group (2^shift bitmap words per bit)
+    // whose table fits the hook's shared-memory budget; groups larger than
+    // a compress block's 64 words are not built
+    const u64 nwords = (n + 31) / 32;
+    u32 sh = 0;
+    while (((nwords + (1ull << sh) - 1) >> sh) > (u64)kS0fMaxBytes * 8) ++sh;
+    bool sum_ok = sh <= 6;
+    if (const char* e = std::getenv("HCC_S0F")) sum_ok = sum_ok && std::atoi(e) != 0;
+    if (sum_ok) {
+      P.sum = true;
+      P.sum_shift = sh;
+      P.sum_words = (u32)((((nwords + (1ull << sh) - 1) >> sh) + 31) / 32);
+      ensure_s0f(c, P.sum_words);
+    }
+  }
   {
     const char* w = std::getenv("HCC_WALK");
     P.walk = w ? std::atoi(w) : kDefaultWalk;
   }
   if (o->max_threads == 0) {
-    P.block_hook = kHookThreads;
+    P.block_hook = kHookCta;
     P.grid_hook = (unsigned)(c->sms * c->occ_hook);
     P.block_vert = kVertThreads;
     // k_compress / k_init_pi take four vertices per thread.  The grid covers
@@ -1252,6 +1357,19 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
     unsigned grd = (unsigned)std::max<u64>(1, std::min<u64>(t / blk, 1u << 20));
     P.block_hook = P.block_vert = blk;
     P.grid_hook = P.grid_vert = grd;
+  }
+  if (uses_wl && o->max_threads == 0) {
+    // streaming hooks (unrolled topology slots, worklist passes) append in
+    // per-warp chunks and pad every warp's last chunk of a launch with
+    // no-op records: room for all launches appending to one list (the
+    // unrolled slots; the looped-segment path keeps exact block appends)
+    P.chunked = true;
+    const u64 warps = std::max<u64>((u64)P.grid_hook * (P.block_hook / 32),
+                                    (u64)c->sms * c->occ_hook_sum * (kHookSumCta / 32));
+    const u64 launches = (P.nseg <= kMaxUnrolledSegments ? P.nseg : 0) + 2;
+    ensure_wl(c, m + launches * warps * kWlChunk);
+    P.wl0 = c->wl[0];
+    P.wl1 = c->wl[1];
   }
 
   const bool observer = o->observer != nullptr;
@@ -1291,6 +1409,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   key.flags = o->flags;
   key.walk = P.walk;
   key.s0b = P.s0b;
+  key.sum = P.sum;
   key.plan = key.plan * 31 + (P.adapt ? 1000 + P.adapt_shift + 100000ull * P.forming_pct : 0);
   for (u64 x : P.bounds) key.plan = key.plan * 1000003ull + x;
 
@@ -1302,9 +1421,17 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
       try {
         enqueue_run(c, P, q);
       } catch (...) {
+        // end the open captures innermost first (loop bodies capture into
+        // conditional-node graphs on streams[1..depth]), then the root
         cudaGraph_t tmp = nullptr;
+        for (int d = q.depth; d >= 1; --d) {
+          tmp = nullptr;
+          cudaStreamEndCapture(q.streams[d], &tmp);
+        }
+        tmp = nullptr;
         cudaStreamEndCapture(c->stream, &tmp);
         if (tmp) cudaGraphDestroy(tmp);
+        cudaGetLastError();
         for (size_t i = 1; i < q.streams.size(); ++i)
           cudaStreamDestroy(q.streams[i]);
         throw;
@@ -1404,6 +1531,11 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
     if (o->algo == HCC_ALGO_BASELINE_MJ && !P.full_passes && !P.bounds.empty()) {
       const u64 wl = nrec > nseg ? nrec - nseg : 0;
       k += 3 * nseg + 3 * wl;  // hook+compress+step per slot and per wl pass
+      if (P.sum && P.adapt && nseg <= kMaxUnrolledSegments) {
+        // voted launches: summary and plain hook back to back
+        for (u64 sgi = 1; sgi < nseg; ++sgi) k += slot_small(P, sgi) ? 0 : 1;
+        k += wl;
+      }
     } else {
       k += 3 * iters;  // hook/compress(or jump)/step per record
     }
@@ -1418,6 +1550,8 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   if (mx) *mx = out;
   if (hc.err & 2u)
     return fail(HCC_ECUDA, "device loop exceeded its step cap (runaway loop)");
+  if (hc.err & 4u)
+    return fail(HCC_ECUDA, "worklist capacity exceeded (chunked appends)");
   if ((o->flags & HCC_FLAG_CHECK_STAR) && hc.flag)
     return fail(HCC_ENOTSTAR, "extract_labels: forest is not star-shaped");
   return HCC_OK;
@@ -1819,7 +1953,7 @@ int hcc_rehook(hcc_ctx* c, hcc_forest* f, const uint32_t* dev_bits_or,
   P.nseg = 1;
   P.walk = kDefaultWalk;
   P.s0b = false;
-  P.block_hook = kHookThreads;
+  P.block_hook = kHookCta;
   P.grid_hook = (unsigned)(c->sms * c->occ_hook);
   P.block_vert = kVertThreads;
   P.grid_vert = grid_for((n + 3) / 4, kVertThreads, 0x7fffffffull);

@@ -23,6 +23,25 @@ typedef unsigned int u32;
 
 constexpr int kMaxRecs = 4096;    // per-run phase records kept on device
 constexpr int kHookThreads = 256;
+// Streaming hook CTA (k_hook): threads per CTA; its shared-memory star-0
+// summary table holds at most HCC_S0F_MAX_BYTES.
+#ifndef HCC_HOOK_CTA
+#define HCC_HOOK_CTA 1024
+#endif
+#ifndef HCC_S0F_MAX_BYTES
+#define HCC_S0F_MAX_BYTES 65536
+#endif
+constexpr int kHookCta = HCC_HOOK_CTA;
+#ifndef HCC_HOOK_SUM_CTA
+#define HCC_HOOK_SUM_CTA 1024
+#endif
+constexpr int kHookSumCta = HCC_HOOK_SUM_CTA;  // k_hook_sum (one CTA per SM)
+constexpr u32 kS0fMaxBytes = HCC_S0F_MAX_BYTES;
+constexpr int kHookSlow = 4;
+// HookArgs.gate: k_hook_sum and k_hook are launched back to back for a
+// voted slot and the one not chosen (DevCtrl.use_sum) exits at entry.
+constexpr int kGateAlways = 0, kGateIfSum = 1, kGateIfPlain = 2;     // queued edges per lane per slow-path round
+constexpr u32 kWlChunk = 256;    // worklist records a warp reserves at once
 #ifndef HCC_HOOK_EPT
 #define HCC_HOOK_EPT 8
 #endif
@@ -56,6 +75,8 @@ struct DevCtrl {
   u64 loop_steps;    // loop-step kernels executed (runaway guard)
   u64 seg_b, seg_e;  // adaptive topology plan: current segment range
   u64 t_start;       // globaltimer at k_start (span timeline origin)
+  u32 use_sum;       // last summary vote (k_step_adapt): next hook uses k_hook_sum
+  u32 pad_;
 };
 
 // k_compress_s0b modes.
@@ -93,6 +114,15 @@ struct HookArgs {
   int walk;          // max root-walk steps before a store (0 = Fig. 2 hook)
   const u32* s0b;    // star-0 bitmap (bit v = pi(v) == 0 after the last
                      // compress), or null
+  const u32* s0f;    // star-0 summary: bit i = bitmap words
+                     // [i << s0f_shift, (i + 1) << s0f_shift) are all ones;
+                     // staged in shared memory by k_hook; or null
+  u32 s0f_words;     // u32 words of s0f
+  u32 s0f_shift;
+  u64 wl_cap;        // records each worklist buffer holds
+  int chunked;       // full-warp launch with per-warp chunked appends
+                     // (padding records; the host sized the worklists)
+  int gate;          // kGate*: run only if ctrl->use_sum says so
   u32* pi;
   uint2* wl0;
   uint2* wl1;
@@ -114,19 +144,22 @@ __global__ void k_begin(DevCtrl* ctrl, DevRec* recs, u64 nseg);
 __global__ void k_init_pi(u32* pi, u64 n, u32* bits);
 __global__ void k_hook(HookArgs a);
 __global__ void k_hook_small(HookArgs a);
+__global__ void k_hook_sum(HookArgs a);
 __global__ void k_cas_hook(HookArgs a);
 __global__ void k_compress(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
                            int skip_if_clean);
 __global__ void k_compress_s0b(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
-                               u32* bits, int skip_if_clean);
+                               u32* bits, int skip_if_clean, u32* sum, u32 sum_words,
+                               u32 sum_shift);
 __global__ void k_start(u32* pi, u64 n, u32* bits, DevCtrl* ctrl, DevRec* recs, u64 nseg,
-                        u64 m, u32 plan_shift);
+                        u64 m, u32 plan_shift, u32* sum, u32 sum_words);
 __global__ void k_jump(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs);
 __global__ void k_step_worklist(DevCtrl* ctrl, DevRec* recs,
                                 cudaGraphConditionalHandle h, int use_cond);
 __global__ void k_step_segment(DevCtrl* ctrl, DevRec* recs,
                                cudaGraphConditionalHandle h, int use_cond);
-__global__ void k_step_adapt(DevCtrl* ctrl, DevRec* recs, u64 m, u32 forming_pct);
+__global__ void k_step_adapt(DevCtrl* ctrl, DevRec* recs, u64 m, u32 forming_pct,
+                             const u32* sum, u32 sum_words);
 __global__ void k_step_outer(DevCtrl* ctrl, DevRec* recs,
                              cudaGraphConditionalHandle h, int use_cond);
 __global__ void k_step_jump(DevCtrl* ctrl, cudaGraphConditionalHandle h,

@@ -82,6 +82,20 @@ __device__ __forceinline__ u32 ld_bits(const u32* p) {
 #define HCC_HOOK_DEDUP 0
 #endif
 
+// Shared-memory slot of summary word i: each 32-word row is XOR-permuted by
+// a hash of its row index.  Skewed graphs hit summary words whose indices
+// have few one bits (RMAT hubs: 0, 32, 64, 1024, ...), which would all sit
+// in bank 0 unswizzled.
+__device__ __forceinline__ u32 sum_swz(u32 i) {
+  return i ^ (((i >> 5) ^ (i >> 10)) & 31u);
+}
+
+// Vertex x's group is all in star 0 (summary bit of bitmap word x >> 5).
+__device__ __forceinline__ bool sum_covered(const u32* s_sum, u32 x, u32 shift) {
+  const u32 g = x >> (5u + shift);
+  return (s_sum[sum_swz(g >> 5)] >> (g & 31u)) & 1u;
+}
+
 // Coherent (L2) read: sees other threads' stores made during this kernel.
 __device__ __forceinline__ u32 ld_fresh(const u32* p) { return __ldcg(p); }
 
@@ -243,7 +257,7 @@ __global__ void k_begin(DevCtrl* ctrl, DevRec* recs, u64 nseg) {
 // first range (plan_shift < 64), and pi(v) = v + the star-0 bitmap
 // (k_init_pi), in one launch.
 __global__ void k_start(u32* pi, u64 n, u32* bits, DevCtrl* ctrl, DevRec* recs, u64 nseg,
-                        u64 m, u32 plan_shift) {
+                        u64 m, u32 plan_shift, u32* sum, u32 sum_words) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     DevCtrl c = {};
     c.nseg = nseg ? nseg : 1;
@@ -261,6 +275,8 @@ __global__ void k_start(u32* pi, u64 n, u32* bits, DevCtrl* ctrl, DevRec* recs, 
   const u64 stride = (u64)gridDim.x * blockDim.x;
   if (bits)
     for (u64 w = tid; w < ((n + 31) >> 5); w += stride) bits[w] = w == 0 ? 1u : 0u;
+  if (sum)
+    for (u64 w = tid; w < sum_words; w += stride) sum[w] = 0u;
   const u64 n4 = n >> 2;
   uint4* p4 = reinterpret_cast<uint4*>(pi);
   for (u64 i = tid; i < n4; i += stride) {
@@ -286,11 +302,118 @@ __global__ void k_init_pi(u32* pi, u64 n, u32* bits) {
   for (u64 v = (n4 << 2) + tid; v < n; v += stride) pi[v] = (u32)v;
 }
 
+// Lookups, root walk and stores for S edges of one thread (the body of a
+// hook tile).  Returns the mask of edges whose (h, l) pair in (pu, pv)
+// must be appended to the worklist (stored links and deferred walks).
+template <int S, bool SUM>
+__device__ __forceinline__ u32 resolve_edges(const HookArgs& a, const u32* s_sum,
+                                             const uint2 (&ed)[S], u32 (&pu)[S],
+                                             u32 (&pv)[S]) {
+  u32* pi = a.pi;
+  if (a.s0b) {
+    // Star-0 bitmap: one L1-friendly word read answers pi(x) == 0 for
+    // the giant component's vertices; only the rest gather pi.
+    u32 wu[S], wv[S];
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      const u32 xu = ed[k].x >> 5, xv = ed[k].y >> 5;
+      if (SUM) {
+        wu[k] = sum_covered(s_sum, ed[k].x, a.s0f_shift) ? ~0u : ld_bits(a.s0b + xu);
+        wv[k] = sum_covered(s_sum, ed[k].y, a.s0f_shift) ? ~0u : ld_bits(a.s0b + xv);
+      } else {
+        wu[k] = ld_bits(a.s0b + xu);
+        wv[k] = ld_bits(a.s0b + xv);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      pu[k] = (wu[k] >> (ed[k].x & 31u)) & 1u ? 0u : ld_pi(pi + ed[k].x);
+      pv[k] = (wv[k] >> (ed[k].y & 31u)) & 1u ? 0u : ld_pi(pi + ed[k].y);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      pu[k] = ld_pi(pi + ed[k].x);
+      pv[k] = ld_pi(pi + ed[k].y);
+    }
+  }
+  // Candidates (pu != pv) walk down like Fig. 3's atomic hook, but with a
+  // plain load in place of the CAS: read pi[h]; already linked -> drop;
+  // h still a root -> plain store; otherwise continue from (pi[h], l).
+  // Every value met is a root of the forest at the start of the pass, so
+  // only pass-start roots are ever stored to, and every store is recorded
+  // in the worklist.  A walk that runs out of `walk`
+  // steps is deferred to the worklist unstored (below).  This removes the
+  // redundant stores that single-level reads make to hub slots while the
+  // hub structure forms.
+  // The S walks of a thread advance in lockstep, one level per round
+  // with all their loads in flight (in the forming segments a walk is
+  // several dependent round trips).
+  u32 walking = 0;
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const u32 x = pu[k], y = pv[k];
+    pu[k] = max(x, y);  // h
+    pv[k] = min(x, y);  // l
+    walking |= x != y ? 1u << k : 0u;
+  }
+  u32 act = walking, roots = a.walk == 0 ? walking : 0u;
+  for (int step = 0; step < a.walk && walking; ++step) {
+    // L1-cached read: any value the slot ever held is a recorded link
+    // (pass-start link or a worklist pair), so a stale value is a safe
+    // basis for both "drop" and "descend"; reading through L1 keeps the
+    // hub slots every edge touches off the L2 slices.
+    u32 ph[S];
+#pragma unroll
+    for (int k = 0; k < S; ++k) ph[k] = walking & (1u << k) ? ld_pi(pi + pu[k]) : 0u;
+    u32 fresh = 0;  // edges that stored in this round
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      if (!(walking & (1u << k))) continue;
+      // A root this thread linked earlier in the round: see that store,
+      // as a one-edge-at-a-time walk would (stores of earlier rounds are
+      // seen through memory).
+      u32 p = ph[k];
+#if HCC_HOOK_DEDUP
+#pragma unroll
+      for (int k2 = 0; k2 < k; ++k2)
+        if ((fresh & (1u << k2)) && pu[k2] == pu[k]) p = pv[k2];
+#endif
+      if (p == pu[k]) {               // root: store now
+        pi[pu[k]] = pv[k];
+        fresh |= 1u << k;
+        walking &= ~(1u << k);
+      } else if (p == pv[k]) {        // already linked
+        act &= ~(1u << k);
+        walking &= ~(1u << k);
+      } else {
+        const u32 l = pv[k];
+        pu[k] = max(p, l);
+        pv[k] = min(p, l);
+      }
+    }
+  }
+  // A walk that ran out of steps defers the pair to the worklist without
+  // storing: h may be an interior vertex whose link existed at pass start
+  // (the forest need not be a star), and only slots observed as roots may
+  // be written.
+#pragma unroll
+  for (int k = 0; k < S; ++k)
+    if (roots & (1u << k)) pi[pu[k]] = pv[k];
+  return act;
+}
+
+// Copy the star-0 summary into shared memory (swizzled rows).
+__device__ __forceinline__ void load_summary(const HookArgs& a, u32* s_sum) {
+  for (u32 i = threadIdx.x; i < a.s0f_words; i += blockDim.x) s_sum[sum_swz(i)] = a.s0f[i];
+  __syncthreads();
+}
+
 // Atomic-free Hook (forest.hpp:83-89) over an edge range, a segment or the
 // current worklist.  See the file comment for the design.  EPT edges per
 // thread per tile; the next tile's edge loads are issued before the current
 // tile's dependent gathers (software pipelining).
-template <int EPT>
+template <int EPT, bool SUM>
 __device__ __forceinline__ void hook_impl(const HookArgs& a) {
   const uint2* src;
   u64 b, e;
@@ -378,6 +501,11 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
     }
   }
 
+  // Star-0 summary staged in shared memory: a lane whose endpoint's
+  // 32-vertex word is known all-ones skips the bitmap gather (the L1 miss /
+  // wavefront that bounds the steady segments).
+  extern __shared__ u32 s_sum[];
+  if (SUM) load_summary(a, s_sum);
   const uint4* s4 = reinterpret_cast<const uint4*>(src + b2);
   const u64 pol = policy_evict_first();
   const u64 tile = (u64)blockDim.x * (EPT / 2);
@@ -401,90 +529,7 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
     }
     if (t + gridDim.x < ntiles) load_tile(t + gridDim.x, nq);
     u32 pu[EPT], pv[EPT];
-    if (a.s0b) {
-      // Star-0 bitmap: one L1-friendly word read answers pi(x) == 0 for
-      // the giant component's vertices; only the rest gather pi.
-      u32 wu[EPT], wv[EPT];
-#pragma unroll
-      for (int k = 0; k < EPT; ++k) {
-        wu[k] = ld_bits(a.s0b + (ed[k].x >> 5));
-        wv[k] = ld_bits(a.s0b + (ed[k].y >> 5));
-      }
-#pragma unroll
-      for (int k = 0; k < EPT; ++k) {
-        pu[k] = (wu[k] >> (ed[k].x & 31u)) & 1u ? 0u : ld_pi(pi + ed[k].x);
-        pv[k] = (wv[k] >> (ed[k].y & 31u)) & 1u ? 0u : ld_pi(pi + ed[k].y);
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < EPT; ++k) {
-        pu[k] = ld_pi(pi + ed[k].x);
-        pv[k] = ld_pi(pi + ed[k].y);
-      }
-    }
-    // Candidates (pu != pv) walk down like Fig. 3's atomic hook, but with a
-    // plain load in place of the CAS: read pi[h]; already linked -> drop;
-    // h still a root -> plain store; otherwise continue from (pi[h], l).
-    // Every value met is a root of the forest at the start of the pass, so
-    // only pass-start roots are ever stored to, and every store is recorded
-    // in the worklist.  After `walk` steps the store is
-    // made regardless (it may overwrite a transient link; the worklist
-    // records it).  This removes the redundant stores that single-level
-    // reads make to hub slots while the hub structure forms.
-    // The EPT walks of a thread advance in lockstep, one level per round
-    // with all their loads in flight (in the forming segments a walk is
-    // several dependent round trips).
-    u32 walking = 0;
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      const u32 x = pu[k], y = pv[k];
-      pu[k] = max(x, y);  // h
-      pv[k] = min(x, y);  // l
-      walking |= x != y ? 1u << k : 0u;
-    }
-    u32 act = walking, roots = a.walk == 0 ? walking : 0u;
-    for (int step = 0; step < a.walk && walking; ++step) {
-      // L1-cached read: any value the slot ever held is a recorded link
-      // (pass-start link or a worklist pair), so a stale value is a safe
-      // basis for both "drop" and "descend"; reading through L1 keeps the
-      // hub slots every edge touches off the L2 slices.
-      u32 ph[EPT];
-#pragma unroll
-      for (int k = 0; k < EPT; ++k) ph[k] = walking & (1u << k) ? ld_pi(pi + pu[k]) : 0u;
-      u32 fresh = 0;  // edges that stored in this round
-#pragma unroll
-      for (int k = 0; k < EPT; ++k) {
-        if (!(walking & (1u << k))) continue;
-        // A root this thread linked earlier in the round: see that store,
-        // as a one-edge-at-a-time walk would (stores of earlier rounds are
-        // seen through memory).
-        u32 p = ph[k];
-#if HCC_HOOK_DEDUP
-#pragma unroll
-        for (int k2 = 0; k2 < k; ++k2)
-          if ((fresh & (1u << k2)) && pu[k2] == pu[k]) p = pv[k2];
-#endif
-        if (p == pu[k]) {               // root: store now
-          pi[pu[k]] = pv[k];
-          fresh |= 1u << k;
-          walking &= ~(1u << k);
-        } else if (p == pv[k]) {        // already linked
-          act &= ~(1u << k);
-          walking &= ~(1u << k);
-        } else {
-          const u32 l = pv[k];
-          pu[k] = max(p, l);
-          pv[k] = min(p, l);
-        }
-      }
-    }
-    // A walk that ran out of steps defers the pair to the worklist without
-    // storing: h may be an interior vertex whose link existed at pass start
-    // (the forest need not be a star), and only slots observed as roots may
-    // be written.
-#pragma unroll
-    for (int k = 0; k < EPT; ++k)
-      if (roots & (1u << k)) pi[pu[k]] = pv[k];
+    const u32 act = resolve_edges<EPT, SUM>(a, s_sum, ed, pu, pv);
     if (a.append) {
       u64 pos;
       if (block_reserve(__popc(act), cnt_out, pos, appended)) {
@@ -507,23 +552,215 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
   block_t1(&r->hook_t1);
 }
 
+
+// Per-warp output of the streaming hook: the warp's current chunk of the
+// output worklist [pos, end), its real appends and its change flag (all
+// warp-uniform).
+struct WarpOut {
+  u64 pos = 0, end = 0;
+  u32 appended = 0, changed = 0;
+};
+
+// Append the (h, l) pairs selected by each lane's `act` mask (at most N per
+// lane) to the warp's chunk; a full chunk is padded with (0, 0) no-op
+// records and a new one is reserved with one global atomic.
+template <int N>
+__device__ __forceinline__ void warp_emit(const HookArgs& a, WarpOut& w, uint2* wl_out,
+                                          u64* cnt_out, u32 lane, u32 act,
+                                          const u32 (&h)[N], const u32 (&l)[N]) {
+  static_assert(32 * N <= (int)kWlChunk, "a warp's appends must fit one chunk");
+  const u32 cnt = __popc(act);
+  u32 incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (u32)o) incl += y;
+  }
+  const u32 total = __shfl_sync(0xffffffffu, incl, 31);
+  if (total == 0) return;
+  if (!a.append) {
+    w.changed = 1;
+    return;
+  }
+  if (w.pos + total > w.end) {
+    for (u64 i = w.pos + lane; i < w.end; i += 32) wl_out[i] = make_uint2(0u, 0u);
+    u64 base = 0;
+    if (lane == 0) base = atomicAdd(cnt_out, (u64)kWlChunk);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base + kWlChunk > a.wl_cap) {  // sized on the host; never expected
+      if (lane == 0) atomicOr(&a.ctrl->err, 4u);
+      w.pos = w.end = 0;
+      return;
+    }
+    w.pos = base;
+    w.end = base + kWlChunk;
+  }
+  u64 pos = w.pos + (incl - cnt);
+#pragma unroll
+  for (int k = 0; k < N; ++k)
+    if (act & (1u << k)) wl_out[pos++] = make_uint2(h[k], l[k]);
+  w.pos += total;
+  w.appended += total;
+}
+
+// Streaming hook for full-warp launches: no block barriers after the
+// prologue; appends go to per-warp chunks of the output worklist (one
+// global atomic per kWlChunk records; a chunk's unused tail is padded with
+// (0, 0) self-loops, which the next pass skips as no-ops).
+//
+// SUM (k_hook_sum, chosen on the device when the star-0 summary covers at
+// least half of its groups): each thread first tests its EPT edges against
+// the summary staged in shared memory (two shared loads per edge, no global
+// traffic when both endpoints' words are all in star 0); the warp compacts
+// the rest into its shared-memory queue and resolves them kHookSlow per
+// lane per round.  Otherwise (k_hook: no shared memory, so L1 keeps its full
+// size for the bitmap's hot words; e.g. RMAT, whose isolated vertices break
+// most words) every edge takes the bitmap / gather path directly.
+template <int EPT, bool SUM>
+__device__ __forceinline__ void hook_stream(const HookArgs& a) {
+  constexpr int S = kHookSlow;
+  const uint2* src;
+  u64 b, e;
+  u32 out;
+  resolve_src(a, src, b, e, out);
+  DevCtrl* ctrl = a.ctrl;
+  DevRec* r = cur_rec(ctrl, a.recs);
+  block_t0(&r->hook_t0);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && e > b) {
+    atomicAdd(&r->edges_in, e - b);
+    atomicAdd(&ctrl->edges_processed, e - b);
+  }
+  uint2* wl_out = out ? a.wl1 : a.wl0;
+  u64* cnt_out = &ctrl->wl_count[out];
+  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+
+  extern __shared__ u32 s_sum[];
+  if (SUM) load_summary(a, s_sum);
+  uint2* s_q = reinterpret_cast<uint2*>(s_sum + ((a.s0f_words + 3u) & ~3u)) +
+               (size_t)warp * (32 * EPT);
+  WarpOut wo;
+
+  // head / tail edges that do not fill a 16-byte pair: warp 0 of block 0
+  u64 b2 = b + (b & 1ull);
+  if (b2 > e) b2 = e;
+  const u64 n4 = (e - b2) >> 1;
+  if (blockIdx.x == 0 && warp == 0) {
+    uint2 ed[1] = {make_uint2(0u, 0u)};
+    if (lane == 0 && b2 != b) ed[0] = src[b];
+    if (lane == 1 && ((e - b2) & 1ull)) ed[0] = src[e - 1];
+    u32 h[1], l[1];
+    const u32 act = resolve_edges<1, false>(a, s_sum, ed, h, l);
+    warp_emit<1>(a, wo, wl_out, cnt_out, lane, act, h, l);
+  }
+
+  const uint4* s4 = reinterpret_cast<const uint4*>(src + b2);
+  const u64 pol = policy_evict_first();
+  const u64 tile = (u64)blockDim.x * (EPT / 2);
+  const u64 ntiles = (n4 + tile - 1) / tile;
+  // Out-of-range slots become the self-loop (0,0): a no-op hook.
+  auto load_tile = [&](u64 t, uint4* q) {
+#pragma unroll
+    for (int j = 0; j < EPT / 2; ++j) {
+      const u64 i = t * tile + (u64)j * blockDim.x + threadIdx.x;
+      q[j] = i < n4 ? ld_stream16(s4 + i, pol) : make_uint4(0u, 0u, 0u, 0u);
+    }
+  };
+  uint4 nq[EPT / 2];
+  if ((u64)blockIdx.x < ntiles) load_tile(blockIdx.x, nq);
+  for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    uint2 ed[EPT];
+#pragma unroll
+    for (int j = 0; j < EPT / 2; ++j) {
+      ed[2 * j] = make_uint2(nq[j].x, nq[j].y);
+      ed[2 * j + 1] = make_uint2(nq[j].z, nq[j].w);
+    }
+    if (t + gridDim.x < ntiles) load_tile(t + gridDim.x, nq);
+    if (!SUM) {
+      u32 h[EPT], l[EPT];
+      const u32 act = resolve_edges<EPT, false>(a, s_sum, ed, h, l);
+      warp_emit<EPT>(a, wo, wl_out, cnt_out, lane, act, h, l);
+      continue;
+    }
+    // fast path: both endpoints in summary-covered words (or a self loop)
+    u32 need = 0;
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const bool done = ed[k].x == ed[k].y ||
+                        (sum_covered(s_sum, ed[k].x, a.s0f_shift) &&
+                         sum_covered(s_sum, ed[k].y, a.s0f_shift));
+      need |= done ? 0u : 1u << k;
+    }
+    const u32 nneed = __popc(need);
+    u32 incl = nneed;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (u32)o) incl += y;
+    }
+    const u32 total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) continue;
+    u32 o = incl - nneed;
+#pragma unroll
+    for (int k = 0; k < EPT; ++k)
+      if (need & (1u << k)) s_q[o++] = ed[k];
+    __syncwarp();
+    for (u32 base = 0; base < total; base += 32u * S) {
+      uint2 q2[S];
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        const u32 idx = base + (u32)j * 32u + lane;
+        q2[j] = idx < total ? s_q[idx] : make_uint2(0u, 0u);
+      }
+      u32 h[S], l[S];
+      const u32 act = resolve_edges<S, true>(a, s_sum, q2, h, l);
+      warp_emit<S>(a, wo, wl_out, cnt_out, lane, act, h, l);
+    }
+    __syncwarp();
+  }
+  // pad this warp's chunk tail; publish the real appends
+  for (u64 i = wo.pos + lane; i < wo.end; i += 32) wl_out[i] = make_uint2(0u, 0u);
+  if (lane == 0) {
+    if (wo.appended) {
+      atomicAdd(&r->edges_out, (u64)wo.appended);
+      ctrl->dirty = 1;
+    }
+    if (wo.changed) {
+      ctrl->changed = 1;
+      ctrl->dirty = 1;
+    }
+  }
+  block_t1(&r->hook_t1);
+}
+
 #ifndef HCC_HOOK_MINB
-#define HCC_HOOK_MINB 4
+#define HCC_HOOK_MINB (1024 / HCC_HOOK_CTA)
 #endif
-__global__ void __launch_bounds__(kHookThreads, HCC_HOOK_MINB) k_hook(HookArgs a) {
-  hook_impl<kHookEPT>(a);
+__global__ void __launch_bounds__(kHookCta, HCC_HOOK_MINB) k_hook(HookArgs a) {
+  // (the summary path is k_hook_sum; s0f is ignored here)
+  if (a.gate == kGateIfPlain && *(volatile u32*)&a.ctrl->use_sum) return;
+  if (a.chunked && (blockDim.x & 31u) == 0)
+    hook_stream<kHookEPT, false>(a);
+  else
+    hook_impl<kHookEPT, false>(a);
+}
+
+// Streaming hook with the star-0 summary in shared memory (full warps,
+// chunked appends, s0f set).
+__global__ void __launch_bounds__(kHookSumCta, 1) k_hook_sum(HookArgs a) {
+  if (a.gate == kGateIfSum && !*(volatile u32*)&a.ctrl->use_sum) return;
+  hook_stream<kHookEPT, true>(a);
 }
 
 // Small segments (the forming regime): two edges per thread, one tile per
 // block over a full grid, so long root walks run side by side instead of
 // eight deep per thread.
 __global__ void __launch_bounds__(kHookThreads) k_hook_small(HookArgs a) {
-  hook_impl<2>(a);
+  hook_impl<2, false>(a);
 }
 
 // CAS-verified hook (forest.hpp:107-122): walks down until it acquires a
 // root slot; counters follow the reference definitions.
-__global__ void __launch_bounds__(kHookThreads) k_cas_hook(HookArgs a) {
+__global__ void __launch_bounds__(kHookCta) k_cas_hook(HookArgs a) {
   const uint2* src;
   u64 b, e;
   u32 out;
@@ -623,7 +860,7 @@ __global__ void __launch_bounds__(kVertThreads)
 // three warp shuffles (8 lanes = one 32-vertex word) and stored once.
 __global__ void __launch_bounds__(kVertThreads)
     k_compress_s0b(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs, u32* bits,
-                   int mode) {
+                   int mode, u32* sum, u32 sum_words, u32 sum_shift) {
   if (mode && *(volatile u32*)&ctrl->dirty == 0) return;
   DevRec* r = cur_rec(ctrl, recs);
   block_t0(&r->comp_t0);
@@ -708,6 +945,44 @@ __global__ void __launch_bounds__(kVertThreads)
   w |= __shfl_xor_sync(0xffffffffu, w, 1);
   w |= __shfl_xor_sync(0xffffffffu, w, 2);
   if ((lane & 3u) == 0 && v0 < n) bits[v0 >> 5] = w;
+  if (sum) {
+    // Star-0 summary: this block's 64 words -> 64 >> sum_shift bits (bit =
+    // every word of its group is all ones).  Star 0 only grows (pi(v) = 0
+    // is never rewritten), so bits only turn on: groups shared with other
+    // blocks are merged with atomicOr, whole summary words are stored.
+    __shared__ u32 s_full[8];
+    const u32 full = __ballot_sync(0xffffffffu, (lane & 3u) == 0 && v0 < n && w == ~0u);
+    u32 b8 = 0;  // bit j = word (warp * 8 + j) is all ones
+#pragma unroll
+    for (int j = 0; j < 8; ++j) b8 |= ((full >> (4 * j)) & 1u) << j;
+    if (sum_shift == 0) {
+      // one summary bit per word: a warp's 8 words are one summary byte
+      const u64 byte_idx = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+      if (lane == 0 && byte_idx < (u64)sum_words * 4)
+        reinterpret_cast<unsigned char*>(sum)[byte_idx] = (unsigned char)b8;
+    } else {
+    if (lane == 0) s_full[threadIdx.x >> 5] = b8;
+    __syncthreads();
+    if (threadIdx.x == 0 && blockDim.x == kVertThreads) {
+      u64 f = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) f |= (u64)s_full[i] << (8 * i);
+      const u32 g = 1u << sum_shift, nb = 64u >> sum_shift;
+      u64 bitsg = 0;
+      for (u32 i = 0; i < nb; ++i) {
+        const u64 mask = (g == 64 ? ~0ull : ((1ull << g) - 1)) << (i * g);
+        if ((f & mask) == mask) bitsg |= 1ull << i;
+      }
+      const u64 pos = (u64)blockIdx.x * nb;  // first summary bit of this block
+      if (nb >= 32) {
+        for (u32 k = 0; k < nb / 32; ++k)
+          if ((pos >> 5) + k < sum_words) sum[(pos >> 5) + k] = (u32)(bitsg >> (32 * k));
+      } else if (bitsg && (pos >> 5) < sum_words) {
+        atomicOr(sum + (pos >> 5), (u32)bitsg << (pos & 31));
+      }
+    }
+    }
+  }
   add_counter(&r->jump_steps, steps);
   block_t1(&r->comp_t1);
 }
@@ -775,7 +1050,25 @@ __global__ void k_step_segment(DevCtrl* c, DevRec* recs,
 
 // Adaptive segment finished: choose the next range from this segment's
 // store ratio (records are per segment).
-__global__ void k_step_adapt(DevCtrl* c, DevRec* recs, u64 m, u32 forming_pct) {
+__global__ void k_step_adapt(DevCtrl* c, DevRec* recs, u64 m, u32 forming_pct,
+                             const u32* sum, u32 sum_words) {
+  // Star-0 summary vote for the next hook launch (one block): the summary
+  // path pays off when at least half of the groups are covered.
+  if (sum) {
+    __shared__ u32 s_cov;
+    if (threadIdx.x == 0) s_cov = 0;
+    __syncthreads();
+    u32 cov = 0;
+    for (u32 i = threadIdx.x; i < sum_words; i += blockDim.x) cov += __popc(sum[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cov += __shfl_xor_sync(0xffffffffu, cov, o);
+    if ((threadIdx.x & 31u) == 0 && cov) atomicAdd(&s_cov, cov);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      c->use_sum = (u64)s_cov * 2 >= (u64)sum_words * 32 ? 1u : 0u;
+    }
+  }
+  if (threadIdx.x != 0) return;
   const DevRec& r = recs[c->rec < (u32)kMaxRecs ? c->rec : (u32)kMaxRecs - 1];
   const u64 len = c->seg_e - c->seg_b;
   const bool forming = r.edges_in > 0 && r.edges_out * 100 > r.edges_in * forming_pct;
