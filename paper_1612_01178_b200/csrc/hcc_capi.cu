@@ -488,6 +488,10 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           }
           if (P.hook_events) q.record(c->seg_ev[2 * sgi + 1]);
           q.phase_done(HCC_PHASE_HOOK);
+          // star of the next bitmap (the giant need not contain vertex 0)
+          // (not after the last slot: only the worklist passes would see it)
+          if (P.s0b && P.adapt && sgi >= 1 && sgi + 1 < P.nseg)
+            k_star_pick<<<1, 32, 0, q.s()>>>(P.pi, P.n, ctrl);
           // compress (+ star-0 bitmap, initialised by k_start)
           if (P.s0b)
             k_compress_s0b<<<grid_for((P.n + 7) / 8, kVertThreads, 0x7fffffffull),
@@ -1531,6 +1535,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
     if (o->algo == HCC_ALGO_BASELINE_MJ && !P.full_passes && !P.bounds.empty()) {
       const u64 wl = nrec > nseg ? nrec - nseg : 0;
       k += 3 * nseg + 3 * wl;  // hook+compress+step per slot and per wl pass
+      if (P.s0b && P.adapt && nseg >= 3) k += nseg - 2;  // k_star_pick, slots 1..nseg-2
       if (P.sum && P.adapt && nseg <= kMaxUnrolledSegments) {
         // voted launches: summary and plain hook back to back
         for (u64 sgi = 1; sgi < nseg; ++sgi) k += slot_small(P, sgi) ? 0 : 1;

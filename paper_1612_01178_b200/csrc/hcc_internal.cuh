@@ -76,6 +76,9 @@ struct DevCtrl {
   u64 seg_b, seg_e;  // adaptive topology plan: current segment range
   u64 t_start;       // globaltimer at k_start (span timeline origin)
   u32 use_sum;       // last summary vote (k_step_adapt): next hook uses k_hook_sum
+  u32 star_hint;     // a vertex of the component the star bitmap tracks
+  u32 star;          // its root at the last compress: bit v of the bitmap
+                     // means pi(v) == star (k_compress_s0b)
   u32 pad_;
 };
 
@@ -145,6 +148,7 @@ __global__ void k_init_pi(u32* pi, u64 n, u32* bits);
 __global__ void k_hook(HookArgs a);
 __global__ void k_hook_small(HookArgs a);
 __global__ void k_hook_sum(HookArgs a);
+__global__ void k_star_pick(const u32* pi, u64 n, DevCtrl* ctrl);
 __global__ void k_cas_hook(HookArgs a);
 __global__ void k_compress(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
                            int skip_if_clean);

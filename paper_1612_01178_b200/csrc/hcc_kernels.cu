@@ -96,6 +96,11 @@ __device__ __forceinline__ bool sum_covered(const u32* s_sum, u32 x, u32 shift) 
   return (s_sum[sum_swz(g >> 5)] >> (g & 31u)) & 1u;
 }
 
+// Control words a kernel reads at entry (dirty, star, use_sum) are written
+// only by earlier kernels, so they are read through the non-coherent path:
+// a volatile (L2) load by every thread of a 16K-block grid piles onto one
+// L2 slice (measured: +5-8 us per compress).
+
 // Coherent (L2) read: sees other threads' stores made during this kernel.
 __device__ __forceinline__ u32 ld_fresh(const u32* p) { return __ldcg(p); }
 
@@ -306,7 +311,7 @@ __global__ void k_init_pi(u32* pi, u64 n, u32* bits) {
 // hook tile).  Returns the mask of edges whose (h, l) pair in (pu, pv)
 // must be appended to the worklist (stored links and deferred walks).
 template <int S, bool SUM>
-__device__ __forceinline__ u32 resolve_edges(const HookArgs& a, const u32* s_sum,
+__device__ __forceinline__ u32 resolve_edges(const HookArgs& a, const u32* s_sum, u32 star,
                                              const uint2 (&ed)[S], u32 (&pu)[S],
                                              u32 (&pv)[S]) {
   u32* pi = a.pi;
@@ -327,8 +332,8 @@ __device__ __forceinline__ u32 resolve_edges(const HookArgs& a, const u32* s_sum
     }
 #pragma unroll
     for (int k = 0; k < S; ++k) {
-      pu[k] = (wu[k] >> (ed[k].x & 31u)) & 1u ? 0u : ld_pi(pi + ed[k].x);
-      pv[k] = (wv[k] >> (ed[k].y & 31u)) & 1u ? 0u : ld_pi(pi + ed[k].y);
+      pu[k] = (wu[k] >> (ed[k].x & 31u)) & 1u ? star : ld_pi(pi + ed[k].x);
+      pv[k] = (wv[k] >> (ed[k].y & 31u)) & 1u ? star : ld_pi(pi + ed[k].y);
     }
   } else {
 #pragma unroll
@@ -421,6 +426,8 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
   resolve_src(a, src, b, e, out);
   DevCtrl* ctrl = a.ctrl;
   DevRec* r = cur_rec(ctrl, a.recs);
+  // root of the star the bitmap tracks (set by the last compress)
+  const u32 star = a.s0b ? __ldg(&ctrl->star) : 0u;
   block_t0(&r->hook_t0);
   if (blockIdx.x == 0 && threadIdx.x == 0 && e > b) {
     atomicAdd(&r->edges_in, e - b);
@@ -529,7 +536,7 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
     }
     if (t + gridDim.x < ntiles) load_tile(t + gridDim.x, nq);
     u32 pu[EPT], pv[EPT];
-    const u32 act = resolve_edges<EPT, SUM>(a, s_sum, ed, pu, pv);
+    const u32 act = resolve_edges<EPT, SUM>(a, s_sum, star, ed, pu, pv);
     if (a.append) {
       u64 pos;
       if (block_reserve(__popc(act), cnt_out, pos, appended)) {
@@ -625,6 +632,8 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
   resolve_src(a, src, b, e, out);
   DevCtrl* ctrl = a.ctrl;
   DevRec* r = cur_rec(ctrl, a.recs);
+  // root of the star the bitmap tracks (set by the last compress)
+  const u32 star = a.s0b ? __ldg(&ctrl->star) : 0u;
   block_t0(&r->hook_t0);
   if (blockIdx.x == 0 && threadIdx.x == 0 && e > b) {
     atomicAdd(&r->edges_in, e - b);
@@ -649,7 +658,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
     if (lane == 0 && b2 != b) ed[0] = src[b];
     if (lane == 1 && ((e - b2) & 1ull)) ed[0] = src[e - 1];
     u32 h[1], l[1];
-    const u32 act = resolve_edges<1, false>(a, s_sum, ed, h, l);
+    const u32 act = resolve_edges<1, false>(a, s_sum, star, ed, h, l);
     warp_emit<1>(a, wo, wl_out, cnt_out, lane, act, h, l);
   }
 
@@ -677,7 +686,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
     if (t + gridDim.x < ntiles) load_tile(t + gridDim.x, nq);
     if (!SUM) {
       u32 h[EPT], l[EPT];
-      const u32 act = resolve_edges<EPT, false>(a, s_sum, ed, h, l);
+      const u32 act = resolve_edges<EPT, false>(a, s_sum, star, ed, h, l);
       warp_emit<EPT>(a, wo, wl_out, cnt_out, lane, act, h, l);
       continue;
     }
@@ -712,7 +721,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
         q2[j] = idx < total ? s_q[idx] : make_uint2(0u, 0u);
       }
       u32 h[S], l[S];
-      const u32 act = resolve_edges<S, true>(a, s_sum, q2, h, l);
+      const u32 act = resolve_edges<S, true>(a, s_sum, star, q2, h, l);
       warp_emit<S>(a, wo, wl_out, cnt_out, lane, act, h, l);
     }
     __syncwarp();
@@ -737,7 +746,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
 #endif
 __global__ void __launch_bounds__(kHookCta, HCC_HOOK_MINB) k_hook(HookArgs a) {
   // (the summary path is k_hook_sum; s0f is ignored here)
-  if (a.gate == kGateIfPlain && *(volatile u32*)&a.ctrl->use_sum) return;
+  if (a.gate == kGateIfPlain && __ldg(&a.ctrl->use_sum)) return;
   if (a.chunked && (blockDim.x & 31u) == 0)
     hook_stream<kHookEPT, false>(a);
   else
@@ -747,7 +756,7 @@ __global__ void __launch_bounds__(kHookCta, HCC_HOOK_MINB) k_hook(HookArgs a) {
 // Streaming hook with the star-0 summary in shared memory (full warps,
 // chunked appends, s0f set).
 __global__ void __launch_bounds__(kHookSumCta, 1) k_hook_sum(HookArgs a) {
-  if (a.gate == kGateIfSum && !*(volatile u32*)&a.ctrl->use_sum) return;
+  if (a.gate == kGateIfSum && !__ldg(&a.ctrl->use_sum)) return;
   hook_stream<kHookEPT, true>(a);
 }
 
@@ -803,7 +812,7 @@ __global__ void __launch_bounds__(kHookCta) k_cas_hook(HookArgs a) {
 // whose lanes are all in that state exit the chase loop together.
 __global__ void __launch_bounds__(kVertThreads)
     k_compress(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs, int skip_if_clean) {
-  if (skip_if_clean && *(volatile u32*)&ctrl->dirty == 0) return;
+  if (skip_if_clean && __ldg(&ctrl->dirty) == 0) return;
   DevRec* r = cur_rec(ctrl, recs);
   block_t0(&r->comp_t0);
   u64 steps = 0;
@@ -854,23 +863,88 @@ __global__ void __launch_bounds__(kVertThreads)
   block_t1(&r->comp_t1);
 }
 
+// Star choice after a topology hook (one warp): the bitmap built by the
+// next compress tracks the component of ctrl->star_hint.  A fixed 32-vertex
+// sample is chased to its roots; when one component clearly outnumbers the
+// tracked one (ER: the giant forms around vertex 1 while vertex 0 is still
+// isolated; any graph whose vertex 0 is isolated), the hint moves to it.
+constexpr int kStarChase = 32;
+
+__global__ void k_star_pick(const u32* pi, u64 n, DevCtrl* ctrl) {
+  const u32 lane = threadIdx.x & 31u;
+  if (threadIdx.x >= 32 || n == 0) return;
+  u64 hsh = (u64)(lane + 1) * 0x9E3779B97F4A7C15ull;
+  hsh ^= hsh >> 29;
+  hsh *= 0xBF58476D1CE4E5B9ull;
+  hsh ^= hsh >> 32;
+  // bounded chases: before a compress the trees can be long chains (grid
+  // rows); a sample that does not reach its root within the bound counts
+  // as unknown (~0); an unresolved current star (~0) leaves the next
+  // bitmap empty unless a candidate wins
+  u32 x = (u32)(hsh % n);
+  // the tracked star already holds a quarter of the sample: keep it (leaf
+  // slots are not written by a hook, so pi(x) == star still marks it)
+  const u32 star0 = *(volatile u32*)&ctrl->star;
+  if (star0 < n && ld_fresh(pi + star0) == star0 &&
+      __popc(__ballot_sync(0xffffffffu, ld_fresh(pi + x) == star0)) >= 8)
+    return;
+  bool rooted = false;
+  for (int i = 0; i < kStarChase && !rooted; ++i) {
+    const u32 p = ld_fresh(pi + x);
+    rooted = p == x;
+    x = p;
+  }
+  if (!rooted) x = ~0u;
+  u32 cur = ctrl->star_hint;
+  bool cur_rooted = false;
+  for (int i = 0; i < kStarChase && !cur_rooted; ++i) {
+    const u32 p = ld_fresh(pi + cur);
+    cur_rooted = p == cur;
+    cur = p;
+  }
+  if (!cur_rooted) cur = ~0u;
+  const u32 same = __match_any_sync(0xffffffffu, x);
+  unsigned long long best = x == ~0u ? 0ull : ((unsigned long long)__popc(same) << 32) | x;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+    best = y > best ? y : best;
+  }
+  const u32 n_cand = (u32)(best >> 32), cand = (u32)best;
+  const u32 n_cur = __popc(__ballot_sync(0xffffffffu, cur != ~0u && x == cur));
+  if (lane == 0) {
+    // publish the root the next compress builds the bitmap for
+    const u32 star = (n_cand >= 6 && n_cand > 2 * n_cur) ? cand : cur;
+    if (star != ~0u) ctrl->star_hint = star;
+    ctrl->star = star;
+  }
+}
+
 // Multi-Jump compress fused with the star-0 bitmap build (HC engine, full
 // grid): thread q owns vertices [4q, 4q+4); after the chases every thread
 // knows its vertices' roots, so bit v = (root(v) == 0) is assembled with
 // three warp shuffles (8 lanes = one 32-vertex word) and stored once.
-__global__ void __launch_bounds__(kVertThreads)
+#ifndef HCC_COMP_MINB
+#define HCC_COMP_MINB 6
+#endif
+__global__ void __launch_bounds__(kVertThreads, HCC_COMP_MINB)
     k_compress_s0b(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs, u32* bits,
                    int mode, u32* sum, u32 sum_words, u32 sum_shift) {
-  if (mode && *(volatile u32*)&ctrl->dirty == 0) return;
+  if (mode && __ldg(&ctrl->dirty) == 0) return;
   DevRec* r = cur_rec(ctrl, recs);
   block_t0(&r->comp_t0);
   u64 steps = 0;
   // Thread q owns vertices [8q, 8q+8): two 16-byte reads and eight parent
   // gathers in flight before any chase (ascending order is kept: a thread's
   // vertices are consecutive and blocks start in ascending order).
+  // The bitmap tracks the star rooted at ctrl->star: k_star_pick resolved
+  // it after the last hook (vertex 0, the initial star, is never hooked).
+  // Should it have been hooked since (a slot without a pick), no root
+  // equals it and this bitmap is simply empty.
+  const u32 star = __ldg(&ctrl->star);
   const u64 q = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   const u64 v0 = q << 3;
-  u32 byte = 0;  // bit j = (root(v0 + j) == 0)
+  u32 byte = 0;  // bit j = (root(v0 + j) == star)
   if (v0 + 8 <= n) {
     const uint4* p4 = reinterpret_cast<const uint4*>(pi) + (q << 1);
     const uint4 pa = __ldcg(p4), pb = __ldcg(p4 + 1);
@@ -923,7 +997,7 @@ __global__ void __launch_bounds__(kVertThreads)
       }
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) byte |= (a[j] == 0u) ? 1u << j : 0u;
+    for (int j = 0; j < 8; ++j) byte |= (a[j] == star) ? 1u << j : 0u;
   } else if (v0 < n) {
     for (u64 v = v0; v < n; ++v) {
       u32 a = ld_fresh(pi + v);
@@ -936,7 +1010,7 @@ __global__ void __launch_bounds__(kVertThreads)
           b = ld_fresh(pi + a);
         }
       }
-      byte |= (a == 0u) ? 1u << (u32)(v - v0) : 0u;
+      byte |= (a == star) ? 1u << (u32)(v - v0) : 0u;
     }
   }
   // four lanes = one 32-vertex word
@@ -977,8 +1051,13 @@ __global__ void __launch_bounds__(kVertThreads)
       if (nb >= 32) {
         for (u32 k = 0; k < nb / 32; ++k)
           if ((pos >> 5) + k < sum_words) sum[(pos >> 5) + k] = (u32)(bitsg >> (32 * k));
-      } else if (bitsg && (pos >> 5) < sum_words) {
-        atomicOr(sum + (pos >> 5), (u32)bitsg << (pos & 31));
+      } else if ((pos >> 5) < sum_words) {
+        // this block owns nb bits of a shared word: clear, then set (the
+        // star may have moved since the last compress)
+        const u32 mask = (u32)((1ull << nb) - 1) << (pos & 31);
+        const u32 val = (u32)bitsg << (pos & 31);
+        if (~val & mask) atomicAnd(sum + (pos >> 5), ~(mask & ~val));
+        if (val) atomicOr(sum + (pos >> 5), val);
       }
     }
     }
@@ -1052,7 +1131,7 @@ __global__ void k_step_segment(DevCtrl* c, DevRec* recs,
 // store ratio (records are per segment).
 __global__ void k_step_adapt(DevCtrl* c, DevRec* recs, u64 m, u32 forming_pct,
                              const u32* sum, u32 sum_words) {
-  // Star-0 summary vote for the next hook launch (one block): the summary
+  // Star summary vote for the next hook launch (one block): the summary
   // path pays off when at least half of the groups are covered.
   if (sum) {
     __shared__ u32 s_cov;

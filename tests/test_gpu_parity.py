@@ -479,6 +479,30 @@ def test_star0_bitmap_paths(ctx, oracle, spec):
                 os.environ.pop(k, None)
 
 
+@pytest.mark.parametrize("shift", [1, 977])
+def test_star_moves_off_vertex0(ctx, oracle, shift):
+    """Vertex 0 isolated (ER endpoints shifted by `shift`): the star bitmap must
+    follow the giant component's root (sampled on the device) and give the
+    oracle's labels under every plan, with and without the summary hook."""
+    import os
+    n = 1 << 21
+    e = oracle.gen_erx(n - shift, 5, 0, 12 * n).astype(np.uint64) + shift
+    g = ctx.graph_from_edges(e.astype(np.uint32), n)
+    want = oracle.cc(n, e)
+    assert want[0] == 0 and np.sum(want == 0) == 1  # vertex 0 alone
+    for s0f in ("1", "0"):
+        os.environ["HCC_S0F"] = s0f
+        try:
+            for plan in ("adapt:7:4", "adapt:9:4", "adapt:5:3"):
+                os.environ["HCC_PLAN"] = plan
+                lab, mx = ctx.cc(g, "baseline-mj")
+                assert np.array_equal(lab, want), (s0f, plan)
+        finally:
+            os.environ.pop("HCC_PLAN", None)
+            os.environ.pop("HCC_S0F", None)
+    g.close()
+
+
 def test_hook_events_flag_and_timeline(ctx, oracle, capi):
     """HCC_FLAG_HOOK_EVENTS adds per-launch CUDA events (bench roofline) without
     changing results; the device timeline is ordered hook -> compress -> next."""
