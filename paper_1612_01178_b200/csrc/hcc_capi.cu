@@ -409,6 +409,14 @@ bool slot_small(const Plan& P, u64 sgi) {
          seg_edges < (u64)P.grid_hook * P.block_hook * kHookEPT * 2;
 }
 
+// Streaming hook (chunked appends, full warps) or the block-aggregated one.
+void launch_hook(const Plan& P, cudaStream_t s, const HookArgs& a) {
+  if (a.chunked && (P.block_hook & 31u) == 0)
+    k_hook<<<P.grid_hook, P.block_hook, 0, s>>>(a);
+  else
+    k_hook_legacy<<<P.grid_hook, P.block_hook, 0, s>>>(a);
+}
+
 // Enqueue one full CC run (pi init through convergence) on seq.
 void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
   c->seg_ev_used = 0;
@@ -422,7 +430,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
   switch (P.algo) {
     case HCC_ALGO_BASELINE: {
       q.loop([&](cudaGraphConditionalHandle ho, int uo) {
-        k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(
+        launch_hook(P, q.s(), 
             hook_args(c, P, kSrcRange, 0));
         q.phase_done(HCC_PHASE_HOOK);
         q.loop([&](cudaGraphConditionalHandle hi, int ui) {
@@ -437,7 +445,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
     case HCC_ALGO_BASELINE_MJ: {
       if (P.full_passes) {
         q.loop([&](cudaGraphConditionalHandle h, int u) {
-          k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(
+          launch_hook(P, q.s(), 
               hook_args(c, P, kSrcRange, 0));
           q.phase_done(HCC_PHASE_HOOK);
           k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
@@ -481,9 +489,9 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
               hp.gate = kGateIfPlain;
               k_hook_sum<<<c->sms * c->occ_hook_sum, kHookSumCta, hook_smem(ha, kHookSumCta),
                            q.s()>>>(ha);
-              k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(hp);
+              launch_hook(P, q.s(), hp);
             } else {
-              k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(hp);
+              launch_hook(P, q.s(), hp);
             }
           }
           if (P.hook_events) q.record(c->seg_ev[2 * sgi + 1]);
@@ -508,19 +516,22 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           if (P.adapt) {
             // the next hook's summary vote rides on the step kernel (the
             // worklist passes reuse the last one: coverage only grows)
+            // and so does the bitmap-use decision (a 2048-endpoint sample)
             const bool vote = P.sum && sgi + 1 < P.nseg && !slot_small(P, sgi + 1);
-            if (vote)
-              k_step_adapt<<<1, 1024, 0, q.s()>>>(ctrl, recs, P.m, P.forming_pct, c->s0f,
-                                                 P.sum_words);
+            if (P.s0b)
+              k_step_adapt<<<1, 1024, 0, q.s()>>>(ctrl, recs, P.m, P.forming_pct,
+                                                 vote ? c->s0f : nullptr, P.sum_words,
+                                                 P.edges, c->s0b);
             else
-              k_step_adapt<<<1, 1, 0, q.s()>>>(ctrl, recs, P.m, P.forming_pct, nullptr, 0);
+              k_step_adapt<<<1, 1, 0, q.s()>>>(ctrl, recs, P.m, P.forming_pct, nullptr, 0,
+                                              nullptr, nullptr);
           } else
             k_step_segment<<<1, 1, 0, q.s()>>>(ctrl, recs, 0, 0);
         }
         c->seg_ev_used = P.hook_events ? P.nseg : 0;
       } else {
         q.loop([&](cudaGraphConditionalHandle h, int u) {
-          k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(
+          launch_hook(P, q.s(), 
               hook_args(c, P, kSrcSegment, 1));
           q.phase_done(HCC_PHASE_HOOK);
           k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
@@ -541,10 +552,10 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           wp.s0f = nullptr;
           k_hook_sum<<<c->sms * c->occ_hook_sum, kHookSumCta, hook_smem(wa, kHookSumCta),
                        q.s()>>>(wa);
-          k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(wp);
+          launch_hook(P, q.s(), wp);
         } else {
           wa.s0f = nullptr;
-          k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(wa);
+          launch_hook(P, q.s(), wa);
         }
         q.phase_done(HCC_PHASE_HOOK);
         if (P.s0b && !P.bounds.empty())
@@ -1983,7 +1994,7 @@ int hcc_rehook(hcc_ctx* c, hcc_forest* f, const uint32_t* dev_bits_or,
   DevCtrl* ctrl = c->d_ctrl;
   DevRec* recs = c->d_recs;
   q.loop([&](cudaGraphConditionalHandle h, int u) {
-    k_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(hook_args(c, P, kSrcWorklist, 1));
+    launch_hook(P, q.s(), hook_args(c, P, kSrcWorklist, 1));
     k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl, recs, 1);
     k_step_worklist<<<1, 1, 0, q.s()>>>(ctrl, recs, h, u);
   });

@@ -79,7 +79,7 @@ struct DevCtrl {
   u32 star_hint;     // a vertex of the component the star bitmap tracks
   u32 star;          // its root at the last compress: bit v of the bitmap
                      // means pi(v) == star (k_compress_s0b)
-  u32 pad_;
+  u32 use_bits;      // next plain hook looks the bitmap up (k_step_adapt)
 };
 
 // k_compress_s0b modes.
@@ -148,6 +148,7 @@ __global__ void k_init_pi(u32* pi, u64 n, u32* bits);
 __global__ void k_hook(HookArgs a);
 __global__ void k_hook_small(HookArgs a);
 __global__ void k_hook_sum(HookArgs a);
+__global__ void k_hook_legacy(HookArgs a);
 __global__ void k_star_pick(const u32* pi, u64 n, DevCtrl* ctrl);
 __global__ void k_cas_hook(HookArgs a);
 __global__ void k_compress(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
@@ -163,7 +164,8 @@ __global__ void k_step_worklist(DevCtrl* ctrl, DevRec* recs,
 __global__ void k_step_segment(DevCtrl* ctrl, DevRec* recs,
                                cudaGraphConditionalHandle h, int use_cond);
 __global__ void k_step_adapt(DevCtrl* ctrl, DevRec* recs, u64 m, u32 forming_pct,
-                             const u32* sum, u32 sum_words);
+                             const u32* sum, u32 sum_words, const uint2* edges,
+                             const u32* bits);
 __global__ void k_step_outer(DevCtrl* ctrl, DevRec* recs,
                              cudaGraphConditionalHandle h, int use_cond);
 __global__ void k_step_jump(DevCtrl* ctrl, cudaGraphConditionalHandle h,

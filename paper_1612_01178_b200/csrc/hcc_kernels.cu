@@ -267,6 +267,7 @@ __global__ void k_start(u32* pi, u64 n, u32* bits, DevCtrl* ctrl, DevRec* recs, 
     DevCtrl c = {};
     c.nseg = nseg ? nseg : 1;
     c.t_start = gtime();
+    c.use_bits = 1;
     if (plan_shift < 64) {
       u64 first = m >> plan_shift;
       if (first == 0) first = m < 1 ? m : 1;
@@ -311,23 +312,24 @@ __global__ void k_init_pi(u32* pi, u64 n, u32* bits) {
 // hook tile).  Returns the mask of edges whose (h, l) pair in (pu, pv)
 // must be appended to the worklist (stored links and deferred walks).
 template <int S, bool SUM>
-__device__ __forceinline__ u32 resolve_edges(const HookArgs& a, const u32* s_sum, u32 star,
+__device__ __forceinline__ u32 resolve_edges(const HookArgs& a, const u32* bits,
+                                             const u32* s_sum, u32 star,
                                              const uint2 (&ed)[S], u32 (&pu)[S],
                                              u32 (&pv)[S]) {
   u32* pi = a.pi;
-  if (a.s0b) {
-    // Star-0 bitmap: one L1-friendly word read answers pi(x) == 0 for
-    // the giant component's vertices; only the rest gather pi.
+  if (bits) {
+    // Star bitmap: one L1-friendly word read answers pi(x) == star for
+    // the tracked component's vertices; only the rest gather pi.
     u32 wu[S], wv[S];
 #pragma unroll
     for (int k = 0; k < S; ++k) {
       const u32 xu = ed[k].x >> 5, xv = ed[k].y >> 5;
       if (SUM) {
-        wu[k] = sum_covered(s_sum, ed[k].x, a.s0f_shift) ? ~0u : ld_bits(a.s0b + xu);
-        wv[k] = sum_covered(s_sum, ed[k].y, a.s0f_shift) ? ~0u : ld_bits(a.s0b + xv);
+        wu[k] = sum_covered(s_sum, ed[k].x, a.s0f_shift) ? ~0u : ld_bits(bits + xu);
+        wv[k] = sum_covered(s_sum, ed[k].y, a.s0f_shift) ? ~0u : ld_bits(bits + xv);
       } else {
-        wu[k] = ld_bits(a.s0b + xu);
-        wv[k] = ld_bits(a.s0b + xv);
+        wu[k] = ld_bits(bits + xu);
+        wv[k] = ld_bits(bits + xv);
       }
     }
 #pragma unroll
@@ -426,8 +428,10 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
   resolve_src(a, src, b, e, out);
   DevCtrl* ctrl = a.ctrl;
   DevRec* r = cur_rec(ctrl, a.recs);
-  // root of the star the bitmap tracks (set by the last compress)
+  // root of the star the bitmap tracks (set by the last compress), and
+  // whether the last step found the bitmap worth a lookup
   const u32 star = a.s0b ? __ldg(&ctrl->star) : 0u;
+  const u32* bits = (a.s0b && (SUM || __ldg(&ctrl->use_bits))) ? a.s0b : nullptr;
   block_t0(&r->hook_t0);
   if (blockIdx.x == 0 && threadIdx.x == 0 && e > b) {
     atomicAdd(&r->edges_in, e - b);
@@ -536,7 +540,7 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
     }
     if (t + gridDim.x < ntiles) load_tile(t + gridDim.x, nq);
     u32 pu[EPT], pv[EPT];
-    const u32 act = resolve_edges<EPT, SUM>(a, s_sum, star, ed, pu, pv);
+    const u32 act = resolve_edges<EPT, SUM>(a, bits, s_sum, star, ed, pu, pv);
     if (a.append) {
       u64 pos;
       if (block_reserve(__popc(act), cnt_out, pos, appended)) {
@@ -632,8 +636,10 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
   resolve_src(a, src, b, e, out);
   DevCtrl* ctrl = a.ctrl;
   DevRec* r = cur_rec(ctrl, a.recs);
-  // root of the star the bitmap tracks (set by the last compress)
+  // root of the star the bitmap tracks (set by the last compress), and
+  // whether the last step found the bitmap worth a lookup
   const u32 star = a.s0b ? __ldg(&ctrl->star) : 0u;
+  const u32* bits = (a.s0b && (SUM || __ldg(&ctrl->use_bits))) ? a.s0b : nullptr;
   block_t0(&r->hook_t0);
   if (blockIdx.x == 0 && threadIdx.x == 0 && e > b) {
     atomicAdd(&r->edges_in, e - b);
@@ -658,7 +664,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
     if (lane == 0 && b2 != b) ed[0] = src[b];
     if (lane == 1 && ((e - b2) & 1ull)) ed[0] = src[e - 1];
     u32 h[1], l[1];
-    const u32 act = resolve_edges<1, false>(a, s_sum, star, ed, h, l);
+    const u32 act = resolve_edges<1, false>(a, bits, s_sum, star, ed, h, l);
     warp_emit<1>(a, wo, wl_out, cnt_out, lane, act, h, l);
   }
 
@@ -686,7 +692,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
     if (t + gridDim.x < ntiles) load_tile(t + gridDim.x, nq);
     if (!SUM) {
       u32 h[EPT], l[EPT];
-      const u32 act = resolve_edges<EPT, false>(a, s_sum, star, ed, h, l);
+      const u32 act = resolve_edges<EPT, false>(a, bits, s_sum, star, ed, h, l);
       warp_emit<EPT>(a, wo, wl_out, cnt_out, lane, act, h, l);
       continue;
     }
@@ -721,7 +727,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
         q2[j] = idx < total ? s_q[idx] : make_uint2(0u, 0u);
       }
       u32 h[S], l[S];
-      const u32 act = resolve_edges<S, true>(a, s_sum, star, q2, h, l);
+      const u32 act = resolve_edges<S, true>(a, bits, s_sum, star, q2, h, l);
       warp_emit<S>(a, wo, wl_out, cnt_out, lane, act, h, l);
     }
     __syncwarp();
@@ -747,10 +753,14 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
 __global__ void __launch_bounds__(kHookCta, HCC_HOOK_MINB) k_hook(HookArgs a) {
   // (the summary path is k_hook_sum; s0f is ignored here)
   if (a.gate == kGateIfPlain && __ldg(&a.ctrl->use_sum)) return;
-  if (a.chunked && (blockDim.x & 31u) == 0)
-    hook_stream<kHookEPT, false>(a);
-  else
-    hook_impl<kHookEPT, false>(a);
+  hook_stream<kHookEPT, false>(a);
+}
+
+// Block-aggregated hook (per-tile block scan for appends): launches that are
+// not full warps or not sized for chunk padding (baseline passes, the
+// looped-segment path, re-hook, max_threads launches).
+__global__ void __launch_bounds__(kHookCta, HCC_HOOK_MINB) k_hook_legacy(HookArgs a) {
+  hook_impl<kHookEPT, false>(a);
 }
 
 // Streaming hook with the star-0 summary in shared memory (full warps,
@@ -1130,9 +1140,43 @@ __global__ void k_step_segment(DevCtrl* c, DevRec* recs,
 // Adaptive segment finished: choose the next range from this segment's
 // store ratio (records are per segment).
 __global__ void k_step_adapt(DevCtrl* c, DevRec* recs, u64 m, u32 forming_pct,
-                             const u32* sum, u32 sum_words) {
-  // Star summary vote for the next hook launch (one block): the summary
-  // path pays off when at least half of the groups are covered.
+                             const u32* sum, u32 sum_words, const uint2* edges,
+                             const u32* bits) {
+  __shared__ u64 s_b, s_e;
+  if (threadIdx.x == 0) {
+    const DevRec& r = recs[c->rec < (u32)kMaxRecs ? c->rec : (u32)kMaxRecs - 1];
+    const u64 len = c->seg_e - c->seg_b;
+    const bool forming = r.edges_in > 0 && r.edges_out * 100 > r.edges_in * forming_pct;
+    c->seg_b = c->seg_e;
+    u64 next = forming ? len * kAdaptGrowth : m;
+    if (next < 1) next = 1;
+    if (c->seg + 2 >= c->nseg) next = m;  // the next slot is the last one
+    c->seg_e = (m - c->seg_b) <= next ? m : c->seg_b + next;
+    c->seg += 1;
+    c->passes += (len > 0);
+    c->dirty = 0;
+    next_rec(c, recs);
+    s_b = c->seg_b;
+    s_e = c->seg_e;
+  }
+  if (blockDim.x == 1) return;
+  __syncthreads();
+  // Bitmap use for the next hook (one block): a lookup pays only when it
+  // usually answers; the share of the next segment's endpoints in the star
+  // decides (RMAT: 81-98% with hub words L1-resident; ER's giant at 37%
+  // made its bitmap lookups a net loss, 0.63 vs 0.51 ms).
+  if (bits && s_e > s_b) {
+    u64 hsh = (((u64)c->seg << 32) + threadIdx.x + 1) * 0x9E3779B97F4A7C15ull;
+    hsh ^= hsh >> 29;
+    hsh *= 0xBF58476D1CE4E5B9ull;
+    hsh ^= hsh >> 32;
+    const uint2 ed = edges[s_b + hsh % (s_e - s_b)];
+    const u32 hits = ((bits[ed.x >> 5] >> (ed.x & 31u)) & 1u) + ((bits[ed.y >> 5] >> (ed.y & 31u)) & 1u);
+    const int n_hit = __syncthreads_count(hits == 2) * 2 + __syncthreads_count(hits == 1);
+    if (threadIdx.x == 0) c->use_bits = (u32)n_hit * 2 >= 2 * blockDim.x ? 1u : 0u;
+  }
+  // Star summary vote for the next hook launch: the summary path pays off
+  // when at least half of the groups are covered.
   if (sum) {
     __shared__ u32 s_cov;
     if (threadIdx.x == 0) s_cov = 0;
@@ -1143,23 +1187,8 @@ __global__ void k_step_adapt(DevCtrl* c, DevRec* recs, u64 m, u32 forming_pct,
     for (int o = 16; o > 0; o >>= 1) cov += __shfl_xor_sync(0xffffffffu, cov, o);
     if ((threadIdx.x & 31u) == 0 && cov) atomicAdd(&s_cov, cov);
     __syncthreads();
-    if (threadIdx.x == 0) {
-      c->use_sum = (u64)s_cov * 2 >= (u64)sum_words * 32 ? 1u : 0u;
-    }
+    if (threadIdx.x == 0) c->use_sum = (u64)s_cov * 2 >= (u64)sum_words * 32 ? 1u : 0u;
   }
-  if (threadIdx.x != 0) return;
-  const DevRec& r = recs[c->rec < (u32)kMaxRecs ? c->rec : (u32)kMaxRecs - 1];
-  const u64 len = c->seg_e - c->seg_b;
-  const bool forming = r.edges_in > 0 && r.edges_out * 100 > r.edges_in * forming_pct;
-  c->seg_b = c->seg_e;
-  u64 next = forming ? len * kAdaptGrowth : m;
-  if (next < 1) next = 1;
-  if (c->seg + 2 >= c->nseg) next = m;  // the next slot is the last one
-  c->seg_e = (m - c->seg_b) <= next ? m : c->seg_b + next;
-  c->seg += 1;
-  c->passes += (len > 0);
-  c->dirty = 0;
-  next_rec(c, recs);
 }
 
 // Baseline outer iteration finished: loop while some hook changed.
