@@ -77,11 +77,6 @@ __device__ __forceinline__ u32 ld_bits(const u32* p) {
 #endif
 }
 
-// Same-round store visibility between a thread's walks (see hook_impl).
-#ifndef HCC_HOOK_DEDUP
-#define HCC_HOOK_DEDUP 0
-#endif
-
 // Shared-memory slot of summary word i: each 32-word row is XOR-permuted by
 // a hash of its row index.  Skewed graphs hit summary words whose indices
 // have few one bits (RMAT hubs: 0, 32, 64, 1024, ...), which would all sit
@@ -373,22 +368,12 @@ __device__ __forceinline__ u32 resolve_edges(const HookArgs& a, const u32* bits,
     u32 ph[S];
 #pragma unroll
     for (int k = 0; k < S; ++k) ph[k] = walking & (1u << k) ? ld_pi(pi + pu[k]) : 0u;
-    u32 fresh = 0;  // edges that stored in this round
 #pragma unroll
     for (int k = 0; k < S; ++k) {
       if (!(walking & (1u << k))) continue;
-      // A root this thread linked earlier in the round: see that store,
-      // as a one-edge-at-a-time walk would (stores of earlier rounds are
-      // seen through memory).
-      u32 p = ph[k];
-#if HCC_HOOK_DEDUP
-#pragma unroll
-      for (int k2 = 0; k2 < k; ++k2)
-        if ((fresh & (1u << k2)) && pu[k2] == pu[k]) p = pv[k2];
-#endif
+      const u32 p = ph[k];
       if (p == pu[k]) {               // root: store now
         pi[pu[k]] = pv[k];
-        fresh |= 1u << k;
         walking &= ~(1u << k);
       } else if (p == pv[k]) {        // already linked
         act &= ~(1u << k);
