@@ -352,6 +352,7 @@ struct Plan {
   bool s0b;                 // star-0 bitmap for hook passes after a compress
   bool sum = false;         // star-0 summary staged in the hook's shared memory
   bool chunked = false;     // streaming hooks with per-warp chunked appends
+  bool small_slots = true;  // forming slots below two tiles use k_hook_small
   u32 sum_words = 0, sum_shift = 0;
   bool hook_events = false;  // CUDA events around unrolled hook launches
   bool adapt;               // device-side adaptive topology plan
@@ -405,7 +406,7 @@ constexpr size_t kHookSmemMax = kS0fMaxBytes + (size_t)kHookSumCta * kHookEPT * 
 // Unrolled topology slot that runs the small-segment hook (forming regime).
 bool slot_small(const Plan& P, u64 sgi) {
   const u64 seg_edges = P.bounds[sgi + 1] - P.bounds[sgi];  // adaptive: estimate
-  return P.block_hook == kHookCta &&
+  return P.small_slots && P.block_hook == kHookCta &&
          seg_edges < (u64)P.grid_hook * P.block_hook * kHookEPT * 2;
 }
 
@@ -475,7 +476,8 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
             // forming-regime segment: EPT 2 over a full grid
             ha.s0f = nullptr;
             const u64 seg_edges = ha.e - ha.b;  // adaptive: the static estimate
-            k_hook_small<<<grid_for((seg_edges + 1) / 2 + 1, kHookThreads, 0x7fffffffull),
+            k_hook_small<<<grid_for((seg_edges + kSmallEPT - 1) / kSmallEPT + 1, kHookThreads,
+                                    0x7fffffffull),
                            kHookThreads, 0, q.s()>>>(ha);
           } else {
             ha.chunked = P.chunked ? 1 : 0;
@@ -1332,6 +1334,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   P.adapt = adapt;
   P.adapt_shift = adapt_shift;
   P.hook_events = (o->flags & HCC_FLAG_HOOK_EVENTS) != 0;
+  if (const char* e = std::getenv("HCC_HOOK_SMALL")) P.small_slots = std::atoi(e) != 0;
   P.forming_pct = std::getenv("HCC_FORMING_PCT") ? (u32)std::atoi(std::getenv("HCC_FORMING_PCT"))
                                                   : kAdaptFormingPct;
   if (P.s0b) {
@@ -1425,6 +1428,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   key.walk = P.walk;
   key.s0b = P.s0b;
   key.sum = P.sum;
+  key.plan = key.plan * 7 + (P.small_slots ? 1 : 0);
   key.plan = key.plan * 31 + (P.adapt ? 1000 + P.adapt_shift + 100000ull * P.forming_pct : 0);
   for (u64 x : P.bounds) key.plan = key.plan * 1000003ull + x;
 

@@ -23,6 +23,10 @@ typedef unsigned int u32;
 
 constexpr int kMaxRecs = 4096;    // per-run phase records kept on device
 constexpr int kHookThreads = 256;
+#ifndef HCC_SMALL_EPT
+#define HCC_SMALL_EPT 2
+#endif
+constexpr int kSmallEPT = HCC_SMALL_EPT;  // k_hook_small edges per thread
 // Streaming hook CTA (k_hook): threads per CTA; its shared-memory star-0
 // summary table holds at most HCC_S0F_MAX_BYTES.
 #ifndef HCC_HOOK_CTA

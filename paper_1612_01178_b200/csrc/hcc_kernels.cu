@@ -778,11 +778,10 @@ __global__ void __launch_bounds__(kHookSumCta, 1) k_hook_sum(HookArgs a) {
   hook_stream<kHookEPT, true>(a);
 }
 
-// Small segments (the forming regime): two edges per thread, one tile per
-// block over a full grid, so long root walks run side by side instead of
-// eight deep per thread.
+// Small segments (the forming regime): kSmallEPT (2) edges per thread, one
+// tile per block over a full grid, two-sided walks.
 __global__ void __launch_bounds__(kHookThreads) k_hook_small(HookArgs a) {
-  hook_impl<2, false, true>(a);
+  hook_impl<kSmallEPT, false, true>(a);
 }
 
 // CAS-verified hook (forest.hpp:107-122): walks down until it acquires a
@@ -1189,8 +1188,22 @@ __global__ void k_step_adapt(DevCtrl* c, DevRec* recs, u64 m, u32 forming_pct,
     __shared__ u32 s_cov;
     if (threadIdx.x == 0) s_cov = 0;
     __syncthreads();
+    // 16-byte loads, four in flight per thread (the table is 64 KB at most;
+    // a serial word loop was ~10 us of the step)
     u32 cov = 0;
-    for (u32 i = threadIdx.x; i < sum_words; i += blockDim.x) cov += __popc(sum[i]);
+    const uint4* s4 = reinterpret_cast<const uint4*>(sum);
+    const u32 n4 = sum_words / 4;
+    for (u32 i = threadIdx.x; i < n4; i += 4 * blockDim.x) {
+      uint4 q[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const u32 k = i + (u32)j * blockDim.x;
+        q[j] = k < n4 ? __ldg(s4 + k) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cov += __popc(q[j].x) + __popc(q[j].y) + __popc(q[j].z) + __popc(q[j].w);
+    }
+    for (u32 i = n4 * 4 + threadIdx.x; i < sum_words; i += blockDim.x) cov += __popc(sum[i]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) cov += __shfl_xor_sync(0xffffffffu, cov, o);
     if ((threadIdx.x & 31u) == 0 && cov) atomicAdd(&s_cov, cov);
