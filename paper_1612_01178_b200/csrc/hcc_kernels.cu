@@ -99,6 +99,22 @@ __device__ __forceinline__ bool sum_covered(const u32* s_sum, u32 x, u32 shift) 
 // Coherent (L2) read: sees other threads' stores made during this kernel.
 __device__ __forceinline__ u32 ld_fresh(const u32* p) { return __ldcg(p); }
 
+// Compress chase step.  During a compress no root changes, so a stale value
+// (an older ancestor) is safe and a root always reads as itself.  Through L1:
+// chases into a giant component all end on the same few root lines, and as
+// coherent L2 loads they queued on one L2 slice (ER-2^24's forming
+// compresses 0.25 -> 0.13 ms, grid -46 us).  HCC_CHASE_L1=0 restores them.
+#ifndef HCC_CHASE_L1
+#define HCC_CHASE_L1 1
+#endif
+__device__ __forceinline__ u32 ld_chase(const u32* p) {
+#if HCC_CHASE_L1
+  return ld_pi(p);
+#else
+  return ld_fresh(p);
+#endif
+}
+
 __device__ __forceinline__ void rec_clear(DevRec& r) {
   r.hook_t0 = ~0ull;
   r.hook_t1 = 0;
@@ -856,24 +872,26 @@ __global__ void __launch_bounds__(kVertThreads)
       // parent inside this group: re-read after the earlier chases wrote it
       // (keeps the one-thread schedule identical to the reference's
       // sequential ascending pass, forest.hpp:127-136 / parallel.hpp:52-55)
-      if (j > 0 && a >= v0 && a != v0 + j) b = ld_fresh(pi + a);
+      // (own writes are visible to the L1-cached reads, so a one-thread
+      // launch reads exactly what the reference's sequential pass reads)
+      if (j > 0 && a >= v0 && a != v0 + j) b = ld_chase(pi + a);
       while (b != a) {  // eager writes: every step is visible to other chasers
         pi[v0 + j] = b;
         ++steps;
         a = b;
-        b = ld_fresh(pi + a);
+        b = ld_chase(pi + a);
       }
     }
   }
   for (u64 v = (n4 << 2) + tid; v < n; v += stride) {
-    u32 a = ld_fresh(pi + v);
+    u32 a = ld_chase(pi + v);
     if (a == (u32)v) continue;
-    u32 b = ld_fresh(pi + a);
+    u32 b = ld_chase(pi + a);
     while (b != a) {
       pi[v] = b;
       ++steps;
       a = b;
-      b = ld_fresh(pi + a);
+      b = ld_chase(pi + a);
     }
   }
   add_counter(&r->jump_steps, steps);
@@ -993,7 +1011,7 @@ __global__ void __launch_bounds__(kVertThreads, HCC_COMP_MINB)
           pi[v0 + j] = b[j];
           ++steps;
           a[j] = b[j];
-          b[j] = ld_fresh(pi + a[j]);
+          b[j] = ld_chase(pi + a[j]);
         }
 #pragma unroll
       for (int j = 0; j < 8; ++j)
@@ -1017,14 +1035,14 @@ __global__ void __launch_bounds__(kVertThreads, HCC_COMP_MINB)
     for (int j = 0; j < 8; ++j) byte |= (a[j] == star) ? 1u << j : 0u;
   } else if (v0 < n) {
     for (u64 v = v0; v < n; ++v) {
-      u32 a = ld_fresh(pi + v);
+      u32 a = ld_chase(pi + v);
       if (a != (u32)v) {
-        u32 b = ld_fresh(pi + a);
+        u32 b = ld_chase(pi + a);
         while (b != a) {
           pi[v] = b;
           ++steps;
           a = b;
-          b = ld_fresh(pi + a);
+          b = ld_chase(pi + a);
         }
       }
       byte |= (a == star) ? 1u << (u32)(v - v0) : 0u;
