@@ -88,6 +88,11 @@ constexpr u32 kAdaptShift = 7;
 // Unrolled adaptive slots (HCC_PLAN=adapt:<k>:<slots>); the last takes every
 // remaining edge, so a plan never needs an empty trailing launch.
 constexpr int kAdaptSlots = 4;
+// Floor of the first adaptive segment: n >> kAdaptNShift edges
+// (HCC_PLAN_NSHIFT; 0 disables, the default).  n/8 takes sparse ER (2^25
+// vertices, 4 edges each) from 5.2 to 4.0 ms but costs grid 4096^2 0.1 ms
+// (a lattice wants a small first segment); the BASELINE configs are dense.
+constexpr u32 kAdaptNShift = 0;
 
 int usable_devices() {
   int count = 0;
@@ -356,7 +361,8 @@ struct Plan {
   u32 sum_words = 0, sum_shift = 0;
   bool hook_events = false;  // CUDA events around unrolled hook launches
   bool adapt;               // device-side adaptive topology plan
-  u32 adapt_shift;          // first adaptive segment = m >> adapt_shift
+  u32 adapt_shift;          // first adaptive segment = m >> adapt_shift ...
+  u64 adapt_first = 0;      // ... or n >> kAdaptNShift if larger (edges)
   u32 forming_pct;          // store ratio (%) above which a segment is forming
   unsigned grid_hook, block_hook, grid_vert, block_vert;
 };
@@ -423,7 +429,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
   c->seg_ev_used = 0;
   k_start<<<P.grid_vert, P.block_vert, 0, q.s()>>>(
       P.pi, P.n, P.s0b ? c->s0b : nullptr, c->d_ctrl, c->d_recs, P.nseg, P.m,
-      P.adapt ? P.adapt_shift : 64u, P.sum ? c->s0f : nullptr, P.sum_words);
+      P.adapt ? P.adapt_first : 0, P.sum ? c->s0f : nullptr, P.sum_words);
   HCC_CUDA(cudaGetLastError());
   DevCtrl* ctrl = c->d_ctrl;
   DevRec* recs = c->d_recs;
@@ -1256,6 +1262,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   std::vector<u64> bounds;
   bool adapt = false;
   u32 adapt_shift = kAdaptShift;
+  u64 adapt_first = 0;
   if (geo_plan) {
     const char* pe = std::getenv("HCC_PLAN");
     int sh = 0;
@@ -1272,7 +1279,18 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
       }
       // at most `slots` launches; the device gives the last one every
       // remaining edge (k_step_adapt)
-      u64 first = std::max<u64>(1, m >> adapt_shift), len = first, covered = first;
+      // first segment: m/128, optionally at least n >> nshift edges.
+      // Forming lasts a number of edges proportional to n (the giant
+      // emerges near n/2), so sparse graphs (m = 4n) would want the
+      // n-relative floor for the forming slots to finish before the last
+      // slot takes the rest (see kAdaptNShift).
+      u32 nshift = kAdaptNShift;
+      if (const char* e2 = std::getenv("HCC_PLAN_NSHIFT")) nshift = (u32)std::atoi(e2);
+      const u64 nfloor = nshift && nshift < 64 ? (n >> nshift) : 0;
+      u64 first = std::min<u64>(std::max<u64>(std::max<u64>(1, m >> adapt_shift), nfloor),
+                                std::max<u64>(m, 1));
+      adapt_first = first;
+      u64 len = first, covered = first;
       nseg = 1;
       while (covered < m && nseg < (u64)slots) {
         len = std::min<u64>(len * kAdaptGrowth, m - covered);
@@ -1333,6 +1351,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   P.s0b = s0b && !bounds.empty();
   P.adapt = adapt;
   P.adapt_shift = adapt_shift;
+  P.adapt_first = adapt_first;
   P.hook_events = (o->flags & HCC_FLAG_HOOK_EVENTS) != 0;
   if (const char* e = std::getenv("HCC_HOOK_SMALL")) P.small_slots = std::atoi(e) != 0;
   P.forming_pct = std::getenv("HCC_FORMING_PCT") ? (u32)std::atoi(std::getenv("HCC_FORMING_PCT"))
@@ -1430,6 +1449,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   key.sum = P.sum;
   key.plan = key.plan * 7 + (P.small_slots ? 1 : 0);
   key.plan = key.plan * 31 + (P.adapt ? 1000 + P.adapt_shift + 100000ull * P.forming_pct : 0);
+  key.plan = key.plan * 1000003ull + P.adapt_first;
   for (u64 x : P.bounds) key.plan = key.plan * 1000003ull + x;
 
   if (graph_mode) {

@@ -22,7 +22,10 @@ typedef unsigned long long u64;
 typedef unsigned int u32;
 
 constexpr int kMaxRecs = 4096;    // per-run phase records kept on device
-constexpr int kHookThreads = 256;
+#ifndef HCC_SMALL_CTA
+#define HCC_SMALL_CTA 256
+#endif
+constexpr int kHookThreads = HCC_SMALL_CTA;  // k_hook_small CTA (full grid)
 #ifndef HCC_SMALL_EPT
 #define HCC_SMALL_EPT 2
 #endif
@@ -161,7 +164,7 @@ __global__ void k_compress_s0b(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
                                u32* bits, int skip_if_clean, u32* sum, u32 sum_words,
                                u32 sum_shift);
 __global__ void k_start(u32* pi, u64 n, u32* bits, DevCtrl* ctrl, DevRec* recs, u64 nseg,
-                        u64 m, u32 plan_shift, u32* sum, u32 sum_words);
+                        u64 m, u64 plan_first, u32* sum, u32 sum_words);
 __global__ void k_jump(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs);
 __global__ void k_step_worklist(DevCtrl* ctrl, DevRec* recs,
                                 cudaGraphConditionalHandle h, int use_cond);

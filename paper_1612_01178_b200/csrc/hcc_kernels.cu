@@ -270,18 +270,17 @@ __global__ void k_begin(DevCtrl* ctrl, DevRec* recs, u64 nseg) {
 }
 
 // Run start: control block + first record (k_begin), the adaptive plan's
-// first range (plan_shift < 64), and pi(v) = v + the star-0 bitmap
-// (k_init_pi), in one launch.
+// first range (plan_first > 0), and pi(v) = v + the star bitmap and
+// summary (k_init_pi), in one launch.
 __global__ void k_start(u32* pi, u64 n, u32* bits, DevCtrl* ctrl, DevRec* recs, u64 nseg,
-                        u64 m, u32 plan_shift, u32* sum, u32 sum_words) {
+                        u64 m, u64 plan_first, u32* sum, u32 sum_words) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     DevCtrl c = {};
     c.nseg = nseg ? nseg : 1;
     c.t_start = gtime();
     c.use_bits = 1;
-    if (plan_shift < 64) {
-      u64 first = m >> plan_shift;
-      if (first == 0) first = m < 1 ? m : 1;
+    if (plan_first) {  // adaptive plan: the first range (the host sized it)
+      u64 first = plan_first < m ? plan_first : m;
       if (c.nseg <= 1) first = m;  // a single slot takes every edge
       c.seg_e = first;
     }

@@ -40,6 +40,18 @@ def test_full_size_configs_exact(ctx, oracle, spec):
         assert np.array_equal(lab2, want)
 
 
+def test_grouped_summary_exact(ctx, oracle):
+    """n = 2^24 + 1: 524,289 bitmap words, so the star summary holds one bit
+    per 2 words (shift 1; blocks share summary words: clear-then-set
+    atomics), and ER's giant makes the device vote pick the summary hook for
+    the steady slot."""
+    g = ctx.generate("erx:n=16777217,m=268435456,seed=2")
+    want = oracle.cc(g.n, g.edges())
+    lab, mx = ctx.cc(g, "baseline-mj")
+    assert np.array_equal(lab, want)
+    assert mx["star0_bitmap"]
+
+
 def test_rmat16_reference_generator_exact(ctx, oracle):
     """The reference's own rmat(16, 16, 1) graph (BASELINE configs[0])."""
     e = oracle.gen_rmat(16, 16, 1)
