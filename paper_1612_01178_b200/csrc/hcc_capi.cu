@@ -424,6 +424,14 @@ void launch_hook(const Plan& P, cudaStream_t s, const HookArgs& a) {
     k_hook_legacy<<<P.grid_hook, P.block_hook, 0, s>>>(a);
 }
 
+// Topology slot whose hook is voted between the summary and the plain
+// streaming hook: the last one (the steady segment).  Earlier slots are in
+// the forming regime, where no measured graph covers half of its summary
+// groups, and a voted slot costs a second (gated) launch.
+bool sum_slot(const Plan& P, u64 sgi) {
+  return P.sum && P.adapt && sgi >= 1 && sgi + 1 == P.nseg && !slot_small(P, sgi);
+}
+
 // Enqueue one full CC run (pi init through convergence) on seq.
 void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
   c->seg_ev_used = 0;
@@ -489,7 +497,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
             ha.chunked = P.chunked ? 1 : 0;
             HookArgs hp = ha;  // plain streaming hook: bitmap only, full L1
             hp.s0f = nullptr;
-            if (P.sum && sgi >= 1 && P.adapt) {
+            if (sum_slot(P, sgi)) {
               // the previous step's device vote picks the summary hook or
               // the plain one; the other launch exits at entry (cheaper
               // than an IF/ELSE graph node, measured ~20 us per slot)
@@ -525,7 +533,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
             // the next hook's summary vote rides on the step kernel (the
             // worklist passes reuse the last one: coverage only grows)
             // and so does the bitmap-use decision (a 2048-endpoint sample)
-            const bool vote = P.sum && sgi + 1 < P.nseg && !slot_small(P, sgi + 1);
+            const bool vote = sgi + 1 < P.nseg && sum_slot(P, sgi + 1);
             if (P.s0b)
               k_step_adapt<<<1, 1024, 0, q.s()>>>(ctrl, recs, P.m, P.forming_pct,
                                                  vote ? c->s0f : nullptr, P.sum_words,
@@ -1573,7 +1581,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
       if (P.s0b && P.adapt && nseg >= 3) k += nseg - 2;  // k_star_pick, slots 1..nseg-2
       if (P.sum && P.adapt && nseg <= kMaxUnrolledSegments) {
         // voted launches: summary and plain hook back to back
-        for (u64 sgi = 1; sgi < nseg; ++sgi) k += slot_small(P, sgi) ? 0 : 1;
+        for (u64 sgi = 1; sgi < nseg; ++sgi) k += sum_slot(P, sgi) ? 1 : 0;
         k += wl;
       }
     } else {
