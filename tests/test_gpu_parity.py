@@ -479,6 +479,28 @@ def test_star0_bitmap_paths(ctx, oracle, spec):
                 os.environ.pop(k, None)
 
 
+def test_degenerate_graphs_with_star_machinery(ctx, oracle):
+    """n >= 2^16 turns on the star bitmap, summary, sampler and chunked
+    appends: empty, single-edge, self-loop-only and boundary-vertex graphs."""
+    n = 70001  # not a multiple of 32: partial last bitmap / summary words
+    rng = np.random.default_rng(5)
+    cases = {
+        "empty": np.zeros((0, 2), np.uint64),
+        "one": np.array([[n - 1, 0]], np.uint64),
+        "loops": np.repeat(np.arange(0, n, 7, dtype=np.uint64)[:, None], 2, axis=1),
+        "last": np.stack([np.full(5000, n - 1, np.uint64),
+                          rng.integers(0, n, 5000).astype(np.uint64)], axis=1),
+        "path_rev": np.stack([np.arange(n - 1, 0, -1, dtype=np.uint64),
+                              np.arange(n - 2, -1, -1, dtype=np.uint64)], axis=1),
+    }
+    for name, e in cases.items():
+        want = oracle.cc(n, e)
+        for algo in ALGOS:
+            lab, mx = run(ctx, n, e, algo)
+            assert np.array_equal(lab, want.astype(np.uint64)), (name, algo)
+            assert mx["components"] == int(np.sum(want == np.arange(n, dtype=np.uint32)))
+
+
 @pytest.mark.parametrize("shift", [1, 977])
 def test_star_moves_off_vertex0(ctx, oracle, shift):
     """Vertex 0 isolated (ER endpoints shifted by `shift`): the star bitmap must
