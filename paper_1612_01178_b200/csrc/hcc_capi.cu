@@ -358,6 +358,10 @@ struct Plan {
   bool sum = false;         // star-0 summary staged in the hook's shared memory
   bool chunked = false;     // streaming hooks with per-warp chunked appends
   bool small_slots = true;  // forming slots below two tiles use k_hook_small
+  // HCC_HOOK_CAS: root stores by CAS (no record, no re-check) in 0: no
+  // launch; 1: the worklist passes (stores are rare there); 2: also the
+  // last topology slot
+  int cas_mode = 1;
   u32 sum_words = 0, sum_shift = 0;
   bool hook_events = false;  // CUDA events around unrolled hook launches
   bool adapt;               // device-side adaptive topology plan
@@ -385,6 +389,7 @@ HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
   a.wl_cap = c->wl_cap;
   a.chunked = 0;
   a.gate = kGateAlways;
+  a.cas = 0;
   a.ctrl = c->d_ctrl;
   a.recs = c->d_recs;
   return a;
@@ -418,10 +423,23 @@ bool slot_small(const Plan& P, u64 sgi) {
 
 // Streaming hook (chunked appends, full warps) or the block-aggregated one.
 void launch_hook(const Plan& P, cudaStream_t s, const HookArgs& a) {
-  if (a.chunked && (P.block_hook & 31u) == 0)
-    k_hook<<<P.grid_hook, P.block_hook, 0, s>>>(a);
-  else
+  if (a.chunked && (P.block_hook & 31u) == 0) {
+    if (a.cas)
+      k_hook_cas<<<P.grid_hook, P.block_hook, 0, s>>>(a);
+    else
+      k_hook<<<P.grid_hook, P.block_hook, 0, s>>>(a);
+  } else {
     k_hook_legacy<<<P.grid_hook, P.block_hook, 0, s>>>(a);
+  }
+}
+
+// The summary hook (one CTA per SM, the summary and queues in shared memory).
+void launch_hook_sum(hcc_ctx* c, cudaStream_t s, const HookArgs& a) {
+  const size_t smem = hook_smem(a, kHookSumCta);
+  if (a.cas)
+    k_hook_sum_cas<<<c->sms * c->occ_hook_sum, kHookSumCta, smem, s>>>(a);
+  else
+    k_hook_sum<<<c->sms * c->occ_hook_sum, kHookSumCta, smem, s>>>(a);
 }
 
 // Topology slot whose hook is voted between the summary and the plain
@@ -495,6 +513,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
                            kHookThreads, 0, q.s()>>>(ha);
           } else {
             ha.chunked = P.chunked ? 1 : 0;
+            ha.cas = P.cas_mode >= 2 && sgi + 1 == P.nseg ? 1 : 0;
             HookArgs hp = ha;  // plain streaming hook: bitmap only, full L1
             hp.s0f = nullptr;
             if (sum_slot(P, sgi)) {
@@ -503,8 +522,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
               // than an IF/ELSE graph node, measured ~20 us per slot)
               ha.gate = kGateIfSum;
               hp.gate = kGateIfPlain;
-              k_hook_sum<<<c->sms * c->occ_hook_sum, kHookSumCta, hook_smem(ha, kHookSumCta),
-                           q.s()>>>(ha);
+              launch_hook_sum(c, q.s(), ha);
               launch_hook(P, q.s(), hp);
             } else {
               launch_hook(P, q.s(), hp);
@@ -561,13 +579,13 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
         HookArgs wa = hook_args(c, P, kSrcWorklist, 1);
         if (P.s0b && !P.bounds.empty()) use_s0b(c, P, wa);
         wa.chunked = P.chunked ? 1 : 0;
+        wa.cas = P.cas_mode >= 1 && P.chunked ? 1 : 0;
         if (wa.s0f && P.adapt) {
           HookArgs wp = wa;
           wa.gate = kGateIfSum;
           wp.gate = kGateIfPlain;
           wp.s0f = nullptr;
-          k_hook_sum<<<c->sms * c->occ_hook_sum, kHookSumCta, hook_smem(wa, kHookSumCta),
-                       q.s()>>>(wa);
+          launch_hook_sum(c, q.s(), wa);
           launch_hook(P, q.s(), wp);
         } else {
           wa.s0f = nullptr;
@@ -786,6 +804,8 @@ int hcc_create(int device, hcc_ctx** out) {
   c->occ_hook = std::max(occ, 1);
   // the summary hook stages the star-0 summary and its slow-path queues
   HCC_CUDA(cudaFuncSetAttribute(k_hook_sum, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kHookSmemMax));
+  HCC_CUDA(cudaFuncSetAttribute(k_hook_sum_cas, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kHookSmemMax));
   HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_sum, kHookSumCta,
                                                           kHookSmemMax));
@@ -1362,6 +1382,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   P.adapt_first = adapt_first;
   P.hook_events = (o->flags & HCC_FLAG_HOOK_EVENTS) != 0;
   if (const char* e = std::getenv("HCC_HOOK_SMALL")) P.small_slots = std::atoi(e) != 0;
+  if (const char* e = std::getenv("HCC_HOOK_CAS")) P.cas_mode = std::atoi(e);
   P.forming_pct = std::getenv("HCC_FORMING_PCT") ? (u32)std::atoi(std::getenv("HCC_FORMING_PCT"))
                                                   : kAdaptFormingPct;
   if (P.s0b) {
@@ -1456,6 +1477,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   key.s0b = P.s0b;
   key.sum = P.sum;
   key.plan = key.plan * 7 + (P.small_slots ? 1 : 0);
+  key.plan = key.plan * 5 + (u64)P.cas_mode;
   key.plan = key.plan * 31 + (P.adapt ? 1000 + P.adapt_shift + 100000ull * P.forming_pct : 0);
   key.plan = key.plan * 1000003ull + P.adapt_first;
   for (u64 x : P.bounds) key.plan = key.plan * 1000003ull + x;

@@ -133,6 +133,8 @@ struct HookArgs {
   int chunked;       // full-warp launch with per-warp chunked appends
                      // (padding records; the host sized the worklists)
   int gate;          // kGate*: run only if ctrl->use_sum says so
+  int cas;           // launch the CAS-storing kernel (k_hook_cas /
+                     // k_hook_sum_cas): links are not recorded
   u32* pi;
   uint2* wl0;
   uint2* wl1;
@@ -156,6 +158,8 @@ __global__ void k_hook(HookArgs a);
 __global__ void k_hook_small(HookArgs a);
 __global__ void k_hook_sum(HookArgs a);
 __global__ void k_hook_legacy(HookArgs a);
+__global__ void k_hook_cas(HookArgs a);
+__global__ void k_hook_sum_cas(HookArgs a);
 __global__ void k_star_pick(const u32* pi, u64 n, DevCtrl* ctrl);
 __global__ void k_cas_hook(HookArgs a);
 __global__ void k_compress(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,

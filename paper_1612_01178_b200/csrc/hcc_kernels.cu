@@ -321,8 +321,8 @@ __global__ void k_init_pi(u32* pi, u64 n, u32* bits) {
 // Lookups, root walk and stores for S edges of one thread (the body of a
 // hook tile).  Returns the mask of edges whose (h, l) pair in (pu, pv)
 // must be appended to the worklist (stored links and deferred walks).
-template <int S, bool SUM, bool BOTH = false>
-__device__ __forceinline__ u32 resolve_edges(const HookArgs& a, const u32* bits,
+template <int S, bool SUM, bool BOTH = false, bool CAS = false>
+__device__ __forceinline__ u32 resolve_edges(const HookArgs& a, u32& links, const u32* bits,
                                              const u32* s_sum, u32 star,
                                              const uint2 (&ed)[S], u32 (&pu)[S],
                                              u32 (&pv)[S]) {
@@ -411,6 +411,25 @@ __device__ __forceinline__ u32 resolve_edges(const HookArgs& a, const u32* bits,
         continue;
       }
       if (p == pu[k]) {               // root: store now
+        if (CAS) {
+          // CAS (k_hook_cas: worklist passes, where stores are rare): a
+          // link made this way is never lost, so it is not recorded and no
+          // further pass has to re-check it
+          const u32 old = atomicCAS(pi + pu[k], pu[k], pv[k]);
+          if (old == pu[k]) {
+            ++links;
+            act &= ~(1u << k);
+            walking &= ~(1u << k);
+          } else if (old == pv[k]) {  // someone linked h to l
+            act &= ~(1u << k);
+            walking &= ~(1u << k);
+          } else {                    // h got a parent: descend from it
+            const u32 l = pv[k];
+            pu[k] = max(old, l);
+            pv[k] = min(old, l);
+          }
+          continue;
+        }
         pi[pu[k]] = pv[k];
         walking &= ~(1u << k);
       } else if (p == pv[k]) {        // already linked
@@ -563,7 +582,8 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
     }
     if (t + gridDim.x < ntiles) load_tile(t + gridDim.x, nq);
     u32 pu[EPT], pv[EPT];
-    const u32 act = resolve_edges<EPT, SUM, BOTH>(a, bits, s_sum, star, ed, pu, pv);
+    u32 links_unused = 0;
+    const u32 act = resolve_edges<EPT, SUM, BOTH>(a, links_unused, bits, s_sum, star, ed, pu, pv);
     if (a.append) {
       u64 pos;
       if (block_reserve(__popc(act), cnt_out, pos, appended)) {
@@ -650,7 +670,7 @@ __device__ __forceinline__ void warp_emit(const HookArgs& a, WarpOut& w, uint2* 
 // lane per round.  Otherwise (k_hook: no shared memory, so L1 keeps its full
 // size for the bitmap's hot words; e.g. RMAT, whose isolated vertices break
 // most words) every edge takes the bitmap / gather path directly.
-template <int EPT, bool SUM>
+template <int EPT, bool SUM, bool CAS = false>
 __device__ __forceinline__ void hook_stream(const HookArgs& a) {
   constexpr int S = kHookSlow;
   const uint2* src;
@@ -677,6 +697,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
   uint2* s_q = reinterpret_cast<uint2*>(s_sum + ((a.s0f_words + 3u) & ~3u)) +
                (size_t)warp * (32 * EPT);
   WarpOut wo;
+  u32 links = 0;  // CAS links made by this thread
 
   // head / tail edges that do not fill a 16-byte pair: warp 0 of block 0
   u64 b2 = b + (b & 1ull);
@@ -687,7 +708,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
     if (lane == 0 && b2 != b) ed[0] = src[b];
     if (lane == 1 && ((e - b2) & 1ull)) ed[0] = src[e - 1];
     u32 h[1], l[1];
-    const u32 act = resolve_edges<1, false>(a, bits, s_sum, star, ed, h, l);
+    const u32 act = resolve_edges<1, false, false, CAS>(a, links, bits, s_sum, star, ed, h, l);
     warp_emit<1>(a, wo, wl_out, cnt_out, lane, act, h, l);
   }
 
@@ -715,7 +736,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
     if (t + gridDim.x < ntiles) load_tile(t + gridDim.x, nq);
     if (!SUM) {
       u32 h[EPT], l[EPT];
-      const u32 act = resolve_edges<EPT, false>(a, bits, s_sum, star, ed, h, l);
+      const u32 act = resolve_edges<EPT, false, false, CAS>(a, links, bits, s_sum, star, ed, h, l);
       warp_emit<EPT>(a, wo, wl_out, cnt_out, lane, act, h, l);
       continue;
     }
@@ -750,16 +771,21 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
         q2[j] = idx < total ? s_q[idx] : make_uint2(0u, 0u);
       }
       u32 h[S], l[S];
-      const u32 act = resolve_edges<S, true>(a, bits, s_sum, star, q2, h, l);
+      const u32 act = resolve_edges<S, true, false, CAS>(a, links, bits, s_sum, star, q2, h, l);
       warp_emit<S>(a, wo, wl_out, cnt_out, lane, act, h, l);
     }
     __syncwarp();
   }
-  // pad this warp's chunk tail; publish the real appends
+  // pad this warp's chunk tail; publish the real appends (CAS links count
+  // as stores for the plan and need a compress too)
   for (u64 i = wo.pos + lane; i < wo.end; i += 32) wl_out[i] = make_uint2(0u, 0u);
+  if (CAS) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) links += __shfl_xor_sync(0xffffffffu, links, o);
+  }
   if (lane == 0) {
-    if (wo.appended) {
-      atomicAdd(&r->edges_out, (u64)wo.appended);
+    if (wo.appended || links) {
+      atomicAdd(&r->edges_out, (u64)wo.appended + links);
       ctrl->dirty = 1;
     }
     if (wo.changed) {
@@ -784,6 +810,18 @@ __global__ void __launch_bounds__(kHookCta, HCC_HOOK_MINB) k_hook(HookArgs a) {
 // looped-segment path, re-hook, max_threads launches).
 __global__ void __launch_bounds__(kHookCta, HCC_HOOK_MINB) k_hook_legacy(HookArgs a) {
   hook_impl<kHookEPT, false>(a);
+}
+
+// CAS-storing variants (separate kernels: the runtime branch in k_hook cost
+// it spills).
+__global__ void __launch_bounds__(kHookCta, HCC_HOOK_MINB) k_hook_cas(HookArgs a) {
+  if (a.gate == kGateIfPlain && __ldg(&a.ctrl->use_sum)) return;
+  hook_stream<kHookEPT, false, true>(a);
+}
+
+__global__ void __launch_bounds__(kHookSumCta, 1) k_hook_sum_cas(HookArgs a) {
+  if (a.gate == kGateIfSum && !__ldg(&a.ctrl->use_sum)) return;
+  hook_stream<kHookEPT, true, true>(a);
 }
 
 // Streaming hook with the star-0 summary in shared memory (full warps,
