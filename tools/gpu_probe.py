@@ -110,18 +110,24 @@ def main():
         envs = args.envs.split(";") if args.envs else [None]
         for spec in args.specs.split(";"):
             for w in walks:
-              for ev in envs:
-                if w is not None:
-                    os.environ["HCC_WALK"] = w
-                    emit(kind="walk", walk=int(w))
-                if ev is not None:
-                    for kv in ev.split(","):
-                        k, v = kv.split("=", 1)
-                        os.environ[k] = v
-                    emit(kind="env", env=ev)
-                timing(ctx, spec, reps=args.reps,
-                       variants=[("baseline-mj", dict(first_pass_segments=s)) for s in segs],
-                       check=not args.no_check)
+                for ev in envs:
+                    # each sweep point sets its variables and restores them after
+                    saved = dict(os.environ)
+                    try:
+                        if w is not None:
+                            os.environ["HCC_WALK"] = w
+                            emit(kind="walk", walk=int(w))
+                        if ev is not None:
+                            for kv in ev.split(","):
+                                k, v = kv.split("=", 1)
+                                os.environ[k] = v
+                            emit(kind="env", env=ev)
+                        timing(ctx, spec, reps=args.reps,
+                               variants=[("baseline-mj", dict(first_pass_segments=s)) for s in segs],
+                               check=not args.no_check)
+                    finally:
+                        os.environ.clear()
+                        os.environ.update(saved)
         return
     timing(ctx, "rmatx:scale=20,ef=16,seed=1")
     timing(ctx, "rmatx:scale=24,ef=16,seed=1")
