@@ -8,20 +8,31 @@
 //   is_star      proj/include/hookcc/forest.hpp:140-146
 //   loops        proj/include/hookcc/engines.hpp:123-291
 //
-// B200 design (DESIGN.md §4):
-//   * k_hook is the atomic-free Hook.  It streams packed u32 edge pairs with
-//     16-byte streaming loads (two edges per uint4, 8 edges per thread per
-//     tile), gathers pi(u), pi(v) for all 8 edges before any store (16 loads
-//     in flight per thread), stores pi[max] = min with a plain st.global,
-//     and appends the (H, L) pair of every store to the next worklist with a
-//     block-aggregated reservation (one global atomic per 2048-edge tile).
-//     The same kernel serves the topology pass (mode range/segment) and the
-//     data-driven passes (mode worklist); the worklist length lives on the
-//     device, so passes chain without host round trips.
-//   * k_compress is Multi-Jump with eager writes, ascending vertex order and
-//     warp-level early exit (a warp whose lanes all see star parents leaves
-//     after one coalesced read + one hot gather).
-//   * Step kernels advance device-side loop state and set the CUDA-graph
+// B200 design (DESIGN.md §3):
+//   * The hook is the atomic-free Hook (Fig. 2) with Fig. 3's root walk and
+//     a plain load in place of the CAS.  Edges stream as packed u32 pairs in
+//     16-byte loads (8 per thread per tile, the next tile prefetched); the
+//     star bitmap answers pi(x) == star for most endpoints; the walks of a
+//     thread advance in lockstep; a stored link is recorded in the worklist
+//     (resolve_edges).
+//       k_hook        persistent, one 1024-thread CTA per SM, per-warp
+//                     chunked appends (no block barriers), full L1
+//       k_hook_sum    + the star summary in shared memory (device vote)
+//       k_hook_cas /  root stores by atomicCAS: worklist passes, where a
+//       k_hook_sum_cas  record would only be re-checked
+//       k_hook_small  forming slots: full grid, 2 edges per thread, two-sided
+//                     walks
+//       k_hook_legacy block-aggregated appends (non-chunked launches)
+//     The same kernels serve the topology slots and the worklist passes; the
+//     worklist length lives on the device, so passes chain without host
+//     round trips.
+//   * k_compress_s0b is Multi-Jump with eager writes in ascending vertex
+//     order (8 vertices per thread, chases in lockstep, in-group parents
+//     resolved from their roots, chase loads through L1), and builds the
+//     star bitmap and summary for the next hook.  k_compress is the ordered
+//     variant without them (one-thread reference schedule, other engines).
+//   * k_star_pick, k_step_* advance device-side plan state (next range,
+//     tracked star, bitmap use, summary vote) and set the CUDA-graph
 //     conditional-node value.
 #include <cuda_runtime.h>
 
