@@ -48,7 +48,10 @@ constexpr int kHookSlow = 4;
 // HookArgs.gate: k_hook_sum and k_hook are launched back to back for a
 // voted slot and the one not chosen (DevCtrl.use_sum) exits at entry.
 constexpr int kGateAlways = 0, kGateIfSum = 1, kGateIfPlain = 2;     // queued edges per lane per slow-path round
-constexpr u32 kWlChunk = 256;    // worklist records a warp reserves at once
+#ifndef HCC_WL_CHUNK
+#define HCC_WL_CHUNK 256
+#endif
+constexpr u32 kWlChunk = HCC_WL_CHUNK;  // worklist records a warp reserves at once
 #ifndef HCC_HOOK_EPT
 #define HCC_HOOK_EPT 8
 #endif
