@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define HCC_ABI_VERSION 2
+#define HCC_ABI_VERSION 3
 
 typedef enum hcc_status {
   HCC_OK = 0,
@@ -150,7 +150,16 @@ typedef struct hcc_segment_rec {
      first sampled block start / last block end of the hook and compress
      launches of this record; -1 if the phase did not run. */
   double hook_start_ms, hook_end_ms, compress_start_ms, compress_end_ms;
+  /* Hook kernel that ran this record's pass: HCC_HOOK_KERNEL_* (0 unknown). */
+  int32_t hook_kernel;
+  int32_t reserved_;
 } hcc_segment_rec;
+
+#define HCC_HOOK_KERNEL_SMALL  1  /* k_hook_small: forming slot, full grid   */
+#define HCC_HOOK_KERNEL_STREAM 2  /* k_hook: persistent streaming hook        */
+#define HCC_HOOK_KERNEL_SUM    3  /* k_hook_sum: + shared-memory star summary */
+#define HCC_HOOK_KERNEL_CAS    4  /* k_hook_cas / k_hook_sum_cas (worklist)   */
+#define HCC_HOOK_KERNEL_LEGACY 5  /* k_hook_legacy / k_cas_hook                */
 
 /* Reference GraphStats (graph.hpp:33-40), computed on the device. */
 typedef struct hcc_graph_stats {

@@ -21,7 +21,9 @@ ALGOS = {"baseline": ALGO_BASELINE, "baseline-mj": ALGO_BASELINE_MJ,
          "atomic": ALGO_ATOMIC, "adaptive": ALGO_ADAPTIVE}
 FLAG_FULL_PASSES, FLAG_HOST_LOOP, FLAG_NO_GRAPH, FLAG_CHECK_STAR = 0x1, 0x2, 0x4, 0x8
 FLAG_HOOK_EVENTS = 0x10
-ABI_VERSION = 2  # HCC_ABI_VERSION of include/hookcc_c.h
+ABI_VERSION = 3  # HCC_ABI_VERSION of include/hookcc_c.h
+HOOK_KERNELS = {1: "k_hook_small", 2: "k_hook", 3: "k_hook_sum", 4: "k_hook_cas",
+                5: "k_hook_legacy"}
 PHASE_HOOK, PHASE_COMPRESS = 0, 1
 
 u64, u32, i32 = C.c_uint64, C.c_uint32, C.c_int
@@ -52,7 +54,8 @@ class SegmentRec(C.Structure):
     _fields_ = [("hook_ms", C.c_double), ("compress_ms", C.c_double), ("counters", Counters),
                 ("edges_in", u64), ("edges_out", u64), ("hook_event_ms", C.c_double),
                 ("hook_start_ms", C.c_double), ("hook_end_ms", C.c_double),
-                ("compress_start_ms", C.c_double), ("compress_end_ms", C.c_double)]
+                ("compress_start_ms", C.c_double), ("compress_end_ms", C.c_double),
+                ("hook_kernel", C.c_int32), ("reserved_", C.c_int32)]
 
 
 class GraphStats(C.Structure):
@@ -192,7 +195,8 @@ class Context:
                             hook_event_ms=r.hook_event_ms,
                             hook_start_ms=r.hook_start_ms, hook_end_ms=r.hook_end_ms,
                             compress_start_ms=r.compress_start_ms,
-                            compress_end_ms=r.compress_end_ms))
+                            compress_end_ms=r.compress_end_ms,
+                            hook_kernel=HOOK_KERNELS.get(r.hook_kernel, "unknown")))
         return out
 
     # -- graphs --

@@ -161,6 +161,10 @@ struct hcc_ctx {
   std::vector<cudaEvent_t> seg_ev;   // 2 per segment
   u64 seg_ev_used = 0;
   u64 exec_seg_ev = 0;  // seg_ev_used of the cached executable graph
+  // hook kernel per unrolled slot (HCC_HOOK_KERNEL_*; SUM means "voted:
+  // summary or streaming") and of the worklist passes, as enqueued
+  std::vector<int> slot_kernel, exec_slot_kernel;
+  int wl_kernel = 0, exec_wl_kernel = 0;
   u32* s0b = nullptr;  // star-0 bitmap
   u64 s0b_words = 0;
   u32* s0f = nullptr;  // star-0 summary (one bit per group of bitmap words)
@@ -460,6 +464,8 @@ bool sum_slot(const Plan& P, u64 sgi) {
 // Enqueue one full CC run (pi init through convergence) on seq.
 void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
   c->seg_ev_used = 0;
+  c->slot_kernel.clear();
+  c->wl_kernel = HCC_HOOK_KERNEL_LEGACY;
   // grid-stride init with 8 CTAs per SM: the 16 K-block vertex grid took
   // 21 us from run start to the first hook, this one 11 us (RMAT-24)
   const unsigned start_grid =
@@ -515,6 +521,10 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           ha.e = P.bounds[sgi + 1];
           if (P.s0b && sgi >= 1) use_s0b(c, P, ha);
           if (P.hook_events) q.record(c->seg_ev[2 * sgi]);
+          c->slot_kernel.push_back(slot_small(P, sgi) ? HCC_HOOK_KERNEL_SMALL
+                                   : sum_slot(P, sgi)   ? HCC_HOOK_KERNEL_SUM
+                                   : P.chunked          ? HCC_HOOK_KERNEL_STREAM
+                                                        : HCC_HOOK_KERNEL_LEGACY);
           if (slot_small(P, sgi)) {
             // forming-regime segment: EPT 2 over a full grid
             ha.s0f = nullptr;
@@ -592,6 +602,8 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
         if (P.s0b && !P.bounds.empty()) use_s0b(c, P, wa);
         wa.chunked = P.chunked ? 1 : 0;
         wa.cas = P.cas_mode >= 1 && P.chunked ? 1 : 0;
+        c->wl_kernel = wa.cas ? HCC_HOOK_KERNEL_CAS
+                              : (P.chunked ? HCC_HOOK_KERNEL_STREAM : HCC_HOOK_KERNEL_LEGACY);
         if (wa.s0f && P.adapt) {
           HookArgs wp = wa;
           wa.gate = kGateIfSum;
@@ -1533,8 +1545,12 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
       }
       c->key = key;
       c->exec_seg_ev = c->seg_ev_used;
+      c->exec_slot_kernel = c->slot_kernel;
+      c->exec_wl_kernel = c->wl_kernel;
     }
     c->seg_ev_used = c->exec_seg_ev;
+    c->slot_kernel = c->exec_slot_kernel;
+    c->wl_kernel = c->exec_wl_kernel;
     HCC_CUDA(cudaEventRecord(c->ev0, c->stream));
     HCC_CUDA(cudaGraphLaunch(c->exec, c->stream));
     HCC_CUDA(cudaEventRecord(c->ev1, c->stream));
@@ -1591,6 +1607,15 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
     sr.hook_end_ms = hk ? rel(r.hook_t1) : -1.0;
     sr.compress_start_ms = cp ? rel(r.comp_t0) : -1.0;
     sr.compress_end_ms = cp ? rel(r.comp_t1) : -1.0;
+    if (P.adapt || !P.bounds.empty()) {
+      if (i < c->slot_kernel.size()) {
+        sr.hook_kernel = c->slot_kernel[i];
+        if (sr.hook_kernel == HCC_HOOK_KERNEL_SUM && !hc.use_sum)
+          sr.hook_kernel = HCC_HOOK_KERNEL_STREAM;  // the vote chose the plain hook
+      } else if (o->algo == HCC_ALGO_BASELINE_MJ && !P.full_passes) {
+        sr.hook_kernel = c->wl_kernel;
+      }
+    }
     sr.hook_event_ms = -1.0;
     if (i < c->seg_ev_used) {
       float ems = 0.f;
