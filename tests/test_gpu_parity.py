@@ -548,6 +548,11 @@ def test_hook_events_flag_and_timeline(ctx, oracle, capi):
                 assert s["hook_end_ms"] <= s["compress_start_ms"] <= s["compress_end_ms"]
                 prev = s["compress_end_ms"]
         assert prev <= mx["total_ms"] + 0.05
+        # each record names the hook kernel that ran its pass
+        kinds = [s["hook_kernel"] for s in segs]
+        assert kinds[0] in ("k_hook_small", "k_hook")
+        assert all(k in ("k_hook_small", "k_hook", "k_hook_sum") for k in kinds[1:mx["s"]])
+        assert all(k == "k_hook_cas" for k in kinds[mx["s"]:])
     g.close()
 
 
