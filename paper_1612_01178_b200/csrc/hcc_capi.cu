@@ -432,6 +432,14 @@ bool slot_small(const Plan& P, u64 sgi) {
          seg_edges < (u64)P.grid_hook * P.block_hook * kHookEPT * 2;
 }
 
+// Star-bitmap compress over the full grid (a persistent grid with cp.async
+// prefetch was slower: DESIGN.md §3.2).
+void launch_compress_s0b(hcc_ctx* c, const Plan& P, cudaStream_t s) {
+  k_compress_s0b<<<grid_for((P.n + 7) / 8, kVertThreads, 0x7fffffffull), kVertThreads, 0, s>>>(
+      P.pi, P.n, c->d_ctrl, c->d_recs, c->s0b, kCompressIfDirty, P.sum ? c->s0f : nullptr,
+      P.sum_words, P.sum_shift);
+}
+
 // Streaming hook (chunked appends, full warps) or the block-aggregated one.
 void launch_hook(const Plan& P, cudaStream_t s, const HookArgs& a) {
   if (a.chunked && (P.block_hook & 31u) == 0) {
@@ -558,11 +566,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
             k_star_pick<<<1, 32, 0, q.s()>>>(P.pi, P.n, ctrl);
           // compress (+ star-0 bitmap, initialised by k_start)
           if (P.s0b)
-            k_compress_s0b<<<grid_for((P.n + 7) / 8, kVertThreads, 0x7fffffffull),
-                             kVertThreads, 0, q.s()>>>(P.pi, P.n, ctrl, recs, c->s0b,
-                                                       kCompressIfDirty,
-                                                       P.sum ? c->s0f : nullptr,
-                                                       P.sum_words, P.sum_shift);
+            launch_compress_s0b(c, P, q.s());
           else
             k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
                                                                 recs, 1);
@@ -617,11 +621,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
         }
         q.phase_done(HCC_PHASE_HOOK);
         if (P.s0b && !P.bounds.empty())
-          k_compress_s0b<<<grid_for((P.n + 7) / 8, kVertThreads, 0x7fffffffull),
-                           kVertThreads, 0, q.s()>>>(P.pi, P.n, ctrl, recs, c->s0b,
-                                                     kCompressIfDirty,
-                                                     P.sum ? c->s0f : nullptr,
-                                                     P.sum_words, P.sum_shift);
+          launch_compress_s0b(c, P, q.s());
         else
           k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl,
                                                               recs, 1);

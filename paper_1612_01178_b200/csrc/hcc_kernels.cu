@@ -1003,34 +1003,13 @@ __global__ void k_star_pick(const u32* pi, u64 n, DevCtrl* ctrl) {
   }
 }
 
-// Multi-Jump compress fused with the star-0 bitmap build (HC engine, full
-// grid): thread q owns vertices [4q, 4q+4); after the chases every thread
-// knows its vertices' roots, so bit v = (root(v) == 0) is assembled with
-// three warp shuffles (8 lanes = one 32-vertex word) and stored once.
-#ifndef HCC_COMP_MINB
-#define HCC_COMP_MINB 6
-#endif
-__global__ void __launch_bounds__(kVertThreads, HCC_COMP_MINB)
-    k_compress_s0b(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs, u32* bits,
-                   int mode, u32* sum, u32 sum_words, u32 sum_shift) {
-  if (mode && __ldg(&ctrl->dirty) == 0) return;
-  DevRec* r = cur_rec(ctrl, recs);
-  block_t0(&r->comp_t0);
-  u64 steps = 0;
-  // Thread q owns vertices [8q, 8q+8): two 16-byte reads and eight parent
-  // gathers in flight before any chase (ascending order is kept: a thread's
-  // vertices are consecutive and blocks start in ascending order).
-  // The bitmap tracks the star rooted at ctrl->star: k_star_pick resolved
-  // it after the last hook (vertex 0, the initial star, is never hooked).
-  // Should it have been hooked since (a slot without a pick), no root
-  // equals it and this bitmap is simply empty.
-  const u32 star = __ldg(&ctrl->star);
-  const u64 q = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  const u64 v0 = q << 3;
-  u32 byte = 0;  // bit j = (root(v0 + j) == star)
-  if (v0 + 8 <= n) {
-    const uint4* p4 = reinterpret_cast<const uint4*>(pi) + (q << 1);
-    const uint4 pa = __ldcg(p4), pb = __ldcg(p4 + 1);
+// Multi-Jump compress of vertices [v0, v0 + 8) (one thread; pa, pb hold
+// pi of the group when it is whole).  Returns bit j = (root(v0 + j) ==
+// star) and counts written levels in `steps`.
+__device__ __forceinline__ u32 compress8(u32* pi, u64 n, u64 v0, bool whole, uint4 pa,
+                                         uint4 pb, u32 star, u64& steps) {
+  u32 byte = 0;
+  if (whole) {
     u32 a[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
     // pi(v) <= v, so a parent inside this group is an earlier vertex of it:
     // those vertices take their parent's root after the chases (ascending,
@@ -1096,55 +1075,95 @@ __global__ void __launch_bounds__(kVertThreads, HCC_COMP_MINB)
       byte |= (a == star) ? 1u << (u32)(v - v0) : 0u;
     }
   }
+  return byte;
+}
+
+// Store the bitmap words and star summary of one 2048-vertex chunk (one
+// block's groups; byte = this thread's 8 bits).  Uniform per block.
+__device__ __forceinline__ void emit_bits(u64 chunk, u64 n, u64 v0, u32 byte, u32* bits,
+                                          u32* sum, u32 sum_words, u32 sum_shift,
+                                          u32* s_full) {
   // four lanes = one 32-vertex word
   const u32 lane = threadIdx.x & 31u;
   u32 w = byte << (8u * (lane & 3u));
   w |= __shfl_xor_sync(0xffffffffu, w, 1);
   w |= __shfl_xor_sync(0xffffffffu, w, 2);
   if ((lane & 3u) == 0 && v0 < n) bits[v0 >> 5] = w;
-  if (sum) {
-    // Star-0 summary: this block's 64 words -> 64 >> sum_shift bits (bit =
-    // every word of its group is all ones).  Star 0 only grows (pi(v) = 0
-    // is never rewritten), so bits only turn on: groups shared with other
-    // blocks are merged with atomicOr, whole summary words are stored.
-    __shared__ u32 s_full[8];
-    const u32 full = __ballot_sync(0xffffffffu, (lane & 3u) == 0 && v0 < n && w == ~0u);
-    u32 b8 = 0;  // bit j = word (warp * 8 + j) is all ones
+  if (!sum) return;
+  // Star-0 summary: this chunk's 64 words -> 64 >> sum_shift bits (bit =
+  // every word of its group is all ones).  Groups shared with other chunks
+  // are merged with atomics (clear, then set), whole summary words stored.
+  const u32 full = __ballot_sync(0xffffffffu, (lane & 3u) == 0 && v0 < n && w == ~0u);
+  u32 b8 = 0;  // bit j = word (warp * 8 + j) is all ones
 #pragma unroll
-    for (int j = 0; j < 8; ++j) b8 |= ((full >> (4 * j)) & 1u) << j;
-    if (sum_shift == 0) {
-      // one summary bit per word: a warp's 8 words are one summary byte
-      const u64 byte_idx = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-      if (lane == 0 && byte_idx < (u64)sum_words * 4)
-        reinterpret_cast<unsigned char*>(sum)[byte_idx] = (unsigned char)b8;
-    } else {
-    if (lane == 0) s_full[threadIdx.x >> 5] = b8;
-    __syncthreads();
-    if (threadIdx.x == 0 && blockDim.x == kVertThreads) {
-      u64 f = 0;
+  for (int j = 0; j < 8; ++j) b8 |= ((full >> (4 * j)) & 1u) << j;
+  if (sum_shift == 0) {
+    // one summary bit per word: a warp's 8 words are one summary byte
+    const u64 byte_idx = (chunk * blockDim.x + threadIdx.x) >> 5;
+    if (lane == 0 && byte_idx < (u64)sum_words * 4)
+      reinterpret_cast<unsigned char*>(sum)[byte_idx] = (unsigned char)b8;
+    return;
+  }
+  if (lane == 0) s_full[threadIdx.x >> 5] = b8;
+  __syncthreads();
+  if (threadIdx.x == 0 && blockDim.x == kVertThreads) {
+    u64 f = 0;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) f |= (u64)s_full[i] << (8 * i);
-      const u32 g = 1u << sum_shift, nb = 64u >> sum_shift;
-      u64 bitsg = 0;
-      for (u32 i = 0; i < nb; ++i) {
-        const u64 mask = (g == 64 ? ~0ull : ((1ull << g) - 1)) << (i * g);
-        if ((f & mask) == mask) bitsg |= 1ull << i;
-      }
-      const u64 pos = (u64)blockIdx.x * nb;  // first summary bit of this block
-      if (nb >= 32) {
-        for (u32 k = 0; k < nb / 32; ++k)
-          if ((pos >> 5) + k < sum_words) sum[(pos >> 5) + k] = (u32)(bitsg >> (32 * k));
-      } else if ((pos >> 5) < sum_words) {
-        // this block owns nb bits of a shared word: clear, then set (the
-        // star may have moved since the last compress)
-        const u32 mask = (u32)((1ull << nb) - 1) << (pos & 31);
-        const u32 val = (u32)bitsg << (pos & 31);
-        if (~val & mask) atomicAnd(sum + (pos >> 5), ~(mask & ~val));
-        if (val) atomicOr(sum + (pos >> 5), val);
-      }
+    for (int i = 0; i < 8; ++i) f |= (u64)s_full[i] << (8 * i);
+    const u32 g = 1u << sum_shift, nb = 64u >> sum_shift;
+    u64 bitsg = 0;
+    for (u32 i = 0; i < nb; ++i) {
+      const u64 mask = (g == 64 ? ~0ull : ((1ull << g) - 1)) << (i * g);
+      if ((f & mask) == mask) bitsg |= 1ull << i;
     }
+    const u64 pos = chunk * nb;  // first summary bit of this chunk
+    if (nb >= 32) {
+      for (u32 k = 0; k < nb / 32; ++k)
+        if ((pos >> 5) + k < sum_words) sum[(pos >> 5) + k] = (u32)(bitsg >> (32 * k));
+    } else if ((pos >> 5) < sum_words) {
+      // this chunk owns nb bits of a shared word: clear, then set (the
+      // star may have moved since the last compress)
+      const u32 mask = (u32)((1ull << nb) - 1) << (pos & 31);
+      const u32 val = (u32)bitsg << (pos & 31);
+      if (~val & mask) atomicAnd(sum + (pos >> 5), ~(mask & ~val));
+      if (val) atomicOr(sum + (pos >> 5), val);
     }
   }
+}
+
+// Multi-Jump compress fused with the star-0 bitmap build (HC engine, full
+// grid): thread q owns vertices [8q, 8q+8); after the chases every thread
+// knows its vertices' roots, so bit v = (root(v) == star) is assembled with
+// two warp shuffles (4 lanes = one 32-vertex word) and stored once.
+#ifndef HCC_COMP_MINB
+#define HCC_COMP_MINB 6
+#endif
+__global__ void __launch_bounds__(kVertThreads, HCC_COMP_MINB)
+    k_compress_s0b(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs, u32* bits,
+                   int mode, u32* sum, u32 sum_words, u32 sum_shift) {
+  if (mode && __ldg(&ctrl->dirty) == 0) return;
+  DevRec* r = cur_rec(ctrl, recs);
+  block_t0(&r->comp_t0);
+  u64 steps = 0;
+  // Two 16-byte reads and eight parent gathers in flight before any chase
+  // (ascending order is kept: a thread's vertices are consecutive and
+  // blocks start in ascending order).  The bitmap tracks the star rooted
+  // at ctrl->star: k_star_pick resolved it after the last hook (vertex 0,
+  // the initial star, is never hooked).  Should it have been hooked since
+  // (a slot without a pick), no root equals it and this bitmap is empty.
+  const u32 star = __ldg(&ctrl->star);
+  const u64 q = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 v0 = q << 3;
+  const bool whole = v0 + 8 <= n;
+  uint4 pa = make_uint4(0u, 0u, 0u, 0u), pb = pa;
+  if (whole) {
+    const uint4* p4 = reinterpret_cast<const uint4*>(pi) + (q << 1);
+    pa = __ldcg(p4);
+    pb = __ldcg(p4 + 1);
+  }
+  const u32 byte = compress8(pi, n, v0, whole, pa, pb, star, steps);
+  __shared__ u32 s_full[8];
+  emit_bits(blockIdx.x, n, v0, byte, bits, sum, sum_words, sum_shift, s_full);
   add_counter(&r->jump_steps, steps);
   block_t1(&r->comp_t1);
 }
