@@ -1594,7 +1594,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
       sr.compress_ms = (double)(r.comp_t1 - r.comp_t0) * 1e-6;
     sr.counters.hook_traversal_steps = r.traversal;
     sr.counters.cas_failures = r.cas_fail;
-    sr.counters.jump_steps = r.jump_steps;
+    sr.counters.jump_steps = r.jump_total();
     sr.edges_in = r.edges_in;
     sr.edges_out = r.edges_out;
     auto rel = [&](u64 t) {
@@ -1630,7 +1630,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
     out.compress_ms += sr.compress_ms;
     out.counters.hook_traversal_steps += r.traversal;
     out.counters.cas_failures += r.cas_fail;
-    out.counters.jump_steps += r.jump_steps;
+    out.counters.jump_steps += r.jump_total();
   }
   out.star0_bitmap = P.s0b ? 1 : 0;
   {

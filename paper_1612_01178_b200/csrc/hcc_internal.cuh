@@ -61,10 +61,23 @@ constexpr int kVertThreads = 256;
 // One record per hook+compress phase pair (segment, outer iteration or
 // worklist pass).  Times are %globaltimer nanoseconds (first block start,
 // last block end).
+// Compress jump counters are striped over kJumpStripes words (by block):
+// tens of thousands of per-warp atomics on one address serialise in its L2
+// slice.  The host sums the stripes.
+#ifndef HCC_JUMP_STRIPES
+#define HCC_JUMP_STRIPES 16
+#endif
+constexpr int kJumpStripes = HCC_JUMP_STRIPES;
 struct DevRec {
   u64 hook_t0, hook_t1, comp_t0, comp_t1;
   u64 traversal, cas_fail, jump_steps;
   u64 edges_in, edges_out;
+  u64 jump_stripe[kJumpStripes];
+  u64 jump_total() const {
+    u64 t = jump_steps;
+    for (int i = 0; i < kJumpStripes; ++i) t += jump_stripe[i];
+    return t;
+  }
 };
 
 struct DevCtrl {

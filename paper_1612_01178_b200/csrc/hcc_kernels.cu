@@ -133,6 +133,7 @@ __device__ __forceinline__ void rec_clear(DevRec& r) {
   r.comp_t1 = 0;
   r.traversal = r.cas_fail = r.jump_steps = 0;
   r.edges_in = r.edges_out = 0;
+  for (int i = 0; i < kJumpStripes; ++i) r.jump_stripe[i] = 0;
 }
 
 __device__ __forceinline__ DevRec* cur_rec(DevCtrl* c, DevRec* recs) {
@@ -942,7 +943,7 @@ __global__ void __launch_bounds__(kVertThreads)
       b = ld_chase(pi + a);
     }
   }
-  add_counter(&r->jump_steps, steps);
+  add_counter(&r->jump_stripe[blockIdx.x & (kJumpStripes - 1)], steps);
   block_t1(&r->comp_t1);
 }
 
@@ -1164,7 +1165,7 @@ __global__ void __launch_bounds__(kVertThreads, HCC_COMP_MINB)
   const u32 byte = compress8(pi, n, v0, whole, pa, pb, star, steps);
   __shared__ u32 s_full[8];
   emit_bits(blockIdx.x, n, v0, byte, bits, sum, sum_words, sum_shift, s_full);
-  add_counter(&r->jump_steps, steps);
+  add_counter(&r->jump_stripe[blockIdx.x & (kJumpStripes - 1)], steps);
   block_t1(&r->comp_t1);
 }
 
@@ -1184,7 +1185,7 @@ __global__ void __launch_bounds__(kVertThreads)
     }
   }
   if (__syncthreads_or(steps != 0) && threadIdx.x == 0) ctrl->jchanged = 1;
-  add_counter(&r->jump_steps, steps);
+  add_counter(&r->jump_stripe[blockIdx.x & (kJumpStripes - 1)], steps);
   block_t1(&r->comp_t1);
 }
 
