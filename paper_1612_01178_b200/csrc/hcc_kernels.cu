@@ -160,14 +160,16 @@ __device__ __forceinline__ void block_t0(u64* t0) {
 }
 
 __device__ __forceinline__ void block_t1(u64* t1) {
+  if (!timer_block()) return;  // uniform per block
   __syncthreads();
-  if (threadIdx.x == 0 && timer_block()) atomicMax(t1, gtime());
+  if (threadIdx.x == 0) atomicMax(t1, gtime());
 }
 
 // Adds a per-thread counter into a global u64.  Must be reached by every
 // thread of the block (uniform control flow).
 __device__ __forceinline__ void add_counter(u64* dst, u64 v) {
   if ((blockDim.x & 31u) == 0) {
+    if (!__any_sync(0xffffffffu, v != 0)) return;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if ((threadIdx.x & 31u) == 0 && v) atomicAdd(dst, v);
@@ -1008,10 +1010,22 @@ __global__ void k_star_pick(const u32* pi, u64 n, DevCtrl* ctrl) {
 // pi of the group when it is whole).  Returns bit j = (root(v0 + j) ==
 // star) and counts written levels in `steps`.
 __device__ __forceinline__ u32 compress8(u32* pi, u64 n, u64 v0, bool whole, uint4 pa,
-                                         uint4 pb, u32 star, u64& steps) {
+                                         uint4 pb, u32 star, bool star_root, u64& steps) {
   u32 byte = 0;
   if (whole) {
     u32 a[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+    // Settled group (most groups once the giant is a star): every vertex
+    // is its own root or a child of the star's root, which is still a
+    // root.  No gathers, no writes.
+    if (star_root) {
+      u32 settled = 1, sb = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        settled &= (a[j] == (u32)v0 + j) | (a[j] == star);
+        sb |= (u32)(a[j] == star) << j;
+      }
+      if (settled) return sb;
+    }
     // pi(v) <= v, so a parent inside this group is an earlier vertex of it:
     // those vertices take their parent's root after the chases (ascending,
     // as the reference's sequential pass would; grid rows chain this way).
@@ -1095,9 +1109,11 @@ __device__ __forceinline__ void emit_bits(u64 chunk, u64 n, u64 v0, u32 byte, u3
   // every word of its group is all ones).  Groups shared with other chunks
   // are merged with atomics (clear, then set), whole summary words stored.
   const u32 full = __ballot_sync(0xffffffffu, (lane & 3u) == 0 && v0 < n && w == ~0u);
-  u32 b8 = 0;  // bit j = word (warp * 8 + j) is all ones
-#pragma unroll
-  for (int j = 0; j < 8; ++j) b8 |= ((full >> (4 * j)) & 1u) << j;
+  // bit j = word (warp * 8 + j) is all ones: every 4th bit of `full`
+  u32 b8 = full & 0x11111111u;
+  b8 = (b8 | (b8 >> 3)) & 0x03030303u;
+  b8 = (b8 | (b8 >> 6)) & 0x000f000fu;
+  b8 = (b8 | (b8 >> 12)) & 0xffu;
   if (sum_shift == 0) {
     // one summary bit per word: a warp's 8 words are one summary byte
     const u64 byte_idx = (chunk * blockDim.x + threadIdx.x) >> 5;
@@ -1162,7 +1178,10 @@ __global__ void __launch_bounds__(kVertThreads, HCC_COMP_MINB)
     pa = __ldcg(p4);
     pb = __ldcg(p4 + 1);
   }
-  const u32 byte = compress8(pi, n, v0, whole, pa, pb, star, steps);
+  // the star's root is read once per thread (one L1 line for the grid):
+  // a compress never moves a root, so the answer holds for the whole pass
+  const bool star_root = star < n && ld_pi(pi + star) == star;
+  const u32 byte = compress8(pi, n, v0, whole, pa, pb, star, star_root, steps);
   __shared__ u32 s_full[8];
   emit_bits(blockIdx.x, n, v0, byte, bits, sum, sum_words, sum_shift, s_full);
   add_counter(&r->jump_stripe[blockIdx.x & (kJumpStripes - 1)], steps);
