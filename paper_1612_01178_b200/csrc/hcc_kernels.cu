@@ -1036,7 +1036,9 @@ __device__ __forceinline__ u32 compress8(u32* pi, u64 n, u64 v0, bool whole, uin
     u32 b[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      b[j] = (a[j] != (u32)v0 + j && !(dep & (1u << j))) ? ld_pi(pi + a[j]) : a[j];
+      b[j] = (a[j] != (u32)v0 + j && !(dep & (1u << j)) && !(star_root && a[j] == star))
+                 ? ld_pi(pi + a[j])
+                 : a[j];
     // The remaining chases advance in lockstep (one level per round, up to
     // eight independent loads in flight) instead of one after another: in
     // the forming segments the trees are deep and a serial chase is one
@@ -1254,35 +1256,44 @@ __global__ void k_step_segment(DevCtrl* c, DevRec* recs,
 __global__ void k_step_adapt(DevCtrl* c, DevRec* recs, u64 m, u32 forming_pct,
                              const u32* sum, u32 sum_words, const uint2* edges,
                              const u32* bits) {
-  __shared__ u64 s_b, s_e;
-  if (threadIdx.x == 0) {
-    const DevRec& r = recs[c->rec < (u32)kMaxRecs ? c->rec : (u32)kMaxRecs - 1];
-    const u64 len = c->seg_e - c->seg_b;
-    const bool forming = r.edges_in > 0 && r.edges_out * 100 > r.edges_in * forming_pct;
-    c->seg_b = c->seg_e;
-    u64 next = forming ? len * kAdaptGrowth : m;
-    if (next < 1) next = 1;
-    if (c->seg + 2 >= c->nseg) next = m;  // the next slot is the last one
-    c->seg_e = (m - c->seg_b) <= next ? m : c->seg_b + next;
-    c->seg += 1;
-    c->passes += (len > 0);
-    c->dirty = 0;
-    next_rec(c, recs);
-    s_b = c->seg_b;
-    s_e = c->seg_e;
-  }
-  if (blockDim.x == 1) return;
-  __syncthreads();
+  // Every thread derives the next range from the pass-start control words
+  // (same addresses: broadcast reads), so the sample loads below issue
+  // without waiting for thread 0's bookkeeping; thread 0 writes after the
+  // barrier, once every thread has read.
+  const u32 ri = c->rec < (u32)kMaxRecs ? c->rec : (u32)kMaxRecs - 1;
+  const u64 r_in = recs[ri].edges_in, r_out = recs[ri].edges_out;
+  const u64 seg = c->seg, nseg = c->nseg, old_b = c->seg_b, old_e = c->seg_e;
+  const u64 len = old_e - old_b;
+  const bool forming = r_in > 0 && r_out * 100 > r_in * forming_pct;
+  u64 next = forming ? len * kAdaptGrowth : m;
+  if (next < 1) next = 1;
+  if (seg + 2 >= nseg) next = m;  // the next slot is the last one
+  const u64 s_b = old_e;
+  const u64 s_e = (m - s_b) <= next ? m : s_b + next;
   // Bitmap use for the next hook (one block): a lookup pays only when it
   // usually answers; the share of the next segment's endpoints in the star
   // decides (RMAT: 81-98% with hub words L1-resident; ER's giant at 37%
   // made its bitmap lookups a net loss, 0.63 vs 0.51 ms).
-  if (bits && s_e > s_b) {
-    u64 hsh = (((u64)c->seg << 32) + threadIdx.x + 1) * 0x9E3779B97F4A7C15ull;
+  const bool sample = blockDim.x > 1 && bits && s_e > s_b;
+  uint2 ed = make_uint2(0u, 0u);
+  if (sample) {
+    u64 hsh = (((seg + 1) << 32) + threadIdx.x + 1) * 0x9E3779B97F4A7C15ull;
     hsh ^= hsh >> 29;
     hsh *= 0xBF58476D1CE4E5B9ull;
     hsh ^= hsh >> 32;
-    const uint2 ed = edges[s_b + hsh % (s_e - s_b)];
+    ed = edges[s_b + hsh % (s_e - s_b)];
+  }
+  if (blockDim.x > 1) __syncthreads();
+  if (threadIdx.x == 0) {
+    c->seg_b = s_b;
+    c->seg_e = s_e;
+    c->seg = seg + 1;
+    c->passes += (len > 0);
+    c->dirty = 0;
+    next_rec(c, recs);
+  }
+  if (blockDim.x == 1) return;
+  if (sample) {
     const u32 hits = ((bits[ed.x >> 5] >> (ed.x & 31u)) & 1u) + ((bits[ed.y >> 5] >> (ed.y & 31u)) & 1u);
     const int n_hit = __syncthreads_count(hits == 2) * 2 + __syncthreads_count(hits == 1);
     if (threadIdx.x == 0) c->use_bits = (u32)n_hit * 2 >= 2 * blockDim.x ? 1u : 0u;
