@@ -968,20 +968,24 @@ __global__ void k_star_pick(const u32* pi, u64 n, DevCtrl* ctrl) {
   // as unknown (~0); an unresolved current star (~0) leaves the next
   // bitmap empty unless a candidate wins
   u32 x = (u32)(hsh % n);
+  // the sample's first parents and the control words are independent
+  // loads: issue them together (one round trip, not three)
+  const u32 px = ld_fresh(pi + x);
+  const u32 star0 = __ldcg(&ctrl->star);
+  u32 cur = __ldcg(&ctrl->star_hint);
   // the tracked star already holds a quarter of the sample: keep it (leaf
   // slots are not written by a hook, so pi(x) == star still marks it)
-  const u32 star0 = *(volatile u32*)&ctrl->star;
   if (star0 < n && ld_fresh(pi + star0) == star0 &&
-      __popc(__ballot_sync(0xffffffffu, ld_fresh(pi + x) == star0)) >= 8)
+      __popc(__ballot_sync(0xffffffffu, px == star0)) >= 8)
     return;
-  bool rooted = false;
-  for (int i = 0; i < kStarChase && !rooted; ++i) {
+  bool rooted = px == x;
+  x = px;
+  for (int i = 1; i < kStarChase && !rooted; ++i) {
     const u32 p = ld_fresh(pi + x);
     rooted = p == x;
     x = p;
   }
   if (!rooted) x = ~0u;
-  u32 cur = ctrl->star_hint;
   bool cur_rooted = false;
   for (int i = 0; i < kStarChase && !cur_rooted; ++i) {
     const u32 p = ld_fresh(pi + cur);
