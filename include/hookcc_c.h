@@ -293,6 +293,12 @@ int hcc_forest_export(hcc_ctx* ctx, hcc_forest* f, uint32_t* dev_bits,
 /* dev_bits_or may be NULL; dev_pairs holds `count` (v, parent) u32 pairs. */
 int hcc_rehook(hcc_ctx* ctx, hcc_forest* f, const uint32_t* dev_bits_or,
                const uint32_t* dev_pairs, uint64_t count, hcc_metrics* out);
+/* As hcc_rehook, with the bitmap given as the all-gathered rows of every
+ * rank (row r at dev_bit_rows + r * row_stride_words): the kernel ORs all
+ * rows except skip_row (the caller's own; ~0 for none) while decoding. */
+int hcc_rehook_rows(hcc_ctx* ctx, hcc_forest* f, const uint32_t* dev_bit_rows,
+                    uint64_t nrows, uint64_t row_stride_words, uint64_t skip_row,
+                    const uint32_t* dev_pairs, uint64_t count, hcc_metrics* out);
 /* Device generator of one shard: edges [first, first+count) of `spec`
  * (partition_edges(m, world) gives the rank's range). */
 int hcc_graph_generate_range(hcc_ctx* ctx, const char* spec,

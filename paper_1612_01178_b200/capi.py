@@ -114,6 +114,7 @@ _SIGS = {
     "hcc_forest_verify": (i32, [vp, vp, vp, C.POINTER(u64), C.POINTER(u64)]),
     "hcc_labels_compare": (i32, [vp, vp, vp, u64, C.POINTER(i32), C.POINTER(i32)]),
     "hcc_rehook": (i32, [vp, vp, vp, vp, u64, C.POINTER(Metrics)]),
+    "hcc_rehook_rows": (i32, [vp, vp, vp, u64, u64, u64, vp, u64, C.POINTER(Metrics)]),
     "hcc_graph_generate_range": (i32, [vp, C.c_char_p, u64, u64, u64, C.POINTER(vp)]),
 }
 
@@ -245,6 +246,15 @@ class Context:
                count: int) -> dict:
         mx = Metrics()
         check(lib().hcc_rehook(self.h, forest.h, dev_bits_or, dev_pairs, count, C.byref(mx)))
+        return metrics_dict(mx)
+
+    def rehook_rows(self, forest: "Forest", dev_rows: int | None, nrows: int, stride: int,
+                    skip: int, dev_pairs: int | None, count: int) -> dict:
+        """hcc_rehook_rows: OR of the gathered bitmap rows but `skip` (-1: none)."""
+        mx = Metrics()
+        check(lib().hcc_rehook_rows(self.h, forest.h, dev_rows, nrows, stride,
+                                    skip if skip >= 0 else 2**64 - 1, dev_pairs, count,
+                                    C.byref(mx)))
         return metrics_dict(mx)
 
     def verify(self, graph: "Graph", forest: "Forest") -> tuple[int, int]:

@@ -2042,7 +2042,18 @@ int hcc_forest_export(hcc_ctx* c, hcc_forest* f, uint32_t* dev_bits,
 // (host-driven passes: the merge needs only a few).
 int hcc_rehook(hcc_ctx* c, hcc_forest* f, const uint32_t* dev_bits_or,
                const uint32_t* dev_pairs, uint64_t count, hcc_metrics* mx) {
+  const uint64_t nwords = f ? (f->n + 31) / 32 : 0;
+  return hcc_rehook_rows(c, f, dev_bits_or, dev_bits_or ? 1 : 0, nwords, ~0ull, dev_pairs,
+                         count, mx);
+}
+
+int hcc_rehook_rows(hcc_ctx* c, hcc_forest* f, const uint32_t* dev_bit_rows, uint64_t nrows,
+                    uint64_t row_stride_words, uint64_t skip_row, const uint32_t* dev_pairs,
+                    uint64_t count, hcc_metrics* mx) {
   if (!f) return fail(HCC_EINVAL, "null forest");
+  if (nrows && !dev_bit_rows) return fail(HCC_EINVAL, "null bitmap rows");
+  if (nrows && row_stride_words < (f->n + 31) / 32)
+    return fail(HCC_EINVAL, "bitmap row stride below ceil(n/32)");
   if (count && !dev_pairs) return fail(HCC_EINVAL, "null pair buffer");
   if (int r = ctx_enter(c)) return r;
   hcc_metrics out{};
@@ -2066,7 +2077,10 @@ int hcc_rehook(hcc_ctx* c, hcc_forest* f, const uint32_t* dev_bits_or,
   P.block_hook = kHookCta;
   P.grid_hook = (unsigned)(c->sms * c->occ_hook);
   P.block_vert = kVertThreads;
-  P.grid_vert = grid_for((n + 3) / 4, kVertThreads, 0x7fffffffull);
+  // grid-stride compress over a few CTAs per SM: after a merge the trees
+  // are stars plus a few remote links, and a pass that finds the forest
+  // clean exits at once (a full grid took 0.45 ms to do nothing at n = 2^28)
+  P.grid_vert = grid_for((n + 3) / 4, kVertThreads, (u64)c->sms * 16);
   HCC_CUDA(cudaEventRecord(c->ev0, c->stream));
   k_begin<<<1, 1, 0, c->stream>>>(c->d_ctrl, c->d_recs, 1);
   u64* d_cnt = reinterpret_cast<u64*>(&c->d_ctrl->wl_count[0]);
@@ -2077,9 +2091,10 @@ int hcc_rehook(hcc_ctx* c, hcc_forest* f, const uint32_t* dev_bits_or,
     HCC_CUDA(cudaMemcpyAsync(d_cnt, &c->h_ctrl->wl_count[0], sizeof(u64),
                              cudaMemcpyHostToDevice, c->stream));
   }
-  if (dev_bits_or && n)
+  if (nrows && n)
     k_decode_bits<<<grid_for((n + 31) / 32 * 32, 256, (u64)c->sms * 32), 256, 0,
-                    c->stream>>>(dev_bits_or, f->d_pi, n, c->wl[0], d_cnt);
+                    c->stream>>>(dev_bit_rows, nrows, row_stride_words, skip_row, f->d_pi, n,
+                                 c->wl[0], d_cnt);
   HCC_CUDA(cudaGetLastError());
   Seq q;
   q.c = c;

@@ -230,7 +230,7 @@ __global__ void k_count_distinct(const u64* k, u64 n, int shift, u64* out);
 // Multi-GPU merge (hcc_multi.cu).
 __global__ void k_export(const u32* pi, u64 n, u32* bits, uint2* pairs, u64 cap,
                          u64* count);
-__global__ void k_decode_bits(const u32* bits_or, const u32* pi, u64 n,
-                              uint2* wl, u64* count);
+__global__ void k_decode_bits(const u32* rows, u64 nrows, u64 stride, u64 skip, const u32* pi,
+                              u64 n, uint2* wl, u64* count);
 
 }  // namespace hcc

@@ -37,34 +37,60 @@ __device__ __forceinline__ void warp_append(bool want, uint2 pr, uint2* out, u64
 
 }  // namespace
 
-// One warp per 32-vertex word.  Requires blockDim.x % 32 == 0.
+// One warp per 32-vertex word, four words per round (four 128-byte reads in
+// flight per warp).  Requires blockDim.x % 32 == 0.
 __global__ void k_export(const u32* pi, u64 n, u32* bits, uint2* pairs, u64 cap,
                          u64* count) {
+  constexpr u32 kW = 4;
   const u32 lane = threadIdx.x & 31u;
   const u64 nwords = (n + 31) >> 5;
   const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
-  for (u64 w = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwords; w += warps) {
-    const u64 v = (w << 5) + lane;
-    const u32 p = v < n ? __ldcg(pi + v) : (u32)v;
-    const u32 b = __ballot_sync(0xffffffffu, v < n && v != 0 && p == 0u);
-    if (lane == 0) bits[w] = b;
-    warp_append(v < n && p != (u32)v && p != 0u, make_uint2((u32)v, p), pairs, cap, count);
+  for (u64 w0 = (((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kW; w0 < nwords;
+       w0 += warps * kW) {
+    u32 p[kW];
+#pragma unroll
+    for (u32 k = 0; k < kW; ++k) {
+      const u64 v = ((w0 + k) << 5) + lane;
+      p[k] = v < n ? __ldcg(pi + v) : (u32)v;
+    }
+#pragma unroll
+    for (u32 k = 0; k < kW; ++k) {
+      if (w0 + k >= nwords) break;  // warp-uniform
+      const u64 v = ((w0 + k) << 5) + lane;
+      const u32 b = __ballot_sync(0xffffffffu, v < n && v != 0 && p[k] == 0u);
+      if (lane == 0) bits[w0 + k] = b;
+      warp_append(v < n && p[k] != (u32)v && p[k] != 0u, make_uint2((u32)v, p[k]), pairs, cap,
+                  count);
+    }
   }
 }
 
 // Append (v, 0) for every v set in the OR of the remote bitmaps that is not
 // already in the local star of 0.
-__global__ void k_decode_bits(const u32* bits_or, const u32* pi, u64 n, uint2* wl,
-                              u64* count) {
+__global__ void k_decode_bits(const u32* rows, u64 nrows, u64 stride, u64 skip, const u32* pi,
+                              u64 n, uint2* wl, u64* count) {
+  // bit v of the OR over the gathered rows (every rank's bitmap but this
+  // one's: `skip`), decoded to (v, 0) worklist edges where v is not yet in 0
+  constexpr u32 kW = 4;
   const u32 lane = threadIdx.x & 31u;
   const u64 nwords = (n + 31) >> 5;
   const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
-  for (u64 w = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwords; w += warps) {
-    const u32 b = bits_or[w];
-    if (b == 0u) continue;  // warp-uniform
-    const u64 v = (w << 5) + lane;
-    const bool want = ((b >> lane) & 1u) && v < n && __ldcg(pi + v) != 0u;
-    warp_append(want, make_uint2((u32)v, 0u), wl, ~0ull, count);
+  for (u64 w0 = (((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kW; w0 < nwords;
+       w0 += warps * kW) {
+    u32 b[kW] = {0u, 0u, 0u, 0u};
+    for (u64 r = 0; r < nrows; ++r) {
+      if (r == skip) continue;
+#pragma unroll
+      for (u32 k = 0; k < kW; ++k)
+        if (w0 + k < nwords) b[k] |= rows[r * stride + w0 + k];
+    }
+#pragma unroll
+    for (u32 k = 0; k < kW; ++k) {
+      if (b[k] == 0u) continue;  // warp-uniform
+      const u64 v = ((w0 + k) << 5) + lane;
+      const bool want = ((b[k] >> lane) & 1u) && v < n && __ldcg(pi + v) != 0u;
+      warp_append(want, make_uint2((u32)v, 0u), wl, ~0ull, count);
+    }
   }
 }
 

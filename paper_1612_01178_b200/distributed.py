@@ -48,12 +48,36 @@ class MergeTimes:
     extra: dict = field(default_factory=dict)
 
 
-def exchange(bits, pairs, group=None):
-    """All-gather the payloads.
+_BUFS: dict = {}
 
-    bits  : int32 tensor [nwords] (bit patterns), this rank's bitmap
-    pairs : int32 tensor [k, 2], this rank's (v, parent) pairs
-    returns (bits_or over the OTHER ranks, remote pairs [K, 2]).
+
+def _buf(key, numel, dtype, device):
+    """Reusable receive buffers (per shape): the exchange runs every step."""
+    import torch
+    t = _BUFS.get(key)
+    if t is None or t.numel() < numel or t.dtype != dtype or t.device != device:
+        t = torch.empty(numel, dtype=dtype, device=device)
+        _BUFS[key] = t
+    return t[:numel]
+
+
+def send_offset(nwords: int) -> int:
+    """Index of the pair count in the send buffer (8-byte aligned)."""
+    return nwords + (nwords & 1)
+
+
+def exchange(bits, pairs, group=None, sendbuf=None, pairs_buf=None):
+    """All-gather the payloads: two collectives and one host read.
+
+    bits      : int32 tensor [nwords] (bit patterns), this rank's bitmap
+    pairs     : int32 tensor [k, 2], this rank's (v, parent) pairs
+    sendbuf   : optional int32 [send_offset(nwords) + 2] whose prefix is
+                `bits`: the pair count rides in its last two words (no extra
+                collective)
+    pairs_buf : optional [cap, 2] tensor whose prefix is `pairs`: sent as is
+                (rows past k are ignored by the receivers), no padding copy
+    returns (rows, rank, remote): the gathered bitmaps as [world, nwords]
+    (the receiver ORs every row but its own), and the remote pairs [K, 2].
     """
     import torch
     import torch.distributed as dist
@@ -61,29 +85,43 @@ def exchange(bits, pairs, group=None):
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     dev = bits.device
-    # flat output buffers: the layout both NCCL and gloo accept
-    gathered = torch.empty(world * bits.numel(), dtype=bits.dtype, device=dev)
-    dist.all_gather_into_tensor(gathered, bits.contiguous(), group=group)
-    gathered = gathered.view(world, bits.numel())
-    others = torch.cat([gathered[:rank], gathered[rank + 1:]]) if world > 1 else gathered[:0]
-    bits_or = torch.zeros_like(bits)
-    for row in others:
-        bits_or.bitwise_or_(row)
-    k = torch.tensor([pairs.shape[0]], dtype=torch.int64, device=dev)
-    sizes = torch.empty(world, dtype=torch.int64, device=dev)
-    dist.all_gather_into_tensor(sizes, k, group=group)
-    sizes_h = sizes.cpu().tolist()
+    nw = bits.numel()
+    off = send_offset(nw)
+    k = int(pairs.shape[0])
+    if sendbuf is None or sendbuf.numel() != off + 2:
+        sendbuf = torch.zeros(off + 2, dtype=torch.int32, device=dev)
+        sendbuf[:nw] = bits
+    sendbuf[off:].view(torch.int64).fill_(k)
+    gathered = _buf(("bits", nw), world * (off + 2), torch.int32, dev)
+    dist.all_gather_into_tensor(gathered, sendbuf, group=group)
+    gathered = gathered.view(world, off + 2)
+    sizes_h = gathered[:, off:].contiguous().view(torch.int64).view(-1).cpu().tolist()
+    rows = gathered[:, :nw]
     kmax = max(sizes_h) if sizes_h else 0
     if kmax == 0:
-        return bits_or, torch.empty((0, 2), dtype=pairs.dtype, device=dev)
-    padded = torch.zeros((kmax, 2), dtype=pairs.dtype, device=dev)
-    padded[: pairs.shape[0]] = pairs
-    allp = torch.empty(world * kmax * 2, dtype=pairs.dtype, device=dev)
-    dist.all_gather_into_tensor(allp, padded.view(-1), group=group)
+        return rows, rank, torch.empty((0, 2), dtype=pairs.dtype, device=dev)
+    if pairs_buf is not None and pairs_buf.shape[0] >= kmax:
+        send = pairs_buf[:kmax]
+    else:
+        send = torch.zeros((kmax, 2), dtype=pairs.dtype, device=dev)
+        send[:k] = pairs
+    allp = _buf(("pairs", kmax), world * kmax * 2, pairs.dtype, dev)
+    dist.all_gather_into_tensor(allp, send.contiguous().view(-1), group=group)
     allp = allp.view(world * kmax, 2)
-    parts = [allp[r * kmax: r * kmax + sizes_h[r]] for r in range(world) if r != rank]
+    parts = [allp[r * kmax: r * kmax + sizes_h[r]] for r in range(world) if r != rank and sizes_h[r]]
     remote = torch.cat(parts) if parts else torch.empty((0, 2), dtype=pairs.dtype, device=dev)
-    return bits_or, remote
+    return rows, rank, remote
+
+
+def or_rows(rows, rank):
+    """OR of the gathered bitmap rows except `rank`'s (backends without a
+    row-aware re-hook)."""
+    import torch
+    out = torch.zeros_like(rows[0])
+    for r in range(rows.shape[0]):
+        if r != rank:
+            out.bitwise_or_(rows[r])
+    return out
 
 
 def merge_round(backend, group=None, sync=None) -> MergeTimes:
@@ -94,10 +132,14 @@ def merge_round(backend, group=None, sync=None) -> MergeTimes:
     bits, pairs = backend.export()
     sync()
     t1 = time.perf_counter()
-    bits_or, remote = exchange(bits, pairs, group)
+    rows, rank, remote = exchange(bits, pairs, group, getattr(backend, "sendbuf", None),
+                                  getattr(backend, "pairs", None))
     sync()
     t2 = time.perf_counter()
-    mx = backend.rehook(bits_or, remote)
+    if hasattr(backend, "rehook_rows"):
+        mx = backend.rehook_rows(rows, rank, remote)
+    else:
+        mx = backend.rehook(or_rows(rows, rank), remote)
     sync()
     t3 = time.perf_counter()
     t.export_ms, t.exchange_ms, t.rehook_ms = 1e3 * (t1 - t0), 1e3 * (t2 - t1), 1e3 * (t3 - t2)
@@ -119,7 +161,10 @@ class CudaBackend:
         self.device = device
         self.forest = ctx.forest(n)
         self.nwords = (n + 31) // 32
-        self.bits = torch.empty(self.nwords, dtype=torch.int32, device=device)
+        # the exported bitmap is the prefix of the exchange's send buffer
+        self.sendbuf = torch.zeros(send_offset(self.nwords) + 2, dtype=torch.int32,
+                                   device=device)
+        self.bits = self.sendbuf[: self.nwords]
         self.cap = max(1 << 16, n // 64)
         self.pairs = torch.empty((self.cap, 2), dtype=torch.int32, device=device)
         self.local_metrics = None
@@ -143,6 +188,15 @@ class CudaBackend:
         return self.ctx.rehook(self.forest, bits_or.data_ptr(),
                                remote.data_ptr() if remote.shape[0] else None,
                                int(remote.shape[0]))
+
+    def rehook_rows(self, rows, rank, remote):
+        # rows: [world, nwords] view of the gathered buffer (row stride
+        # send_offset(nwords) + 2)
+        remote = remote.contiguous()
+        return self.ctx.rehook_rows(self.forest, rows.data_ptr(), int(rows.shape[0]),
+                                    int(rows.stride(0)), int(rank),
+                                    remote.data_ptr() if remote.shape[0] else None,
+                                    int(remote.shape[0]))
 
     def labels(self) -> np.ndarray:
         return self.forest.snapshot()

@@ -18,7 +18,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1612_01178_b200.distributed import edge_range, exchange, merge_round
+from paper_1612_01178_b200.distributed import edge_range, exchange, merge_round, or_rows
 
 
 def test_edge_range_matches_partition_edges(oracle):
@@ -121,8 +121,9 @@ def test_exchange_single_rank():
     try:
         bits = torch.tensor([5, 0, 7], dtype=torch.int32)
         pairs = torch.tensor([[3, 1]], dtype=torch.int32)
-        b, p = exchange(bits, pairs)
-        assert b.tolist() == [0, 0, 0] and p.shape == (0, 2)
+        rows, rank, p = exchange(bits, pairs)
+        assert rank == 0 and rows.tolist() == [[5, 0, 7]] and p.shape == (0, 2)
+        assert or_rows(rows, rank).tolist() == [0, 0, 0]
     finally:
         dist.destroy_process_group()
 
@@ -150,11 +151,22 @@ def test_gpu_emulated_ranks(ctx, oracle, G, spec):
         be.local_cc(g)
         bits, pairs = be.export()
         ranks.append((be, bits.clone(), pairs.clone()))
+    # the gathered bitmap rows as NCCL would lay them out (row stride
+    # send_offset(nwords) + 2, the pair count in the tail words)
+    from paper_1612_01178_b200.distributed import send_offset
+    nw = ranks[0][1].numel()
+    rows = torch.zeros((G, send_offset(nw) + 2), dtype=torch.int32, device=dev)
+    for s, (_, b, _) in enumerate(ranks):
+        rows[s, :nw] = b
     for r, (be, _, _) in enumerate(ranks):
-        bits_or = torch.zeros_like(ranks[0][1])
-        for s, (_, b, _) in enumerate(ranks):
-            if s != r:
-                bits_or |= b
         remote = torch.cat([p for s, (_, _, p) in enumerate(ranks) if s != r])
-        be.rehook(bits_or, remote)
+        if r % 2:
+            # row-aware re-hook: the kernel ORs every row but r's
+            be.rehook_rows(rows[:, :nw], r, remote)
+        else:
+            bits_or = torch.zeros_like(ranks[0][1])
+            for s, (_, b, _) in enumerate(ranks):
+                if s != r:
+                    bits_or |= b
+            be.rehook(bits_or, remote)
         assert np.array_equal(be.labels(), want), (spec, G, r)
