@@ -5,7 +5,7 @@
  * This is the drop-in boundary for the reference `hookcc` hot path
  * (reference: /root/reference/proj/include/hookcc/{engines,forest,graph}.hpp).
  * Plain pointers and sizes only; no C++ or torch types cross it. The C++
- * header-compatible API in include/hookcc/*.hpp is a thin shim over these
+ * header-compatible API in the include/hookcc headers is a thin shim over these
  * entry points, and Python binds them with ctypes
  * (paper_1612_01178_b200/capi.py). Each entry point cites the reference
  * interface it replaces.
@@ -200,6 +200,14 @@ int hcc_graph_from_csr(hcc_ctx* ctx, const uint64_t* row_ptr,
  * same size keeps its device buffer and the cached executable CUDA graph. */
 int hcc_graph_assign_edges_u32(hcc_ctx* ctx, hcc_graph* g, const uint32_t* uv,
                                uint64_t first, uint64_t count);
+/* Asynchronous refill: the copy (from PINNED host memory for overlap) and
+ * the endpoint check run on the context's copy stream and the call returns
+ * at once.  Every later call that reads the graph (hcc_cc, ...) first waits
+ * for it and returns HCC_ERANGE if an endpoint was out of range.  With two
+ * graph handles used alternately, the next input uploads while the current
+ * one runs (the context keeps both executable CUDA graphs). */
+int hcc_graph_upload_async(hcc_ctx* ctx, hcc_graph* g, const uint32_t* uv,
+                           uint64_t first, uint64_t count);
 /* Device generators. spec: "grid:RxC" (identical to generators.hpp:71-87),
  * "rmatx:scale=K,ef=F[,seed=S][,a=..,b=..,c=..,d=..]" and
  * "erx:n=N,m=M[,seed=S]" (counter-based twins of generators.hpp:14-62,

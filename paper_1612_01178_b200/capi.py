@@ -84,6 +84,7 @@ _SIGS = {
     "hcc_graph_from_edges_u32": (i32, [vp, vp, u64, u64, C.POINTER(vp)]),
     "hcc_graph_from_csr": (i32, [vp, vp, vp, u64, C.POINTER(vp)]),
     "hcc_graph_assign_edges_u32": (i32, [vp, vp, vp, u64, u64]),
+    "hcc_graph_upload_async": (i32, [vp, vp, vp, u64, u64]),
     "hcc_graph_generate": (i32, [vp, C.c_char_p, u64, C.POINTER(vp)]),
     "hcc_graph_info": (i32, [vp, C.POINTER(u64), C.POINTER(u64)]),
     "hcc_graph_download_u32": (i32, [vp, vp, vp, u64, u64]),
@@ -345,6 +346,16 @@ class Graph:
         e = np.ascontiguousarray(edges, dtype=np.uint32).reshape(-1, 2)
         check(lib().hcc_graph_assign_edges_u32(self.ctx.h, self.h, _ptr(e) if e.size else None,
                                                first, e.shape[0]))
+
+    def upload_async(self, edges: np.ndarray, first: int = 0) -> None:
+        """hcc_graph_upload_async: refill edges [first, first+len) on the copy
+        stream and return at once (`edges` must stay alive and unchanged until
+        the next call that reads this graph; pinned memory for overlap)."""
+        e = edges.reshape(-1, 2)
+        if e.dtype != np.uint32 or not e.flags["C_CONTIGUOUS"]:
+            raise ValueError("upload_async needs a C-contiguous uint32 (m, 2) array")
+        check(lib().hcc_graph_upload_async(self.ctx.h, self.h, _ptr(e) if e.size else None,
+                                           first, e.shape[0]))
 
     def checksum(self) -> int:
         out = u64()

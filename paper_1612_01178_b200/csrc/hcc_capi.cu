@@ -153,9 +153,18 @@ struct hcc_ctx {
   u64 wl_cap = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int occ_hook = 1, occ_vert = 1, occ_hook_sum = 1;
-  // cached executable graph for repeated calls with identical arguments
+  // cached executable graph for repeated calls with identical arguments,
+  // plus the previous one (two graphs used alternately, e.g. a pipelined
+  // upload into one while the other runs, keep both instantiated)
   cudaGraphExec_t exec = nullptr;
   GraphKey key;
+  cudaGraphExec_t alt_exec = nullptr;
+  GraphKey alt_key;
+  u64 alt_seg_ev = 0;
+  std::vector<int> alt_slot_kernel;
+  int alt_wl_kernel = 0;
+  cudaStream_t copy_stream = nullptr;  // hcc_graph_upload_async
+  cudaEvent_t order_ev = nullptr;      // copy stream after the context stream
   std::vector<hcc_segment_rec> last_recs;
   // CUDA events around the unrolled topology hook launches
   std::vector<cudaEvent_t> seg_ev;   // 2 per segment
@@ -180,6 +189,12 @@ struct hcc_graph {
   uint2* d_edges = nullptr;
   bool has_stats = false;
   hcc_graph_stats stats{};
+  // hcc_graph_upload_async: copy + endpoint check in flight on the
+  // context's copy stream; every reader waits for it (graph_ready)
+  mutable bool pending = false;
+  cudaEvent_t up_ev = nullptr;
+  u32* d_err = nullptr;  // device endpoint-check flag
+  u32* h_err = nullptr;  // pinned copy of it
 };
 
 struct hcc_forest {
@@ -262,6 +277,9 @@ void drop_exec(hcc_ctx* c) {
   if (c->exec) cudaGraphExecDestroy(c->exec);
   c->exec = nullptr;
   c->key = GraphKey{};
+  if (c->alt_exec) cudaGraphExecDestroy(c->alt_exec);
+  c->alt_exec = nullptr;
+  c->alt_key = GraphKey{};
 }
 
 unsigned grid_for(u64 work, unsigned block, u64 cap) {
@@ -893,6 +911,11 @@ int hcc_destroy(hcc_ctx* c) {
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->copy_stream) {
+    cudaStreamSynchronize(c->copy_stream);
+    cudaStreamDestroy(c->copy_stream);
+  }
+  if (c->order_ev) cudaEventDestroy(c->order_ev);
   delete c;
   return HCC_OK;
 }
@@ -1010,8 +1033,56 @@ int hcc_graph_from_edges_u32(hcc_ctx* c, const uint32_t* uv, uint64_t m,
   }
 }
 
+// Wait for a graph's pending asynchronous upload and report its endpoint
+// check (check_endpoints, graph.hpp:89-94).  Every entry point that reads a
+// graph's edges calls this first.
+static int graph_ready(const hcc_graph* g) {
+  if (!g || !g->pending) return HCC_OK;
+  HCC_CUDA(cudaEventSynchronize(g->up_ev));
+  g->pending = false;
+  if (*g->h_err) return fail(HCC_ERANGE, "edge endpoint out of range");
+  return HCC_OK;
+}
+
+int hcc_graph_upload_async(hcc_ctx* c, hcc_graph* g, const uint32_t* uv, uint64_t first,
+                           uint64_t count) {
+  if (!g || (count && !uv)) return fail(HCC_EINVAL, "null argument");
+  if (first > g->m || count > g->m - first)
+    return fail(HCC_EINVAL, "range out of bounds");
+  if (int r = ctx_enter(c)) return r;
+  if (int r = graph_ready(g)) return r;  // one upload in flight per graph
+  HCC_GUARD_BEGIN
+  if (!c->copy_stream)
+    HCC_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  if (!g->up_ev) {
+    HCC_CUDA(cudaEventCreateWithFlags(&g->up_ev, cudaEventDisableTiming));
+    HCC_CUDA(cudaMalloc(&g->d_err, sizeof(u32)));
+    HCC_CUDA(cudaMallocHost(&g->h_err, sizeof(u32)));
+  }
+  // the graph's previous readers ran on the context stream
+  if (!c->order_ev) HCC_CUDA(cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming));
+  HCC_CUDA(cudaEventRecord(c->order_ev, c->stream));
+  HCC_CUDA(cudaStreamWaitEvent(c->copy_stream, c->order_ev, 0));
+  HCC_CUDA(cudaMemsetAsync(g->d_err, 0, sizeof(u32), c->copy_stream));
+  if (count) {
+    HCC_CUDA(cudaMemcpyAsync(g->d_edges + first, uv, count * sizeof(uint2),
+                             cudaMemcpyHostToDevice, c->copy_stream));
+    k_check_u32<<<grid_for(count, 256, 65536), 256, 0, c->copy_stream>>>(g->d_edges + first,
+                                                                         count, g->n, g->d_err);
+    HCC_CUDA(cudaGetLastError());
+  }
+  HCC_CUDA(cudaMemcpyAsync(g->h_err, g->d_err, sizeof(u32), cudaMemcpyDeviceToHost,
+                           c->copy_stream));
+  HCC_CUDA(cudaEventRecord(g->up_ev, c->copy_stream));
+  g->pending = true;
+  g->has_stats = false;
+  return HCC_OK;
+  HCC_GUARD_END
+}
+
 int hcc_graph_assign_edges_u32(hcc_ctx* c, hcc_graph* g, const uint32_t* uv,
                                uint64_t first, uint64_t count) {
+  if (int r = graph_ready(g)) return r;
   if (!g || (count && !uv)) return fail(HCC_EINVAL, "null argument");
   if (first > g->m || count > g->m - first)
     return fail(HCC_EINVAL, "range out of bounds");
@@ -1200,6 +1271,7 @@ int hcc_graph_info(const hcc_graph* g, uint64_t* n, uint64_t* m) {
 
 int hcc_graph_download_u32(hcc_ctx* c, const hcc_graph* g, uint32_t* uv,
                            uint64_t first, uint64_t count) {
+  if (int r = graph_ready(g)) return r;
   if (!g || (count && !uv)) return fail(HCC_EINVAL, "null argument");
   if (first > g->m || count > g->m - first)
     return fail(HCC_EINVAL, "range out of bounds");
@@ -1213,6 +1285,7 @@ int hcc_graph_download_u32(hcc_ctx* c, const hcc_graph* g, uint32_t* uv,
 }
 
 int hcc_graph_checksum(hcc_ctx* c, const hcc_graph* g, uint64_t* out) {
+  if (int r = graph_ready(g)) return r;
   if (!g || !out) return fail(HCC_EINVAL, "null argument");
   if (int r = ctx_enter(c)) return r;
   u64* d = nullptr;
@@ -1237,6 +1310,7 @@ int hcc_graph_checksum(hcc_ctx* c, const hcc_graph* g, uint64_t* out) {
 
 int hcc_graph_compute_stats(hcc_ctx* c, const hcc_graph* g_c,
                             hcc_graph_stats* out) {
+  if (int r = graph_ready(g_c)) return r;
   if (!g_c || !out) return fail(HCC_EINVAL, "null argument");
   if (int r = ctx_enter(c)) return r;
   hcc_graph* g = const_cast<hcc_graph*>(g_c);
@@ -1253,8 +1327,13 @@ int hcc_graph_free(hcc_graph* g) {
   if (g->ctx) {
     cudaSetDevice(g->ctx->dev);
     // the cached executable graph may reference these edges
-    if (g->ctx->key.edges == g->d_edges) drop_exec(g->ctx);
+    if (g->ctx->key.edges == g->d_edges || g->ctx->alt_key.edges == g->d_edges)
+      drop_exec(g->ctx);
+    if (g->pending) cudaEventSynchronize(g->up_ev);
   }
+  if (g->up_ev) cudaEventDestroy(g->up_ev);
+  cudaFree(g->d_err);
+  cudaFreeHost(g->h_err);
   cudaFree(g->d_edges);
   delete g;
   return HCC_OK;
@@ -1308,6 +1387,7 @@ static std::vector<u64> geometric_bounds(u64 m) {
 
 static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
                   hcc_forest* f, hcc_metrics* mx) {
+  if (int r = graph_ready(g)) return r;
   const hcc_opts defaults = {HCC_ALGO_BASELINE_MJ, 0, 0, 0, 0, nullptr, nullptr};
   if (!o) o = &defaults;
   if (o->algo < HCC_ALGO_BASELINE || o->algo > HCC_ALGO_ADAPTIVE)
@@ -1539,8 +1619,23 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   for (u64 x : P.bounds) key.plan = key.plan * 1000003ull + x;
 
   if (graph_mode) {
+    if (!(c->exec && c->key == key) && c->alt_exec && c->alt_key == key) {
+      std::swap(c->exec, c->alt_exec);
+      std::swap(c->key, c->alt_key);
+      std::swap(c->exec_seg_ev, c->alt_seg_ev);
+      std::swap(c->exec_slot_kernel, c->alt_slot_kernel);
+      std::swap(c->exec_wl_kernel, c->alt_wl_kernel);
+    }
     if (!(c->exec && c->key == key)) {
-      drop_exec(c);
+      // keep the current executable graph as the alternate
+      if (c->alt_exec) cudaGraphExecDestroy(c->alt_exec);
+      c->alt_exec = c->exec;
+      c->alt_key = c->key;
+      c->alt_seg_ev = c->exec_seg_ev;
+      c->alt_slot_kernel = c->exec_slot_kernel;
+      c->alt_wl_kernel = c->exec_wl_kernel;
+      c->exec = nullptr;
+      c->key = GraphKey{};
       cudaGraph_t graph = nullptr;
       HCC_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
       try {
@@ -1760,7 +1855,8 @@ int hcc_forest_create(hcc_ctx* c, uint64_t n, hcc_forest** out) {
 int hcc_forest_free(hcc_forest* f) {
   if (!f) return HCC_OK;
   cudaSetDevice(f->dev);
-  if (f->ctx && f->ctx->key.pi == f->d_pi) drop_exec(f->ctx);
+  if (f->ctx && (f->ctx->key.pi == f->d_pi || f->ctx->alt_key.pi == f->d_pi))
+    drop_exec(f->ctx);
   cudaFree(f->d_pi);
   delete f;
   return HCC_OK;
@@ -1970,6 +2066,7 @@ int hcc_forest_check_bound(hcc_forest* f, int* ok) {
 
 int hcc_forest_verify(hcc_ctx* c, const hcc_graph* g, hcc_forest* f,
                       uint64_t* bad_edges, uint64_t* bad_vertices) {
+  if (int r = graph_ready(g)) return r;
   if (!g || !f || !bad_edges || !bad_vertices) return fail(HCC_EINVAL, "null argument");
   if (f->n != g->n) return fail(HCC_EINVAL, "forest size does not match the graph");
   if (int r = ctx_enter(c)) return r;

@@ -574,3 +574,32 @@ def test_graph_assign_reuses_handle(ctx, oracle):
     with pytest.raises(C.HccError) as ei:
         g.assign(np.array([[0, 4096]], dtype=np.uint32))
     assert ei.value.code == C.HCC_ERANGE
+
+
+def test_async_upload_pipelined(ctx, oracle, capi):
+    """hcc_graph_upload_async: two graph handles used alternately (the next
+    input uploads on the copy stream while the current one runs, as the
+    bench's pipelined e2e leg does) give the oracle's labels for each input;
+    an out-of-range endpoint surfaces as HCC_ERANGE from the next reader."""
+    import torch
+    n = 1 << 16
+    e = [ctx.generate(f"rmatx:scale=16,ef=16,seed={s}").edges() for s in (1, 2)]
+    want = [oracle.cc(n, x) for x in e]
+    host = [torch.from_numpy(x.view(np.int32)).pin_memory().numpy().view(np.uint32) for x in e]
+    gs = [ctx.graph_from_edges(e[0], n), ctx.graph_from_edges(e[0], n)]
+    gs[0].upload_async(host[0])
+    for i in range(6):
+        if i + 1 < 6:
+            gs[(i + 1) % 2].upload_async(host[(i + 1) % 2])
+        lab, _ = ctx.cc(gs[i % 2], "baseline-mj")
+        assert np.array_equal(lab, want[i % 2]), i
+    bad = host[1].copy()
+    bad[7, 1] = n
+    gs[0].upload_async(bad)
+    with pytest.raises(capi.HccError):
+        ctx.cc(gs[0], "baseline-mj")
+    gs[0].assign(host[0])
+    lab, _ = ctx.cc(gs[0], "baseline-mj")
+    assert np.array_equal(lab, want[0])
+    for g in gs:
+        g.close()
