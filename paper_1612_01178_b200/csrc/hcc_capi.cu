@@ -165,6 +165,8 @@ struct hcc_ctx {
   int alt_wl_kernel = 0;
   cudaStream_t copy_stream = nullptr;  // hcc_graph_upload_async
   cudaEvent_t order_ev = nullptr;      // copy stream after the context stream
+  cudaStream_t check_stream = nullptr; // endpoint checks of landed chunks
+  std::vector<cudaEvent_t> chunk_ev;   // one per in-flight upload chunk
   std::vector<hcc_segment_rec> last_recs;
   // CUDA events around the unrolled topology hook launches
   std::vector<cudaEvent_t> seg_ev;   // 2 per segment
@@ -915,7 +917,12 @@ int hcc_destroy(hcc_ctx* c) {
     cudaStreamSynchronize(c->copy_stream);
     cudaStreamDestroy(c->copy_stream);
   }
+  if (c->check_stream) {
+    cudaStreamSynchronize(c->check_stream);
+    cudaStreamDestroy(c->check_stream);
+  }
   if (c->order_ev) cudaEventDestroy(c->order_ev);
+  for (cudaEvent_t ev : c->chunk_ev) cudaEventDestroy(ev);
   delete c;
   return HCC_OK;
 }
@@ -1052,8 +1059,10 @@ int hcc_graph_upload_async(hcc_ctx* c, hcc_graph* g, const uint32_t* uv, uint64_
   if (int r = ctx_enter(c)) return r;
   if (int r = graph_ready(g)) return r;  // one upload in flight per graph
   HCC_GUARD_BEGIN
-  if (!c->copy_stream)
+  if (!c->copy_stream) {
     HCC_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    HCC_CUDA(cudaStreamCreateWithFlags(&c->check_stream, cudaStreamNonBlocking));
+  }
   if (!g->up_ev) {
     HCC_CUDA(cudaEventCreateWithFlags(&g->up_ev, cudaEventDisableTiming));
     HCC_CUDA(cudaMalloc(&g->d_err, sizeof(u32)));
@@ -1064,16 +1073,30 @@ int hcc_graph_upload_async(hcc_ctx* c, hcc_graph* g, const uint32_t* uv, uint64_
   HCC_CUDA(cudaEventRecord(c->order_ev, c->stream));
   HCC_CUDA(cudaStreamWaitEvent(c->copy_stream, c->order_ev, 0));
   HCC_CUDA(cudaMemsetAsync(g->d_err, 0, sizeof(u32), c->copy_stream));
-  if (count) {
-    HCC_CUDA(cudaMemcpyAsync(g->d_edges + first, uv, count * sizeof(uint2),
+  // chunked copy; each chunk's endpoint check runs on the check stream while
+  // the next chunk copies, so only the last check follows the transfer
+  constexpr u64 kChunk = 16ull << 20;  // edges (128 MiB)
+  const u64 nch = (count + kChunk - 1) / kChunk;
+  while (c->chunk_ev.size() < nch) {
+    cudaEvent_t ev;
+    HCC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    c->chunk_ev.push_back(ev);
+  }
+  HCC_CUDA(cudaEventRecord(c->order_ev, c->copy_stream));
+  HCC_CUDA(cudaStreamWaitEvent(c->check_stream, c->order_ev, 0));
+  for (u64 k = 0; k < nch; ++k) {
+    const u64 b = first + k * kChunk, cnt = std::min<u64>(kChunk, count - k * kChunk);
+    HCC_CUDA(cudaMemcpyAsync(g->d_edges + b, uv + 2 * (b - first), cnt * sizeof(uint2),
                              cudaMemcpyHostToDevice, c->copy_stream));
-    k_check_u32<<<grid_for(count, 256, 65536), 256, 0, c->copy_stream>>>(g->d_edges + first,
-                                                                         count, g->n, g->d_err);
+    HCC_CUDA(cudaEventRecord(c->chunk_ev[k], c->copy_stream));
+    HCC_CUDA(cudaStreamWaitEvent(c->check_stream, c->chunk_ev[k], 0));
+    k_check_u32<<<grid_for(cnt, 256, 65536), 256, 0, c->check_stream>>>(g->d_edges + b, cnt,
+                                                                        g->n, g->d_err);
     HCC_CUDA(cudaGetLastError());
   }
   HCC_CUDA(cudaMemcpyAsync(g->h_err, g->d_err, sizeof(u32), cudaMemcpyDeviceToHost,
-                           c->copy_stream));
-  HCC_CUDA(cudaEventRecord(g->up_ev, c->copy_stream));
+                           c->check_stream));
+  HCC_CUDA(cudaEventRecord(g->up_ev, c->check_stream));
   g->pending = true;
   g->has_stats = false;
   return HCC_OK;
