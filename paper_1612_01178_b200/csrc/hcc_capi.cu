@@ -1105,28 +1105,9 @@ int hcc_graph_upload_async(hcc_ctx* c, hcc_graph* g, const uint32_t* uv, uint64_
 
 int hcc_graph_assign_edges_u32(hcc_ctx* c, hcc_graph* g, const uint32_t* uv,
                                uint64_t first, uint64_t count) {
-  if (int r = graph_ready(g)) return r;
-  if (!g || (count && !uv)) return fail(HCC_EINVAL, "null argument");
-  if (first > g->m || count > g->m - first)
-    return fail(HCC_EINVAL, "range out of bounds");
-  if (int r = ctx_enter(c)) return r;
-  HCC_GUARD_BEGIN
-  u32* d_err = reinterpret_cast<u32*>(&c->d_ctrl->err);
-  HCC_CUDA(cudaMemsetAsync(d_err, 0, sizeof(u32), c->stream));
-  if (count) {
-    HCC_CUDA(cudaMemcpyAsync(g->d_edges + first, uv, count * sizeof(uint2),
-                             cudaMemcpyHostToDevice, c->stream));
-    k_check_u32<<<grid_for(count, 256, 65536), 256, 0, c->stream>>>(g->d_edges + first,
-                                                                    count, g->n, d_err);
-    HCC_CUDA(cudaGetLastError());
-  }
-  u32 err = 0;
-  HCC_CUDA(cudaMemcpyAsync(&err, d_err, sizeof(u32), cudaMemcpyDeviceToHost, c->stream));
-  HCC_CUDA(cudaStreamSynchronize(c->stream));
-  g->has_stats = false;
-  if (err) return fail(HCC_ERANGE, "edge endpoint out of range");
-  return HCC_OK;
-  HCC_GUARD_END
+  // the chunked upload with overlapped endpoint checks, then wait for it
+  if (int r = hcc_graph_upload_async(c, g, uv, first, count)) return r;
+  return graph_ready(g);
 }
 
 int hcc_graph_from_csr(hcc_ctx* c, const uint64_t* row_ptr, const uint32_t* col,
