@@ -394,6 +394,12 @@ class Forest:
         check(lib().hcc_forest_download_u64(self.h, _ptr(out) if self.n else None))
         return out
 
+    def download_u32(self, out: np.ndarray) -> np.ndarray:
+        """The labels as u32 into a caller buffer (pinned for full PCIe speed)."""
+        assert out.dtype == np.uint32 and out.size >= self.n and out.flags["C_CONTIGUOUS"]
+        check(lib().hcc_forest_download_u32(self.h, _ptr(out) if self.n else None))
+        return out
+
     def upload(self, parents) -> None:
         a = np.ascontiguousarray(parents, dtype=np.uint64)
         check(lib().hcc_forest_upload_u64(self.h, _ptr(a) if self.n else None))
