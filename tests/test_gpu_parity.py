@@ -601,5 +601,11 @@ def test_async_upload_pipelined(ctx, oracle, capi):
     gs[0].assign(host[0])
     lab, _ = ctx.cc(gs[0], "baseline-mj")
     assert np.array_equal(lab, want[0])
+    # three graphs in rotation: the two-entry executable-graph cache misses
+    # and re-captures every call, and must still run the right edges
+    gs.append(ctx.graph_from_edges(e[1], n))
+    for i in range(5):
+        lab, _ = ctx.cc(gs[i % 3], "baseline-mj")
+        assert np.array_equal(lab, want[[0, 1, 1][i % 3]]), i
     for g in gs:
         g.close()
