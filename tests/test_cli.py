@@ -62,6 +62,11 @@ def test_cli_smoke_on_b200(tmp_path):
     bad = labels.replace("0 0\n1 0\n", "0 0\n1 1\n", 1)
     (tmp_path / "bad.txt").write_text(bad)
     assert cc("verify", "--gen", "grid:20x20", tmp_path / "bad.txt").returncode == 1
+    # same partition under other representatives: not equal arrays, so this
+    # goes through the device partition compare (hcc_labels_compare)
+    relab = "".join(f"{ln.split()[0]} 399\n" for ln in labels.splitlines() if ln.strip())
+    (tmp_path / "relab.txt").write_text(relab)
+    assert cc("verify", "--gen", "grid:20x20", tmp_path / "relab.txt").returncode == 0
     r = cc("sweep", "--gen", "rmat:scale=8,ef=8,seed=5", "--sweep-segments", "2,4",
            "--report", "csv", "--metrics-out", tmp_path / "sweep.csv")
     assert r.returncode == 0, r.stderr

@@ -1,6 +1,8 @@
 """Summarise an ncu --set full capture of one RMAT-24 run into profiles/.
 
-python tools/make_profiles.py gpurun_out/<rep>.ncu-rep <tag>
+python tools/make_profiles.py gpurun_out/<rep>.ncu-rep <tag> [workload]
+
+workload defaults to rmat24; hook_traffic.json is written only for rmat24.
 
 Writes
   profiles/<tag>_ncu_launches.csv  one row per captured launch: kernel, grid,
@@ -27,7 +29,16 @@ ROOT = Path(__file__).resolve().parents[1]
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
         "lts__throughput.avg.pct_of_peak_sustained_elapsed",
-        "sm__warps_active.avg.pct_of_peak_sustained_active"]
+        "sm__warps_active.avg.pct_of_peak_sustained_active",
+        # sector efficiency (north star: "dram__bytes and sector-efficiency
+        # counters"): % of each fetched 32-byte sector the global loads /
+        # stores actually use, sectors per load request, L2 hit rate
+        "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.pct",
+        "smsp__sass_average_data_bytes_per_sector_mem_global_op_st.pct",
+        "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+        "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
+        "lts__t_sector_hit_rate.pct",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
 SCALE = {"us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1.0, "byte": 1.0, "Kbyte": 1e3,
          "Mbyte": 1e6, "Gbyte": 1e9, "%": 1.0, "": 1.0}
 
@@ -51,17 +62,27 @@ def rows(rep: str) -> list[dict]:
 
 def main() -> None:
     rep, tag = sys.argv[1], sys.argv[2]
+    workload = sys.argv[3] if len(sys.argv) > 3 else "rmat24"
     rs = rows(rep)
     prof = ROOT / "profiles"
     with open(prof / f"{tag}_ncu_launches.csv", "w", newline="") as f:
         w = csv.writer(f)
         w.writerow(["id", "kernel", "grid", "block", "duration_us", "dram_read_MB",
-                    "dram_write_MB", "l1tex_pct", "lts_pct", "warps_active_pct"])
+                    "dram_write_MB", "dram_GBps", "dram_pct_peak", "l1tex_pct", "lts_pct",
+                    "warps_active_pct", "ld_sector_use_pct", "st_sector_use_pct",
+                    "ld_sectors_per_req", "l2_hit_pct"])
         for e in rs:
+            req = e[KEYS[9]]
             w.writerow([e["id"], e["kernel"], e["grid"], e["block"],
                         round(e[KEYS[0]] * 1e6, 3), round(e[KEYS[1]] / 1e6, 3),
-                        round(e[KEYS[2]] / 1e6, 3), round(e[KEYS[3]], 1), round(e[KEYS[4]], 1),
-                        round(e[KEYS[5]], 1)])
+                        round(e[KEYS[2]] / 1e6, 3),
+                        round((e[KEYS[1]] + e[KEYS[2]]) / e[KEYS[0]] / 1e9, 1),
+                        round(e[KEYS[11]], 1), round(e[KEYS[3]], 1), round(e[KEYS[4]], 1),
+                        round(e[KEYS[5]], 1), round(e[KEYS[6]], 1), round(e[KEYS[7]], 1),
+                        round(e[KEYS[8]] / req, 2) if req else float("nan"),
+                        round(e[KEYS[10]], 1)])
+    if workload != "rmat24":
+        return
     # the streaming topology hook's launches (k_hook / k_hook_sum that did
     # work: a gated-out launch exits in a few microseconds), as the bench's
     # roofline: k_hook_small (slot 0) and the worklist kernels are others
