@@ -1,6 +1,9 @@
 """Summarise an ncu --set full capture of one RMAT-24 run into profiles/.
 
-python tools/make_profiles.py gpurun_out/<rep>.ncu-rep <tag> [workload]
+python tools/make_profiles.py gpurun_out/<rep>.ncu-rep|<raw>.csv.gz <tag> [workload]
+
+Sector use = bytes the global loads / stores use per 32-byte sector fetched
+(smsp__sass_average_data_bytes_per_sector_mem_global_op_*.ratio / 32).
 
 workload defaults to rmat24; hook_traffic.json is written only for rmat24.
 
@@ -33,19 +36,23 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         # sector efficiency (north star: "dram__bytes and sector-efficiency
         # counters"): % of each fetched 32-byte sector the global loads /
         # stores actually use, sectors per load request, L2 hit rate
-        "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.pct",
-        "smsp__sass_average_data_bytes_per_sector_mem_global_op_st.pct",
+        "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.ratio",
+        "smsp__sass_average_data_bytes_per_sector_mem_global_op_st.ratio",
         "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
         "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
         "lts__t_sector_hit_rate.pct",
-        "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]
 SCALE = {"us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1.0, "byte": 1.0, "Kbyte": 1e3,
          "Mbyte": 1e6, "Gbyte": 1e9, "%": 1.0, "": 1.0}
 
 
 def rows(rep: str) -> list[dict]:
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], check=True,
-                         capture_output=True, text=True).stdout
+    if rep.endswith(".csv.gz"):  # `ncu -i rep --page raw --csv | gzip` made on the box
+        import gzip
+        out = gzip.open(rep, "rt").read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], check=True,
+                             capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(out)))
     head, units = r[0], dict(zip(r[0], r[1]))
     res = []
@@ -78,7 +85,8 @@ def main() -> None:
                         round(e[KEYS[2]] / 1e6, 3),
                         round((e[KEYS[1]] + e[KEYS[2]]) / e[KEYS[0]] / 1e9, 1),
                         round(e[KEYS[11]], 1), round(e[KEYS[3]], 1), round(e[KEYS[4]], 1),
-                        round(e[KEYS[5]], 1), round(e[KEYS[6]], 1), round(e[KEYS[7]], 1),
+                        round(e[KEYS[5]], 1), round(e[KEYS[6]] / 32 * 100, 1),
+                        round(e[KEYS[7]] / 32 * 100, 1),
                         round(e[KEYS[8]] / req, 2) if req else float("nan"),
                         round(e[KEYS[10]], 1)])
     if workload != "rmat24":
