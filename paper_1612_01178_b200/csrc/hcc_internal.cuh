@@ -23,7 +23,7 @@ typedef unsigned int u32;
 
 constexpr int kMaxRecs = 4096;    // per-run phase records kept on device
 #ifndef HCC_SMALL_CTA
-#define HCC_SMALL_CTA 256
+#define HCC_SMALL_CTA 1024
 #endif
 constexpr int kHookThreads = HCC_SMALL_CTA;  // k_hook_small CTA (full grid)
 #ifndef HCC_SMALL_EPT
