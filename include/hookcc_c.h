@@ -30,14 +30,16 @@
 extern "C" {
 #endif
 
-#define HCC_ABI_VERSION 3
+#define HCC_ABI_VERSION 4
 
 typedef enum hcc_status {
   HCC_OK = 0,
   HCC_EINVAL = 1,    /* bad argument; reference: std::invalid_argument    */
   HCC_ENOMEM = 2,    /* device or host allocation failed                  */
   HCC_ECUDA = 3,     /* CUDA runtime error                                */
-  HCC_ENCCL = 4,     /* NCCL error (multi-GPU merge)                      */
+  HCC_ENCCL = 4,     /* multi-GPU transport error: no peer access between
+                        the devices of hcc_create_multi (or NCCL, for the
+                        multi-process binding)                            */
   HCC_ENOTSTAR = 5,  /* forest not star-shaped; reference: std::logic_error
                         from extract_labels (engines.hpp:66-70)            */
   HCC_ENODEV = 6,    /* no usable sm_100 GPU                              */
@@ -133,6 +135,12 @@ typedef struct hcc_metrics {
   uint64_t kernels;         /* kernels this run launched (pi init through
                                convergence)                                */
   int star0_bitmap;         /* 1 = the star-0 bitmap fast path was used    */
+  uint64_t wl_capacity;     /* records per worklist buffer (2 buffers): the
+                               streaming engine sizes them to
+                               max(m/8, 2n) + chunk padding, not m          */
+  uint32_t wl_reruns;       /* 1 = a worklist overflowed (device flag) and
+                               the run was repeated with m-sized lists      */
+  uint32_t reserved_m;
 } hcc_metrics;
 
 /* One record per segment / outer iteration / worklist pass
@@ -312,6 +320,45 @@ int hcc_rehook_rows(hcc_ctx* ctx, hcc_forest* f, const uint32_t* dev_bit_rows,
 int hcc_graph_generate_range(hcc_ctx* ctx, const char* spec,
                              uint64_t default_seed, uint64_t first,
                              uint64_t count, hcc_graph** out);
+
+/* ---- multi-GPU in one process (north-star (5); reference entry
+ * points engines.hpp:316-338 run with a device list) -----------------------
+ * hcc_create_multi builds a context with one shard per entry of `devices`
+ * (a device may repeat: its shards then share it; peer access is enabled
+ * between every pair of distinct devices, HCC_ENCCL if unavailable).  On
+ * such a context every graph entry point (hcc_graph_from_edges_*,
+ * hcc_graph_from_csr, hcc_graph_generate[_range], upload/assign/download,
+ * checksum, compute_stats) works on an edge-partitioned graph: shard r =
+ * partition_edges(m, ndev)[r] (engines.hpp:43-58) on devices[r].  hcc_cc /
+ * hcc_cc_u64 then run every shard's local CC concurrently (one host thread
+ * per shard), export each local forest (bitmap of pi(v) == 0 + sparse
+ * (v, pi(v)) pairs), and merge with one kernel per shard that reads the
+ * peers' exports in place over NVLink (P2P) and re-hooks what its forest
+ * lacks: no NCCL, no staging copy, no host read of the payload sizes.
+ * The labels (and a caller forest `pi`, which must live on devices[0]) are
+ * the global min-canonical labels.  metrics.total_ms = max over shards of
+ * (local CC + merge) device time; per-shard detail: hcc_ctx_shard_metrics.
+ * hcc_forest_create on the context allocates on devices[0]. */
+typedef struct hcc_shard_metrics {
+  double total_ms;          /* local_ms + merge_ms (this shard's device time) */
+  double local_ms;          /* local CC, pi init through convergence          */
+  double merge_ms;          /* NVLink gather + re-hook passes                 */
+  double span_ms;           /* first to last event of the shard's call,
+                               including the host hand-off between phases    */
+  uint64_t pairs_exported;  /* sparse pairs this shard exported              */
+  uint64_t records_merged;  /* remote relations this shard re-hooked         */
+  uint64_t rehook_passes;
+  uint64_t bitmap_bytes;    /* exported bitmap size                          */
+  int device;
+  int peer_access;          /* 1: exports read over P2P                      */
+} hcc_shard_metrics;
+
+int hcc_create_multi(const int* devices, int ndev, hcc_ctx** out);
+/* 1 for a single-device context. */
+int hcc_ctx_shards(hcc_ctx* ctx, int* count);
+/* Per-shard metrics of the last hcc_cc on a multi-device context. */
+int hcc_ctx_shard_metrics(hcc_ctx* ctx, hcc_shard_metrics* out, uint64_t cap,
+                          uint64_t* count);
 
 #ifdef __cplusplus
 }  /* extern "C" */

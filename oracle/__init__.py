@@ -63,6 +63,8 @@ def _olib() -> C.CDLL:
             "oracle_checksum_u32": (u64, [vp, u64, u64]),
             "oracle_cc_u64": (i32, [u64, vp, u64, vp]),
             "oracle_cc_u32": (i32, [u64, vp, u64, vp]),
+            "oracle_cc_stream": (i32, [i32, u32, dbl, dbl, dbl, u64, u64, u64, u64, i32, vp,
+                                       C.POINTER(u64), C.POINTER(u64)]),
             "oracle_bfs_cc_u64": (i32, [u64, vp, u64, vp]),
             "oracle_hook": (i32, [vp, u64, u64]),
             "oracle_jump": (i32, [vp, u64]),
@@ -182,6 +184,34 @@ def cc(n: int, edges) -> np.ndarray:
     if _olib().oracle_cc_u64(n, _p(e), e.shape[0], _p(out)):
         raise ValueError("endpoint out of range")
     return out
+
+
+def cc_stream(spec: str, first: int = 0, count: int | None = None, threads: int = 0):
+    """Streaming oracle_cc over a counter-based generator spec (rmatx / erx),
+    never materialising the edges: -> (labels u32, edge checksum, components).
+    For graphs too large to hold (RMAT-28: 2^32 edges, 1 GiB of labels)."""
+    import os
+    kind, params = spec.split(":", 1)
+    kv = dict(p.split("=") for p in params.split(","))
+    seed = int(kv.get("seed", 1))
+    if kind == "rmatx":
+        scale, ef = int(kv["scale"]), int(kv["ef"])
+        n, m, k, n_er = 1 << scale, ef << scale, 0, 0
+        a, b, c = float(kv.get("a", 0.57)), float(kv.get("b", 0.19)), float(kv.get("c", 0.19))
+    elif kind == "erx":
+        n, m, k, scale = int(kv["n"]), int(kv["m"]), 1, 0
+        n_er, a, b, c = n, 0.0, 0.0, 0.0
+    else:
+        raise ValueError(f"cc_stream: unsupported generator `{kind}`")
+    count = m - first if count is None else count
+    out = np.empty(n, dtype=np.uint32)
+    ck, comp = u64(), u64()
+    rc = _olib().oracle_cc_stream(k, scale, a, b, c, n_er, seed, first, count,
+                                  threads or (os.cpu_count() or 1), _p(out), C.byref(ck),
+                                  C.byref(comp))
+    if rc:
+        raise RuntimeError(f"oracle_cc_stream failed ({rc})")
+    return out, ck.value, comp.value
 
 
 def bfs_cc(n: int, edges) -> np.ndarray:

@@ -17,6 +17,7 @@
  *
  * Build: make -C oracle   (gcc -O3 -shared -fPIC -> oracle/liboracle.so)
  */
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -292,6 +293,129 @@ int oracle_cc_u32(u64 n, const u32* uv, u64 m, u32* labels) {
   int r = oracle_finish(&d, n, NULL, labels);
   dsu_free(&d);
   return r;
+}
+
+/* ---- streaming ground truth for graphs too large to hold (RMAT-28) ------
+ * oracle_cc (oracle.hpp:47-62) over edges [first, first+count) of a
+ * counter-based generator, without materialising the edge array: chunk k+1
+ * is generated by `nthreads` worker threads while the main thread unites
+ * chunk k into the DSU (the unions stay strictly sequential, in stored edge
+ * order, exactly as oracle_cc does over a Graph).  RMAT-28 needs 32 GiB of
+ * edges in the reference layout (64 GiB as u64) but only the 1 GiB u32
+ * parent array here.  Also returns the position-keyed checksum of the
+ * generated stream (oracle_checksum_u32) and the component count.
+ *   kind 0: rmatx (scale, a, b, c, seed)      kind 1: erx (n_er, seed)     */
+typedef struct {
+  int kind;
+  u32 scale;
+  double a, b, c;
+  u64 n_er, seed, first, count;
+  u32* uv;
+  u64 sum;
+} stream_job;
+
+static void* stream_gen(void* p) {
+  stream_job* j = (stream_job*)p;
+  if (j->kind == 0)
+    oracle_gen_rmatx(j->scale, j->a, j->b, j->c, j->seed, j->first, j->count, j->uv);
+  else
+    oracle_gen_erx(j->n_er, j->seed, j->first, j->count, j->uv);
+  j->sum = oracle_checksum_u32(j->uv, j->first, j->count);
+  return NULL;
+}
+
+#define STREAM_CHUNK (1ull << 25) /* edges per chunk (256 MiB of u32 pairs) */
+#define STREAM_MAXT 64
+
+static void stream_fill(int kind, u32 scale, double a, double b, double c, u64 n_er, u64 seed,
+                        u64 first, u64 count, int nt, u32* buf, u64* sum) {
+  pthread_t th[STREAM_MAXT];
+  stream_job jb[STREAM_MAXT];
+  const u64 per = (count + (u64)nt - 1) / (u64)nt;
+  int started = 0;
+  for (int t = 0; t < nt; ++t) {
+    const u64 b0 = (u64)t * per;
+    if (b0 >= count) break;
+    stream_job x = {kind, scale, a, b, c, n_er, seed, first + b0,
+                    count - b0 < per ? count - b0 : per, buf + 2 * b0, 0};
+    jb[t] = x;
+    pthread_create(&th[t], NULL, stream_gen, &jb[t]);
+    ++started;
+  }
+  for (int t = 0; t < started; ++t) {
+    pthread_join(th[t], NULL);
+    *sum += jb[t].sum;
+  }
+}
+
+typedef struct {
+  int kind;
+  u32 scale;
+  double a, b, c;
+  u64 n_er, seed, first, count;
+  int nt;
+  u32* buf;
+  u64* sum;
+} fill_job;
+
+static void* fill_thread(void* p) {
+  fill_job* f = (fill_job*)p;
+  stream_fill(f->kind, f->scale, f->a, f->b, f->c, f->n_er, f->seed, f->first, f->count, f->nt,
+              f->buf, f->sum);
+  return NULL;
+}
+
+int oracle_cc_stream(int kind, u32 scale, double a, double b, double c, u64 n_er, u64 seed,
+                     u64 first, u64 count, int nthreads, u32* labels, u64* checksum,
+                     u64* components) {
+  const u64 n = kind == 0 ? (1ull << scale) : n_er;
+  if (n > 0xffffffffull || (kind == 0 && scale > 31)) return 1;
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > STREAM_MAXT) nthreads = STREAM_MAXT;
+  dsu d;
+  if (dsu_init(&d, n)) return 2;
+  u32* buf[2];
+  buf[0] = (u32*)malloc(STREAM_CHUNK * 2 * sizeof(u32));
+  buf[1] = (u32*)malloc(STREAM_CHUNK * 2 * sizeof(u32));
+  if (!buf[0] || !buf[1]) {
+    free(buf[0]);
+    free(buf[1]);
+    dsu_free(&d);
+    return 2;
+  }
+  u64 sum = 0;
+  const u64 nch = (count + STREAM_CHUNK - 1) / STREAM_CHUNK;
+  if (nch)
+    stream_fill(kind, scale, a, b, c, n_er, seed, first,
+                count < STREAM_CHUNK ? count : STREAM_CHUNK, nthreads, buf[0], &sum);
+  for (u64 k = 0; k < nch; ++k) {
+    const u64 off = k * STREAM_CHUNK;
+    const u64 cnt = count - off < STREAM_CHUNK ? count - off : STREAM_CHUNK;
+    pthread_t filler;
+    fill_job fj;
+    const int more = k + 1 < nch;
+    if (more) {
+      const u64 off2 = off + STREAM_CHUNK;
+      fill_job x = {kind, scale, a, b, c, n_er, seed, first + off2,
+                    count - off2 < STREAM_CHUNK ? count - off2 : STREAM_CHUNK, nthreads,
+                    buf[(k + 1) & 1], &sum};
+      fj = x;
+      pthread_create(&filler, NULL, fill_thread, &fj);
+    }
+    const u32* e = buf[k & 1];
+    for (u64 i = 0; i < cnt; ++i) dsu_unite(&d, e[2 * i], e[2 * i + 1]);
+    if (more) pthread_join(filler, NULL);
+  }
+  free(buf[0]);
+  free(buf[1]);
+  int r = oracle_finish(&d, n, NULL, labels);
+  dsu_free(&d);
+  if (r) return r;
+  u64 roots = 0;
+  for (u64 v = 0; v < n; ++v) roots += labels[v] == (u32)v;
+  if (checksum) *checksum = sum;
+  if (components) *components = roots;
+  return 0;
 }
 
 /* bfs_cc (oracle.hpp:67-108): BFS from each unvisited vertex ascending,

@@ -21,7 +21,7 @@ ALGOS = {"baseline": ALGO_BASELINE, "baseline-mj": ALGO_BASELINE_MJ,
          "atomic": ALGO_ATOMIC, "adaptive": ALGO_ADAPTIVE}
 FLAG_FULL_PASSES, FLAG_HOST_LOOP, FLAG_NO_GRAPH, FLAG_CHECK_STAR = 0x1, 0x2, 0x4, 0x8
 FLAG_HOOK_EVENTS = 0x10
-ABI_VERSION = 3  # HCC_ABI_VERSION of include/hookcc_c.h
+ABI_VERSION = 4  # HCC_ABI_VERSION of include/hookcc_c.h
 HOOK_KERNELS = {1: "k_hook_small", 2: "k_hook", 3: "k_hook_sum", 4: "k_hook_cas",
                 5: "k_hook_legacy"}
 PHASE_HOOK, PHASE_COMPRESS = 0, 1
@@ -47,7 +47,8 @@ class Metrics(C.Structure):
                 ("s", u64), ("segments_clamped", i32), ("outer_iterations", u64),
                 ("counters", Counters), ("components", u64), ("n", u64), ("m", u64),
                 ("passes", u64), ("edges_processed", u64), ("records", u64),
-                ("used_device_loop", i32), ("kernels", u64), ("star0_bitmap", i32)]
+                ("used_device_loop", i32), ("kernels", u64), ("star0_bitmap", i32),
+                ("wl_capacity", u64), ("wl_reruns", u32), ("reserved_m", u32)]
 
 
 class SegmentRec(C.Structure):
@@ -61,6 +62,13 @@ class SegmentRec(C.Structure):
 class GraphStats(C.Structure):
     _fields_ = [("n", u64), ("m_stored", u64), ("m_unique", u64), ("avg_degree", C.c_double),
                 ("max_degree", u64)]
+
+
+class ShardMetrics(C.Structure):
+    _fields_ = [("total_ms", C.c_double), ("local_ms", C.c_double), ("merge_ms", C.c_double),
+                ("span_ms", C.c_double), ("pairs_exported", u64), ("records_merged", u64),
+                ("rehook_passes", u64), ("bitmap_bytes", u64), ("device", i32),
+                ("peer_access", i32)]
 
 
 class HccError(RuntimeError):
@@ -117,6 +125,9 @@ _SIGS = {
     "hcc_rehook": (i32, [vp, vp, vp, vp, u64, C.POINTER(Metrics)]),
     "hcc_rehook_rows": (i32, [vp, vp, vp, u64, u64, u64, vp, u64, C.POINTER(Metrics)]),
     "hcc_graph_generate_range": (i32, [vp, C.c_char_p, u64, u64, u64, C.POINTER(vp)]),
+    "hcc_create_multi": (i32, [C.POINTER(i32), i32, C.POINTER(vp)]),
+    "hcc_ctx_shards": (i32, [vp, C.POINTER(i32)]),
+    "hcc_ctx_shard_metrics": (i32, [vp, vp, u64, C.POINTER(u64)]),
 }
 
 
@@ -158,11 +169,33 @@ def _ptr(a: np.ndarray) -> int:
 class Context:
     """hcc_ctx: one device, stream and scratch (per host thread)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, devices: list[int] | None = None):
+        """devices=[d0, d1, ...]: a multi-device context (hcc_create_multi),
+        one edge shard per entry (entries may repeat)."""
         h = vp()
-        check(lib().hcc_create(device, C.byref(h)))
+        if devices:
+            arr = (i32 * len(devices))(*devices)
+            check(lib().hcc_create_multi(arr, len(devices), C.byref(h)))
+            device = devices[0]
+        else:
+            check(lib().hcc_create(device, C.byref(h)))
         self.h = h
         self.device = device
+        self.devices = list(devices) if devices else [device]
+
+    @property
+    def shards(self) -> int:
+        out = i32()
+        check(lib().hcc_ctx_shards(self.h, C.byref(out)))
+        return out.value
+
+    def shard_metrics(self) -> list[dict]:
+        cnt = u64()
+        check(lib().hcc_ctx_shard_metrics(self.h, None, 0, C.byref(cnt)))
+        arr = (ShardMetrics * max(cnt.value, 1))()
+        check(lib().hcc_ctx_shard_metrics(self.h, C.cast(arr, vp), cnt.value, C.byref(cnt)))
+        return [{k: getattr(arr[i], k) for k, _ in ShardMetrics._fields_}
+                for i in range(cnt.value)]
 
     def close(self) -> None:
         if self.h:
@@ -312,7 +345,8 @@ def metrics_dict(mx: Metrics) -> dict:
                 components=mx.components, n=mx.n, m=mx.m, passes=mx.passes,
                 edges_processed=mx.edges_processed, records=mx.records,
                 used_device_loop=bool(mx.used_device_loop), kernels=mx.kernels,
-                star0_bitmap=bool(mx.star0_bitmap))
+                star0_bitmap=bool(mx.star0_bitmap), wl_capacity=mx.wl_capacity,
+                wl_reruns=mx.wl_reruns)
 
 
 class Graph:

@@ -120,22 +120,42 @@ int usable_devices() {
 // ---------------------------------------------------------------------------
 // handles
 
+// Per-shard state of a multi-device merge (hcc_create_multi).
+struct MergeShard {
+  u32* bits = nullptr;       // export bitmap, ceil(n/32) words
+  u64 bits_words = 0;
+  uint2* pairs = nullptr;    // export pairs
+  u64 cap = 0;
+  u64* cnt = nullptr;        // device: pairs the export produced
+  PeerTab* tab = nullptr;    // device: every shard's export buffers
+  bool tab_dirty = true;
+  cudaEvent_t ev_exp = nullptr, ev_t0 = nullptr, ev_m0 = nullptr, ev_t1 = nullptr;
+  hcc_forest* forest = nullptr;  // local forest (shard 0 may use the caller's)
+  double local_ms = 0, merge_ms = 0, total_ms = 0;
+  u64 passes = 0, records = 0, exported = 0;
+};
+
 struct GraphKey {
   int algo = -1;
   const void* edges = nullptr;
   const void* pi = nullptr;
   const void* wl0 = nullptr;
+  const void* wl1 = nullptr;
+  const void* s0b = nullptr;
+  const void* s0f = nullptr;
+  u64 wl_cap = 0;
   u64 n = 0, m = 0, nseg = 0, max_threads = 0;
   u32 flags = 0;
   int walk = 0;
   u64 plan = 0;
-  bool s0b = false;
+  bool s0b_on = false;
   bool sum = false;
   bool operator==(const GraphKey& o) const {
     return algo == o.algo && edges == o.edges && pi == o.pi && wl0 == o.wl0 &&
+           wl1 == o.wl1 && s0b == o.s0b && s0f == o.s0f && wl_cap == o.wl_cap &&
            n == o.n && m == o.m && nseg == o.nseg &&
            max_threads == o.max_threads && flags == o.flags && walk == o.walk &&
-           plan == o.plan && s0b == o.s0b && sum == o.sum;
+           plan == o.plan && s0b_on == o.s0b_on && sum == o.sum;
   }
 };
 
@@ -152,7 +172,7 @@ struct hcc_ctx {
   uint2* wl[2] = {nullptr, nullptr};
   u64 wl_cap = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  int occ_hook = 1, occ_vert = 1, occ_hook_sum = 1;
+  int occ_hook = 1, occ_vert = 1, occ_hook_sum = 1, occ_hook_cas = 1, occ_hook_sum_cas = 1;
   // cached executable graph for repeated calls with identical arguments,
   // plus the previous one (two graphs used alternately, e.g. a pipelined
   // upload into one while the other runs, keep both instantiated)
@@ -180,14 +200,22 @@ struct hcc_ctx {
   u64 s0b_words = 0;
   u32* s0f = nullptr;  // star-0 summary (one bit per group of bitmap words)
   u64 s0f_words = 0;
-  // multi-GPU
-  void* comm = nullptr;
-  int world = 1, rank = 0;
+  // a worklist overflowed once: size the lists to m from now on
+  bool wl_full = false;
+  // multi-device context (hcc_create_multi): one sub-context per edge
+  // shard (devices may repeat), merge buffers per shard
+  std::vector<hcc_ctx*> subs;
+  std::vector<MergeShard> merge;
+  int peer_access = 0;
 };
 
 struct hcc_graph {
   hcc_ctx* ctx = nullptr;
   u64 n = 0, m = 0;
+  u64 first = 0;  // global index of edge 0 (ranged / shard graphs)
+  // multi-device graph: shard r (partition_edges(m, shards)) on ctx->subs[r]
+  std::vector<hcc_graph*> shards;
+  std::vector<u64> bounds;
   uint2* d_edges = nullptr;
   bool has_stats = false;
   hcc_graph_stats stats{};
@@ -236,8 +264,14 @@ u64* thread_scratch(int dev, u64** host) {
   return t_scratch.d_res;
 }
 
+void drop_exec(hcc_ctx* c);
+
+// Every buffer an executable graph bakes into its kernel arguments (pi,
+// worklists, star bitmap and summary) is sized here; a reallocation drops
+// the cached graphs, whose arguments would otherwise point at freed memory.
 void ensure_pi(hcc_ctx* c, u64 n) {
   if (c->scratch_n >= n && c->scratch_pi) return;
+  drop_exec(c);
   if (c->scratch_pi) HCC_CUDA(cudaFree(c->scratch_pi));
   c->scratch_pi = nullptr;
   c->scratch_n = 0;
@@ -248,6 +282,7 @@ void ensure_pi(hcc_ctx* c, u64 n) {
 void ensure_wl(hcc_ctx* c, u64 cap) {
   cap = std::max<u64>(cap, 1024);
   if (c->wl_cap >= cap) return;
+  drop_exec(c);
   for (int i = 0; i < 2; ++i) {
     if (c->wl[i]) HCC_CUDA(cudaFree(c->wl[i]));
     c->wl[i] = nullptr;
@@ -259,6 +294,7 @@ void ensure_wl(hcc_ctx* c, u64 cap) {
 
 void ensure_s0b(hcc_ctx* c, u64 nwords) {
   if (c->s0b_words >= nwords) return;
+  drop_exec(c);
   if (c->s0b) HCC_CUDA(cudaFree(c->s0b));
   c->s0b = nullptr;
   c->s0b_words = 0;
@@ -268,6 +304,7 @@ void ensure_s0b(hcc_ctx* c, u64 nwords) {
 
 void ensure_s0f(hcc_ctx* c, u64 nwords) {
   if (c->s0f_words >= nwords) return;
+  drop_exec(c);
   if (c->s0f) HCC_CUDA(cudaFree(c->s0f));
   c->s0f = nullptr;
   c->s0f_words = 0;
@@ -400,6 +437,7 @@ struct Plan {
   u64 adapt_first = 0;      // ... or n >> kAdaptNShift if larger (edges)
   u32 forming_pct;          // store ratio (%) above which a segment is forming
   unsigned grid_hook, block_hook, grid_vert, block_vert;
+  unsigned grid_cas = 1;    // k_hook_cas grid (kHookCasCta threads per CTA)
 };
 
 HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
@@ -479,7 +517,7 @@ void launch_compress_s0b(hcc_ctx* c, const Plan& P, cudaStream_t s) {
 void launch_hook(const Plan& P, cudaStream_t s, const HookArgs& a) {
   if (a.chunked && (P.block_hook & 31u) == 0) {
     if (a.cas)
-      k_hook_cas<<<P.grid_hook, P.block_hook, 0, s>>>(a);
+      k_hook_cas<<<P.grid_cas, kHookCasCta, 0, s>>>(a);
     else
       k_hook<<<P.grid_hook, P.block_hook, 0, s>>>(a);
   } else {
@@ -489,11 +527,10 @@ void launch_hook(const Plan& P, cudaStream_t s, const HookArgs& a) {
 
 // The summary hook (one CTA per SM, the summary and queues in shared memory).
 void launch_hook_sum(hcc_ctx* c, cudaStream_t s, const HookArgs& a) {
-  const size_t smem = hook_smem(a, kHookSumCta);
   if (a.cas)
-    k_hook_sum_cas<<<c->sms * c->occ_hook_sum, kHookSumCta, smem, s>>>(a);
+    k_hook_sum_cas<<<c->sms * c->occ_hook_sum_cas, kHookCasCta, hook_smem(a, kHookCasCta), s>>>(a);
   else
-    k_hook_sum<<<c->sms * c->occ_hook_sum, kHookSumCta, smem, s>>>(a);
+    k_hook_sum<<<c->sms * c->occ_hook_sum, kHookSumCta, hook_smem(a, kHookSumCta), s>>>(a);
 }
 
 // Topology slot whose hook is voted between the summary and the plain
@@ -815,7 +852,61 @@ bool parse_u64(const std::string& s, u64* out) {
   return true;
 }
 
+// Worklist engine over re-hook records already in wl[0] (remote relations
+// of a multi-GPU merge): the block-append hook, since the list sizes are
+// exact (count + n), then Multi-Jump; host-stepped (a merge needs 1-3).
+Plan rehook_plan(hcc_ctx* c, u32* pi, u64 n) {
+  Plan P;
+  P.algo = HCC_ALGO_BASELINE_MJ;
+  P.full_passes = false;
+  P.n = n;
+  P.m = 0;
+  P.edges = nullptr;
+  P.pi = pi;
+  P.wl0 = c->wl[0];
+  P.wl1 = c->wl[1];
+  P.nseg = 1;
+  P.walk = kDefaultWalk;
+  P.s0b = false;
+  P.adapt = false;
+  P.adapt_shift = 0;
+  P.forming_pct = 0;
+  P.block_hook = kHookCta;
+  P.grid_hook = (unsigned)(c->sms * c->occ_hook);
+  P.block_vert = kVertThreads;
+  // grid-stride compress over a few CTAs per SM: after a merge the trees
+  // are stars plus a few remote links, and a pass that finds the forest
+  // clean exits at once (a full grid took 0.45 ms to do nothing at n = 2^28)
+  P.grid_vert = grid_for((n + 3) / 4, kVertThreads, (u64)c->sms * 16);
+  return P;
+}
+
+void rehook_loop(hcc_ctx* c, const Plan& P) {
+  Seq q;
+  q.c = c;
+  q.graph_mode = false;
+  q.streams.push_back(c->stream);
+  DevCtrl* ctrl = c->d_ctrl;
+  DevRec* recs = c->d_recs;
+  q.loop([&](cudaGraphConditionalHandle h, int u) {
+    launch_hook(P, q.s(), hook_args(c, P, kSrcWorklist, 1));
+    k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl, recs, 1);
+    k_step_worklist<<<1, 1, 0, q.s()>>>(ctrl, recs, h, u);
+  });
+}
+
 }  // namespace
+
+// Multi-device contexts (single process, one sub-context per edge shard;
+// implemented at the end of this file).
+static int multi_from_edges(hcc_ctx* c, const void* uv, bool wide, u64 m, u64 n,
+                            hcc_graph** out);
+static int multi_generate(hcc_ctx* c, const char* spec, u64 seed, u64 n, u64 first, u64 count,
+                          hcc_graph** out);
+static int multi_range_io(hcc_ctx* c, hcc_graph* g, uint32_t* uv, u64 first, u64 count, int op);
+static int multi_stats(hcc_ctx* c, const hcc_graph* g, hcc_graph_stats* out);
+static int multi_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o, hcc_forest* f,
+                    uint32_t* lab32, uint64_t* lab64, hcc_metrics* mx);
 
 // ===========================================================================
 // C-ABI
@@ -869,6 +960,11 @@ int hcc_create(int device, hcc_ctx** out) {
   HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_sum, kHookSumCta,
                                                           kHookSmemMax));
   c->occ_hook_sum = std::max(occ, 1);
+  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_sum_cas, kHookCasCta,
+                                                          kHookSmemMax));
+  c->occ_hook_sum_cas = std::max(occ, 1);
+  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_cas, kHookCasCta, 0));
+  c->occ_hook_cas = std::max(occ, 1);
 #if HCC_SMALL_CARVE >= 0
   HCC_CUDA(cudaFuncSetAttribute(k_hook_small, cudaFuncAttributePreferredSharedMemoryCarveout,
                                 HCC_SMALL_CARVE));
@@ -897,6 +993,18 @@ int hcc_create(int device, hcc_ctx** out) {
 
 int hcc_destroy(hcc_ctx* c) {
   if (!c) return HCC_OK;
+  for (size_t r = 0; r < c->merge.size(); ++r) {
+    MergeShard& ms = c->merge[r];
+    if (r < c->subs.size()) cudaSetDevice(c->subs[r]->dev);
+    if (ms.forest) hcc_forest_free(ms.forest);
+    cudaFree(ms.bits);
+    cudaFree(ms.pairs);
+    cudaFree(ms.cnt);
+    cudaFree(ms.tab);
+    for (cudaEvent_t ev : {ms.ev_exp, ms.ev_t0, ms.ev_m0, ms.ev_t1})
+      if (ev) cudaEventDestroy(ev);
+  }
+  for (hcc_ctx* sc : c->subs) hcc_destroy(sc);
   cudaSetDevice(c->dev);
   drop_exec(c);
   if (c->stream) cudaStreamSynchronize(c->stream);
@@ -954,6 +1062,7 @@ int hcc_graph_from_edges_u64(hcc_ctx* c, const uint64_t* uv, uint64_t m,
     return fail(HCC_EINVAL, "vertex count >= 2^32 is not supported by the "
                             "device forest (u32 ids)");
   if (m > 0 && !uv) return fail(HCC_EINVAL, "null edge buffer");
+  if (!c->subs.empty()) return multi_from_edges(c, uv, true, m, n, out);
   hcc_graph* g = new hcc_graph;
   g->ctx = c;
   g->n = n;
@@ -1004,6 +1113,7 @@ int hcc_graph_from_edges_u32(hcc_ctx* c, const uint32_t* uv, uint64_t m,
   if (int r = ctx_enter(c)) return r;
   if (n > kMaxN) return fail(HCC_EINVAL, "vertex count >= 2^32");
   if (m > 0 && !uv) return fail(HCC_EINVAL, "null edge buffer");
+  if (!c->subs.empty()) return multi_from_edges(c, uv, false, m, n, out);
   hcc_graph* g = new hcc_graph;
   g->ctx = c;
   g->n = n;
@@ -1044,9 +1154,14 @@ int hcc_graph_from_edges_u32(hcc_ctx* c, const uint32_t* uv, uint64_t m,
 // check (check_endpoints, graph.hpp:89-94).  Every entry point that reads a
 // graph's edges calls this first.
 static int graph_ready(const hcc_graph* g) {
+  if (g)
+    for (const hcc_graph* sh : g->shards)
+      if (int r = graph_ready(sh)) return r;
   if (!g || !g->pending) return HCC_OK;
-  HCC_CUDA(cudaEventSynchronize(g->up_ev));
+  const cudaError_t e = cudaEventSynchronize(g->up_ev);
   g->pending = false;
+  if (e != cudaSuccess)
+    return fail(HCC_ECUDA, std::string("graph upload: ") + cudaGetErrorString(e));
   if (*g->h_err) return fail(HCC_ERANGE, "edge endpoint out of range");
   return HCC_OK;
 }
@@ -1057,6 +1172,7 @@ int hcc_graph_upload_async(hcc_ctx* c, hcc_graph* g, const uint32_t* uv, uint64_
   if (first > g->m || count > g->m - first)
     return fail(HCC_EINVAL, "range out of bounds");
   if (int r = ctx_enter(c)) return r;
+  if (!g->shards.empty()) return multi_range_io(c, g, const_cast<uint32_t*>(uv), first, count, 0);
   if (int r = graph_ready(g)) return r;  // one upload in flight per graph
   HCC_GUARD_BEGIN
   if (!c->copy_stream) {
@@ -1123,6 +1239,22 @@ int hcc_graph_from_csr(hcc_ctx* c, const uint64_t* row_ptr, const uint32_t* col,
       return fail(HCC_EINVAL, "row_ptr must be non-decreasing");
   const u64 m = row_ptr[n];
   if (m > 0 && !col) return fail(HCC_EINVAL, "null col");
+  if (!c->subs.empty()) {
+    // sharded: expand on the host (row order), then partition the edge list
+    std::vector<u32> uv;
+    try {
+      uv.resize(2 * m);
+    } catch (const std::bad_alloc&) {
+      return fail(HCC_ENOMEM, "host allocation failed");
+    }
+    for (u64 u = 0; u < n; ++u)
+      for (u64 j = row_ptr[u]; j < row_ptr[u + 1]; ++j) {
+        if (col[j] >= n) return fail(HCC_ERANGE, "column index out of range");
+        uv[2 * j] = (u32)u;
+        uv[2 * j + 1] = col[j];
+      }
+    return multi_from_edges(c, uv.data(), false, m, n, out);
+  }
   hcc_graph* g = new hcc_graph;
   g->ctx = c;
   g->n = n;
@@ -1227,10 +1359,12 @@ static int generate_impl(hcc_ctx* c, const char* spec_c, uint64_t default_seed,
     first = 0;
     count = m;
   }
+  if (!c->subs.empty()) return multi_generate(c, spec_c, default_seed, n, first, count, out);
   hcc_graph* g = new hcc_graph;
   g->ctx = c;
   g->n = n;
   g->m = count;
+  g->first = first;
   HCC_GUARD_BEGIN
   HCC_CUDA(cudaMalloc(&g->d_edges, std::max<u64>(count, 2) * sizeof(uint2)));
   if (count > 0) {
@@ -1280,6 +1414,8 @@ int hcc_graph_download_u32(hcc_ctx* c, const hcc_graph* g, uint32_t* uv,
   if (first > g->m || count > g->m - first)
     return fail(HCC_EINVAL, "range out of bounds");
   if (int r = ctx_enter(c)) return r;
+  if (!g->shards.empty())
+    return multi_range_io(c, const_cast<hcc_graph*>(g), uv, first, count, 2);
   HCC_GUARD_BEGIN
   if (count)
     HCC_CUDA(cudaMemcpy(uv, g->d_edges + first, count * sizeof(uint2),
@@ -1292,13 +1428,23 @@ int hcc_graph_checksum(hcc_ctx* c, const hcc_graph* g, uint64_t* out) {
   if (int r = graph_ready(g)) return r;
   if (!g || !out) return fail(HCC_EINVAL, "null argument");
   if (int r = ctx_enter(c)) return r;
+  if (!g->shards.empty()) {  // position-keyed terms: the shard sums add up
+    u64 sum = 0;
+    for (size_t r = 0; r < g->shards.size(); ++r) {
+      uint64_t x = 0;
+      if (int e = hcc_graph_checksum(c->subs[r], g->shards[r], &x)) return e;
+      sum += x;
+    }
+    *out = sum;
+    return HCC_OK;
+  }
   u64* d = nullptr;
   HCC_GUARD_BEGIN
   HCC_CUDA(cudaMalloc(&d, sizeof(u64)));
   HCC_CUDA(cudaMemsetAsync(d, 0, sizeof(u64), c->stream));
   if (g->m)
     k_checksum<<<grid_for(g->m, 256, (u64)c->sms * 16), 256, 0, c->stream>>>(
-        g->d_edges, g->m, d);
+        g->d_edges, g->m, g->first, d);
   HCC_CUDA(cudaGetLastError());
   HCC_CUDA(cudaMemcpyAsync(out, d, sizeof(u64), cudaMemcpyDeviceToHost,
                            c->stream));
@@ -1318,6 +1464,10 @@ int hcc_graph_compute_stats(hcc_ctx* c, const hcc_graph* g_c,
   if (!g_c || !out) return fail(HCC_EINVAL, "null argument");
   if (int r = ctx_enter(c)) return r;
   hcc_graph* g = const_cast<hcc_graph*>(g_c);
+  if (!g->shards.empty() && !g->has_stats) {
+    if (int r = multi_stats(c, g, &g->stats)) return r;
+    g->has_stats = true;
+  }
   HCC_GUARD_BEGIN
   if (!g->has_stats)
     if (int r = compute_stats_dev(c, g)) return r;
@@ -1328,6 +1478,11 @@ int hcc_graph_compute_stats(hcc_ctx* c, const hcc_graph* g_c,
 
 int hcc_graph_free(hcc_graph* g) {
   if (!g) return HCC_OK;
+  if (!g->shards.empty()) {
+    for (hcc_graph* sh : g->shards) hcc_graph_free(sh);
+    delete g;
+    return HCC_OK;
+  }
   if (g->ctx) {
     cudaSetDevice(g->ctx->dev);
     // the cached executable graph may reference these edges
@@ -1389,9 +1544,29 @@ static std::vector<u64> geometric_bounds(u64 m) {
   return b;
 }
 
+// run_cc's internal "worklist overflowed, repeat" code (never returned).
+constexpr int kRerun = -1;
+
+static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
+                  hcc_forest* f, hcc_metrics* mx);
+
+// run_cc, repeated once with m-sized worklists after an overflow.
+static int run_cc_sized(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o, hcc_forest* f,
+                        hcc_metrics* mx) {
+  int r = run_cc(c, g, o, f, mx);
+  if (r == kRerun) {
+    r = run_cc(c, g, o, f, mx);
+    if (mx) mx->wl_reruns = 1;
+    if (r == kRerun) r = fail(HCC_ECUDA, "worklist capacity exceeded");
+  }
+  return r;
+}
+
 static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
                   hcc_forest* f, hcc_metrics* mx) {
   if (int r = graph_ready(g)) return r;
+  if (!g->shards.empty())
+    return fail(HCC_EINVAL, "sharded graph: run it on its multi-device context");
   const hcc_opts defaults = {HCC_ALGO_BASELINE_MJ, 0, 0, 0, 0, nullptr, nullptr};
   if (!o) o = &defaults;
   if (o->algo < HCC_ALGO_BASELINE || o->algo > HCC_ALGO_ADAPTIVE)
@@ -1498,7 +1673,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   }
   const bool uses_wl =
       o->algo == HCC_ALGO_BASELINE_MJ && !(o->flags & HCC_FLAG_FULL_PASSES);
-  if (uses_wl) ensure_wl(c, m);
+  if (uses_wl && o->max_threads != 0) ensure_wl(c, m);  // exact block appends
   bool s0b = uses_wl && o->max_threads == 0 && n >= (1ull << 16);
   if (const char* e = std::getenv("HCC_S0B")) s0b = s0b && std::atoi(e) != 0;
 
@@ -1548,6 +1723,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   if (o->max_threads == 0) {
     P.block_hook = kHookCta;
     P.grid_hook = (unsigned)(c->sms * c->occ_hook);
+    P.grid_cas = (unsigned)(c->sms * c->occ_hook_cas);
     P.block_vert = kVertThreads;
     // k_compress / k_init_pi take four vertices per thread.  The grid covers
     // n exactly: blocks start in ascending order and a new block starts as
@@ -1569,10 +1745,22 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
     // no-op records: room for all launches appending to one list (the
     // unrolled slots; the looped-segment path keeps exact block appends)
     P.chunked = true;
-    const u64 warps = std::max<u64>((u64)P.grid_hook * (P.block_hook / 32),
-                                    (u64)c->sms * c->occ_hook_sum * (kHookSumCta / 32));
+    const u64 warps = std::max<u64>(
+        std::max<u64>((u64)P.grid_hook * (P.block_hook / 32),
+                      (u64)c->sms * c->occ_hook_sum * (kHookSumCta / 32)),
+        std::max<u64>((u64)P.grid_cas * (kHookCasCta / 32),
+                      (u64)c->sms * c->occ_hook_sum_cas * (kHookCasCta / 32)));
     const u64 launches = (P.nseg <= kMaxUnrolledSegments ? P.nseg : 0) + 2;
-    ensure_wl(c, m + launches * warps * kWlChunk);
+    // Records: every store of the topology slots plus deferred walks, all
+    // slots into one list.  Stores link distinct roots up to benign races,
+    // so ~n at most (grid 4096^2: 16.7 M of 33.5 M edges; RMAT-24: 9.1 M of
+    // 268 M).  max(m/8, 2n) keeps RMAT-28 at 2 x 4.3 GB instead of 2 x 34
+    // GB; an overflow is caught on the device (err bit 4) and the run is
+    // repeated with m-sized lists (wl_full).  HCC_WL_DIV overrides the 8.
+    u64 div = 8;
+    if (const char* e = std::getenv("HCC_WL_DIV")) div = std::max<u64>(1, std::strtoull(e, nullptr, 10));
+    const u64 recs_cap = c->wl_full ? m : std::min<u64>(m, std::max<u64>(m / div, div > 8 ? 0 : 2 * n));
+    ensure_wl(c, recs_cap + launches * warps * kWlChunk);
     P.wl0 = c->wl[0];
     P.wl1 = c->wl[1];
   }
@@ -1607,13 +1795,17 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   key.edges = g->d_edges;
   key.pi = pi;
   key.wl0 = P.wl0;
+  key.wl1 = P.wl1;
+  key.s0b = c->s0b;
+  key.s0f = c->s0f;
+  key.wl_cap = c->wl_cap;
   key.n = n;
   key.m = m;
   key.nseg = nseg;
   key.max_threads = o->max_threads;
   key.flags = o->flags;
   key.walk = P.walk;
-  key.s0b = P.s0b;
+  key.s0b_on = P.s0b;
   key.sum = P.sum;
   key.plan = key.plan * 7 + (P.small_slots ? 1 : 0);
   key.plan = key.plan * 131 + (u64)P.walk_last;
@@ -1779,6 +1971,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
     }
     out.kernels = k;
   }
+  out.wl_capacity = uses_wl ? c->wl_cap : 0;
   if (o->algo == HCC_ALGO_BASELINE_MJ && !P.full_passes)
     out.outer_iterations = 1 + (nrec > nseg ? nrec - nseg : 0);
   else if (o->algo == HCC_ALGO_ADAPTIVE || o->algo == HCC_ALGO_ATOMIC)
@@ -1788,8 +1981,13 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   if (mx) *mx = out;
   if (hc.err & 2u)
     return fail(HCC_ECUDA, "device loop exceeded its step cap (runaway loop)");
-  if (hc.err & 4u)
-    return fail(HCC_ECUDA, "worklist capacity exceeded (chunked appends)");
+  if (hc.err & 4u) {
+    if (!c->wl_full) {
+      c->wl_full = true;  // hcc_cc repeats the run with m-sized worklists
+      return kRerun;
+    }
+    return fail(HCC_ECUDA, "worklist capacity exceeded");
+  }
   if ((o->flags & HCC_FLAG_CHECK_STAR) && hc.flag)
     return fail(HCC_ENOTSTAR, "extract_labels: forest is not star-shaped");
   return HCC_OK;
@@ -1800,7 +1998,8 @@ int hcc_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o, hcc_forest* f,
            uint32_t* labels_out, hcc_metrics* mx) {
   if (!g) return fail(HCC_EINVAL, "null graph");
   if (int r = ctx_enter(c)) return r;
-  if (int r = run_cc(c, g, o, f, mx)) return r;
+  if (!c->subs.empty()) return multi_cc(c, g, o, f, labels_out, nullptr, mx);
+  if (int r = run_cc_sized(c, g, o, f, mx)) return r;
   if (labels_out && g->n) {
     const u32* pi = f ? f->d_pi : c->scratch_pi;
     HCC_GUARD_BEGIN
@@ -1815,7 +2014,8 @@ int hcc_cc_u64(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
                hcc_forest* f, uint64_t* labels_out, hcc_metrics* mx) {
   if (!g) return fail(HCC_EINVAL, "null graph");
   if (int r = ctx_enter(c)) return r;
-  if (int r = run_cc(c, g, o, f, mx)) return r;
+  if (!c->subs.empty()) return multi_cc(c, g, o, f, nullptr, labels_out, mx);
+  if (int r = run_cc_sized(c, g, o, f, mx)) return r;
   if (labels_out && g->n) {
     const u32* pi = f ? f->d_pi : c->scratch_pi;
     HCC_GUARD_BEGIN
@@ -2074,6 +2274,20 @@ int hcc_forest_verify(hcc_ctx* c, const hcc_graph* g, hcc_forest* f,
   if (!g || !f || !bad_edges || !bad_vertices) return fail(HCC_EINVAL, "null argument");
   if (f->n != g->n) return fail(HCC_EINVAL, "forest size does not match the graph");
   if (int r = ctx_enter(c)) return r;
+  if (!g->shards.empty()) {
+    // each shard's edges on its own device against f (peer reads); the
+    // vertex check once
+    u64 be = 0, bv = 0;
+    for (size_t r = 0; r < g->shards.size(); ++r) {
+      uint64_t e = 0, v = 0;
+      if (int st = hcc_forest_verify(c->subs[r], g->shards[r], f, &e, &v)) return st;
+      be += e;
+      if (r == 0) bv = v;
+    }
+    *bad_edges = be;
+    *bad_vertices = bv;
+    return HCC_OK;
+  }
   HCC_GUARD_BEGIN
   u64* d = reinterpret_cast<u64*>(&c->d_ctrl->wl_count[0]);  // two u64 scratch slots
   HCC_CUDA(cudaMemsetAsync(d, 0, 2 * sizeof(u64), c->stream));
@@ -2192,25 +2406,7 @@ int hcc_rehook_rows(hcc_ctx* c, hcc_forest* f, const uint32_t* dev_bit_rows, uin
   HCC_GUARD_BEGIN
   const u64 n = f->n;
   ensure_wl(c, count + n + 1);
-  Plan P;
-  P.algo = HCC_ALGO_BASELINE_MJ;
-  P.full_passes = false;
-  P.n = n;
-  P.m = 0;
-  P.edges = nullptr;
-  P.pi = f->d_pi;
-  P.wl0 = c->wl[0];
-  P.wl1 = c->wl[1];
-  P.nseg = 1;
-  P.walk = kDefaultWalk;
-  P.s0b = false;
-  P.block_hook = kHookCta;
-  P.grid_hook = (unsigned)(c->sms * c->occ_hook);
-  P.block_vert = kVertThreads;
-  // grid-stride compress over a few CTAs per SM: after a merge the trees
-  // are stars plus a few remote links, and a pass that finds the forest
-  // clean exits at once (a full grid took 0.45 ms to do nothing at n = 2^28)
-  P.grid_vert = grid_for((n + 3) / 4, kVertThreads, (u64)c->sms * 16);
+  const Plan P = rehook_plan(c, f->d_pi, n);
   HCC_CUDA(cudaEventRecord(c->ev0, c->stream));
   k_begin<<<1, 1, 0, c->stream>>>(c->d_ctrl, c->d_recs, 1);
   u64* d_cnt = reinterpret_cast<u64*>(&c->d_ctrl->wl_count[0]);
@@ -2226,17 +2422,7 @@ int hcc_rehook_rows(hcc_ctx* c, hcc_forest* f, const uint32_t* dev_bit_rows, uin
                     c->stream>>>(dev_bit_rows, nrows, row_stride_words, skip_row, f->d_pi, n,
                                  c->wl[0], d_cnt);
   HCC_CUDA(cudaGetLastError());
-  Seq q;
-  q.c = c;
-  q.graph_mode = false;
-  q.streams.push_back(c->stream);
-  DevCtrl* ctrl = c->d_ctrl;
-  DevRec* recs = c->d_recs;
-  q.loop([&](cudaGraphConditionalHandle h, int u) {
-    launch_hook(P, q.s(), hook_args(c, P, kSrcWorklist, 1));
-    k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl, recs, 1);
-    k_step_worklist<<<1, 1, 0, q.s()>>>(ctrl, recs, h, u);
-  });
+  rehook_loop(c, P);
   HCC_CUDA(cudaEventRecord(c->ev1, c->stream));
   HCC_CUDA(cudaEventSynchronize(c->ev1));
   float ms = 0.f;
@@ -2250,6 +2436,478 @@ int hcc_rehook_rows(hcc_ctx* c, hcc_forest* f, const uint32_t* dev_bit_rows, uin
   if (mx) *mx = out;
   return HCC_OK;
   HCC_GUARD_END
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Multi-device contexts: edge-partitioned CC in one process (north-star (5),
+// SURVEY.md §8e).  hcc_create_multi(devices, ndev) builds one sub-context
+// per shard (a device may appear several times: several shards share it).
+// Graphs created on such a context are split by partition_edges(m, ndev)
+// (engines.hpp:43-58), shard r on subs[r].  hcc_cc on it:
+//   1. local CC    every shard runs the single-GPU engine (its own stream,
+//                  one host thread per shard) into a full-size local forest,
+//                  then exports it (k_export: bitmap of pi(v) == 0 plus
+//                  sparse (v, pi(v)) pairs) into its merge buffers;
+//   2. merge       every shard waits on the others' export events (device
+//                  waits, cross-device) and runs k_merge_gather, which reads
+//                  the peers' export buffers straight over NVLink (P2P) and
+//                  appends the relations its own forest lacks to its
+//                  worklist; the worklist engine re-hooks them;
+//   3. labels      every shard now holds the global min-canonical forest;
+//                  shard 0's is returned.
+// A pair list that overflowed its buffer (the count is read on the device,
+// the host checks it after the round) grows the buffer and repeats steps
+// 1b-2: the relations already merged are true ones, so a repeat is exact.
+
+#include <condition_variable>
+#include <thread>
+
+namespace {
+
+// fn(r) on one host thread per shard; the first failure's message is moved
+// to the calling thread (g_err is thread-local).
+int for_shards(int G, const std::function<int(int)>& fn) {
+  std::vector<int> rc(G, 0);
+  std::vector<std::string> msg(G);
+  std::vector<std::thread> th;
+  th.reserve(G);
+  for (int r = 0; r < G; ++r)
+    th.emplace_back([&, r] {
+      try {
+        rc[r] = fn(r);
+      } catch (const CudaFail& f) {
+        rc[r] = f.code;
+      } catch (const std::bad_alloc&) {
+        rc[r] = fail(HCC_ENOMEM, "host allocation failed");
+      } catch (const std::exception& e) {
+        rc[r] = fail(HCC_ECUDA, e.what());
+      }
+      if (rc[r]) msg[r] = g_err;
+    });
+  for (std::thread& t : th) t.join();
+  for (int r = 0; r < G; ++r)
+    if (rc[r]) {
+      g_err = msg[r];
+      return rc[r];
+    }
+  return HCC_OK;
+}
+
+// Merge buffers of every shard for n vertices and pair capacity >= cap.
+void ensure_merge(hcc_ctx* c, u64 n, u64 cap) {
+  const int G = (int)c->subs.size();
+  if ((int)c->merge.size() != G) c->merge.resize(G);
+  const u64 nwords = (n + 31) / 32;
+  bool dirty = false;
+  for (int r = 0; r < G; ++r) {
+    MergeShard& ms = c->merge[r];
+    hcc_ctx* sc = c->subs[r];
+    HCC_CUDA(cudaSetDevice(sc->dev));
+    if (!ms.cnt) {
+      HCC_CUDA(cudaMalloc(&ms.cnt, sizeof(u64)));
+      HCC_CUDA(cudaMalloc(&ms.tab, sizeof(PeerTab)));
+      HCC_CUDA(cudaEventCreateWithFlags(&ms.ev_exp, cudaEventDisableTiming));
+      HCC_CUDA(cudaEventCreate(&ms.ev_t0));
+      HCC_CUDA(cudaEventCreate(&ms.ev_m0));
+      HCC_CUDA(cudaEventCreate(&ms.ev_t1));
+      dirty = true;
+    }
+    if (ms.bits_words < nwords) {
+      cudaFree(ms.bits);
+      ms.bits = nullptr;
+      HCC_CUDA(cudaMalloc(&ms.bits, std::max<u64>(nwords, 1) * sizeof(u32)));
+      ms.bits_words = nwords;
+      dirty = true;
+    }
+    if (ms.cap < cap) {
+      cudaFree(ms.pairs);
+      ms.pairs = nullptr;
+      ms.cap = 0;
+      HCC_CUDA(cudaMalloc(&ms.pairs, cap * sizeof(uint2)));
+      ms.cap = cap;
+      dirty = true;
+    }
+  }
+  if (!dirty) return;
+  PeerTab t{};
+  t.npeers = (u32)G;
+  for (int r = 0; r < G; ++r) {
+    t.bits[r] = c->merge[r].bits;
+    t.pairs[r] = c->merge[r].pairs;
+    t.count[r] = c->merge[r].cnt;
+    t.cap[r] = c->merge[r].cap;
+  }
+  for (int r = 0; r < G; ++r) {
+    HCC_CUDA(cudaSetDevice(c->subs[r]->dev));
+    HCC_CUDA(cudaMemcpy(c->merge[r].tab, &t, sizeof(PeerTab), cudaMemcpyHostToDevice));
+  }
+  HCC_CUDA(cudaSetDevice(c->dev));
+}
+
+// Shard r: export its forest into its merge buffers (stream-ordered after
+// its local CC) and record the export event the peers wait on.
+void enqueue_export(hcc_ctx* sc, MergeShard& ms, const hcc_forest* f) {
+  HCC_CUDA(cudaMemsetAsync(ms.cnt, 0, sizeof(u64), sc->stream));
+  const u64 nwords = (f->n + 31) / 32;
+  if (f->n)
+    k_export<<<grid_for(nwords * 32, 256, (u64)sc->sms * 32), 256, 0, sc->stream>>>(
+        f->d_pi, f->n, ms.bits, ms.pairs, ms.cap, ms.cnt);
+  HCC_CUDA(cudaGetLastError());
+  HCC_CUDA(cudaEventRecord(ms.ev_exp, sc->stream));
+}
+
+// Shard r: wait for every peer's export, gather the remote relations over
+// NVLink into the worklist, re-hook until convergence.
+void merge_shard(hcc_ctx* c, int r, hcc_forest* f, u64 records_cap) {
+  hcc_ctx* sc = c->subs[r];
+  MergeShard& ms = c->merge[r];
+  const int G = (int)c->subs.size();
+  const u64 n = f->n;
+  for (int s = 0; s < G; ++s)
+    if (s != r) HCC_CUDA(cudaStreamWaitEvent(sc->stream, c->merge[s].ev_exp, 0));
+  ensure_wl(sc, records_cap);
+  const Plan P = rehook_plan(sc, f->d_pi, n);
+  HCC_CUDA(cudaEventRecord(ms.ev_m0, sc->stream));
+  k_begin<<<1, 1, 0, sc->stream>>>(sc->d_ctrl, sc->d_recs, 1);
+  k_merge_gather<<<std::max<unsigned>(1u, (unsigned)sc->sms * 8u), 256, 0, sc->stream>>>(
+      ms.tab, (u32)r, f->d_pi, n, sc->wl[0], &sc->d_ctrl->wl_count[0], sc->wl_cap,
+      &sc->d_ctrl->err);
+  HCC_CUDA(cudaGetLastError());
+  rehook_loop(sc, P);
+  if (r == 0)
+    k_count_roots<<<grid_for(n, 256, (u64)sc->sms * 16), 256, 0, sc->stream>>>(f->d_pi, n,
+                                                                              sc->d_ctrl);
+  HCC_CUDA(cudaGetLastError());
+  HCC_CUDA(cudaEventRecord(ms.ev_t1, sc->stream));
+  HCC_CUDA(cudaMemcpyAsync(sc->h_ctrl, sc->d_ctrl, sizeof(DevCtrl), cudaMemcpyDeviceToHost,
+                           sc->stream));
+  HCC_CUDA(cudaMemcpyAsync(sc->h_recs, sc->d_recs, sizeof(DevRec), cudaMemcpyDeviceToHost,
+                           sc->stream));
+  HCC_CUDA(cudaStreamSynchronize(sc->stream));
+  if (sc->h_ctrl->err & 4u) throw CudaFail{fail(HCC_ECUDA, "merge worklist overflow")};
+  float ms_merge = 0.f, ms_total = 0.f;
+  HCC_CUDA(cudaEventElapsedTime(&ms_merge, ms.ev_m0, ms.ev_t1));
+  HCC_CUDA(cudaEventElapsedTime(&ms_total, ms.ev_t0, ms.ev_t1));
+  ms.merge_ms += ms_merge;
+  ms.total_ms = ms_total;
+  ms.passes += sc->h_ctrl->passes;
+  ms.records += sc->h_recs[0].edges_in;
+}
+
+}  // namespace
+
+static int multi_from_edges(hcc_ctx* c, const void* uv, bool wide, u64 m, u64 n,
+                            hcc_graph** out) {
+  const int G = (int)c->subs.size();
+  hcc_graph* g = new hcc_graph;
+  g->ctx = c;
+  g->n = n;
+  g->m = m;
+  g->bounds = uniform_bounds(m, (u64)G);
+  g->shards.assign(G, nullptr);
+  const int rc = for_shards(G, [&](int r) -> int {
+    const u64 b = g->bounds[r], k = g->bounds[r + 1] - b;
+    const int st = wide ? hcc_graph_from_edges_u64(c->subs[r], static_cast<const uint64_t*>(uv) + 2 * b,
+                                                   k, n, &g->shards[r])
+                        : hcc_graph_from_edges_u32(c->subs[r], static_cast<const uint32_t*>(uv) + 2 * b,
+                                                   k, n, &g->shards[r]);
+    if (!st) g->shards[r]->first = b;
+    return st;
+  });
+  if (rc) {
+    for (hcc_graph*& sh : g->shards)
+      if (!sh) sh = new hcc_graph;  // placeholders so free() sees a sharded graph
+    hcc_graph_free(g);
+    return rc;
+  }
+  *out = g;
+  return HCC_OK;
+}
+
+static int multi_generate(hcc_ctx* c, const char* spec, u64 seed, u64 n, u64 first, u64 count,
+                          hcc_graph** out) {
+  const int G = (int)c->subs.size();
+  hcc_graph* g = new hcc_graph;
+  g->ctx = c;
+  g->n = n;
+  g->m = count;
+  g->first = first;
+  g->bounds = uniform_bounds(count, (u64)G);
+  g->shards.assign(G, nullptr);
+  const int rc = for_shards(G, [&](int r) -> int {
+    const u64 b = g->bounds[r], k = g->bounds[r + 1] - b;
+    return hcc_graph_generate_range(c->subs[r], spec, seed, first + b, k, &g->shards[r]);
+  });
+  if (rc) {
+    for (hcc_graph*& sh : g->shards)
+      if (!sh) sh = new hcc_graph;
+    hcc_graph_free(g);
+    return rc;
+  }
+  *out = g;
+  return HCC_OK;
+}
+
+// op 0: asynchronous upload, 1: synchronous assign, 2: download.  The range
+// [first, first+count) is split at the shard boundaries.
+static int multi_range_io(hcc_ctx* c, hcc_graph* g, uint32_t* uv, u64 first, u64 count, int op) {
+  for (size_t r = 0; r < g->shards.size(); ++r) {
+    const u64 b = std::max(first, g->bounds[r]);
+    const u64 e = std::min(first + count, g->bounds[r + 1]);
+    if (b >= e) continue;
+    uint32_t* src = uv + 2 * (b - first);
+    const u64 lo = b - g->bounds[r];
+    int st;
+    if (op == 2)
+      st = hcc_graph_download_u32(c->subs[r], g->shards[r], src, lo, e - b);
+    else
+      st = hcc_graph_upload_async(c->subs[r], g->shards[r], src, lo, e - b);
+    if (st) return st;
+  }
+  g->has_stats = false;
+  if (op == 1) return graph_ready(g);
+  return HCC_OK;
+}
+
+// compute_stats of a sharded graph: the shards are copied (peer copies)
+// into one temporary graph on the first device.  Off the hot path.
+static int multi_stats(hcc_ctx* c, const hcc_graph* g, hcc_graph_stats* out) {
+  if (int r = graph_ready(g)) return r;
+  hcc_graph tmp;
+  tmp.ctx = c;
+  tmp.n = g->n;
+  tmp.m = g->m;
+  int rc = HCC_OK;
+  try {
+    HCC_CUDA(cudaSetDevice(c->dev));
+    HCC_CUDA(cudaMalloc(&tmp.d_edges, std::max<u64>(g->m, 2) * sizeof(uint2)));
+    for (size_t r = 0; r < g->shards.size(); ++r)
+      if (g->shards[r]->m)
+        HCC_CUDA(cudaMemcpyPeer(tmp.d_edges + g->bounds[r], c->dev, g->shards[r]->d_edges,
+                                c->subs[r]->dev, g->shards[r]->m * sizeof(uint2)));
+    rc = compute_stats_dev(c, &tmp);
+    if (!rc) *out = tmp.stats;
+  } catch (const CudaFail& f) {
+    rc = f.code;
+  }
+  cudaFree(tmp.d_edges);
+  tmp.d_edges = nullptr;
+  return rc;
+}
+
+static int multi_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o_in, hcc_forest* f,
+                    uint32_t* lab32, uint64_t* lab64, hcc_metrics* mx) {
+  const int G = (int)c->subs.size();
+  if ((int)g->shards.size() != G || g->ctx != c)
+    return fail(HCC_EINVAL, "graph was not created on this multi-device context");
+  if (int r = graph_ready(g)) return r;
+  hcc_opts o = {HCC_ALGO_BASELINE_MJ, 0, 0, 0, 0, nullptr, nullptr};
+  if (o_in) o = *o_in;
+  if (o.algo < HCC_ALGO_BASELINE || o.algo > HCC_ALGO_ADAPTIVE)
+    return fail(HCC_EINVAL, "unknown algorithm");
+  if (o.observer)
+    return fail(HCC_EINVAL, "phase observers need a single-device context");
+  const u64 n = g->n;
+  if (f && f->n != n) return fail(HCC_EINVAL, "forest size does not match the graph");
+  if (f && f->dev != c->subs[0]->dev)
+    return fail(HCC_EINVAL, "the forest must live on the first device of the context");
+  hcc_metrics out{};
+  out.n = n;
+  out.m = g->m;
+  if (o.algo == HCC_ALGO_ADAPTIVE && o.segments == 0) {
+    // s from the WHOLE graph's stats (engines.hpp:245-247), not per shard
+    hcc_graph_stats st;
+    if (int r = hcc_graph_compute_stats(c, g, &st)) return r;
+    o.segments = hcc_choose_segment_count(&st);
+  }
+  if (n == 0) {
+    if (mx) *mx = out;
+    return HCC_OK;
+  }
+  u64 cap = 0;
+  try {
+    cap = c->merge.empty() ? 0 : c->merge[0].cap;
+    if (cap == 0) cap = std::max<u64>(1ull << 16, n / 64);
+    ensure_merge(c, n, cap);
+    for (int r = 0; r < G; ++r) {
+      MergeShard& ms = c->merge[r];
+      if (!(r == 0 && f) && (!ms.forest || ms.forest->n != n)) {
+        if (ms.forest) hcc_forest_free(ms.forest);
+        ms.forest = nullptr;
+        if (int st = hcc_forest_create(c->subs[r], n, &ms.forest)) return st;
+      }
+      ms.local_ms = ms.merge_ms = ms.total_ms = 0;
+      ms.passes = ms.records = ms.exported = 0;
+    }
+  } catch (const CudaFail& fl) {
+    return fl.code;
+  }
+  auto forest_of = [&](int r) { return (r == 0 && f) ? f : c->merge[r].forest; };
+  std::vector<hcc_metrics> lm(G);
+  // 1. local CC + export
+  int rc = for_shards(G, [&](int r) -> int {
+    hcc_ctx* sc = c->subs[r];
+    MergeShard& ms = c->merge[r];
+    HCC_CUDA(cudaSetDevice(sc->dev));
+    HCC_CUDA(cudaEventRecord(ms.ev_t0, sc->stream));
+    if (int st = run_cc_sized(sc, g->shards[r], &o, forest_of(r), &lm[r])) return st;
+    ms.local_ms = lm[r].total_ms;
+    enqueue_export(sc, ms, forest_of(r));
+    return HCC_OK;
+  });
+  // 2. merge; repeated (export + merge) while some pair list overflowed
+  for (int attempt = 0; !rc; ++attempt) {
+    u64 pairs_total = 0;
+    for (int r = 0; r < G; ++r) pairs_total += c->merge[r].cap;
+    rc = for_shards(G, [&](int r) -> int {
+      HCC_CUDA(cudaSetDevice(c->subs[r]->dev));
+      merge_shard(c, r, forest_of(r), n + pairs_total + 1);
+      return HCC_OK;
+    });
+    if (rc) break;
+    u64 need = 0;
+    try {
+      for (int r = 0; r < G; ++r) {
+        HCC_CUDA(cudaSetDevice(c->subs[r]->dev));
+        u64 k = 0;
+        HCC_CUDA(cudaMemcpy(&k, c->merge[r].cnt, sizeof(u64), cudaMemcpyDeviceToHost));
+        c->merge[r].exported = k;
+        need = std::max(need, k);
+      }
+      if (need <= c->merge[0].cap) break;
+      if (attempt >= 2) {
+        rc = fail(HCC_ECUDA, "merge pair buffers kept overflowing");
+        break;
+      }
+      ensure_merge(c, n, need + need / 8);
+    } catch (const CudaFail& fl) {
+      rc = fl.code;
+      break;
+    }
+    rc = for_shards(G, [&](int r) -> int {
+      HCC_CUDA(cudaSetDevice(c->subs[r]->dev));
+      HCC_CUDA(cudaEventRecord(c->merge[r].ev_t0, c->subs[r]->stream));
+      enqueue_export(c->subs[r], c->merge[r], forest_of(r));
+      return HCC_OK;
+    });
+  }
+  cudaSetDevice(c->dev);
+  if (rc) return rc;
+  // metrics: device time of the slowest shard (max over shards)
+  for (int r = 0; r < G; ++r) {
+    const hcc_metrics& l = lm[r];
+    const MergeShard& ms = c->merge[r];
+    out.total_ms = std::max(out.total_ms, ms.local_ms + ms.merge_ms);
+    out.hook_ms = std::max(out.hook_ms, l.hook_ms);
+    out.compress_ms = std::max(out.compress_ms, l.compress_ms);
+    out.outer_iterations = std::max(out.outer_iterations, l.outer_iterations);
+    out.counters.hook_traversal_steps += l.counters.hook_traversal_steps;
+    out.counters.cas_failures += l.counters.cas_failures;
+    out.counters.jump_steps += l.counters.jump_steps;
+    out.passes += l.passes + ms.passes;
+    out.edges_processed += l.edges_processed + ms.records;
+    out.kernels += l.kernels + 3 + 3 * ms.passes;
+    out.wl_reruns |= l.wl_reruns;
+  }
+  out.s = lm[0].s;
+  out.segments_clamped = lm[0].segments_clamped;
+  out.used_device_loop = lm[0].used_device_loop;
+  out.star0_bitmap = lm[0].star0_bitmap;
+  out.wl_capacity = lm[0].wl_capacity;
+  out.components = c->subs[0]->h_ctrl->components;
+  out.records = G;
+  if (mx) *mx = out;
+  if (lab32 || lab64) {
+    const hcc_forest* f0 = forest_of(0);
+    HCC_GUARD_BEGIN
+    HCC_CUDA(cudaSetDevice(c->subs[0]->dev));
+    if (lab32) {
+      HCC_CUDA(cudaMemcpy(lab32, f0->d_pi, n * sizeof(u32), cudaMemcpyDeviceToHost));
+    } else {
+      uint32_t* tmp = reinterpret_cast<uint32_t*>(lab64) + n;
+      HCC_CUDA(cudaMemcpy(tmp, f0->d_pi, n * sizeof(u32), cudaMemcpyDeviceToHost));
+      for (u64 i = 0; i < n; ++i) lab64[i] = tmp[i];
+    }
+    HCC_CUDA(cudaSetDevice(c->dev));
+    return HCC_OK;
+    HCC_GUARD_END
+  }
+  return HCC_OK;
+}
+
+extern "C" {
+
+int hcc_create_multi(const int* devices, int ndev, hcc_ctx** out) {
+  if (!out || !devices) return fail(HCC_EINVAL, "null argument");
+  *out = nullptr;
+  if (ndev < 1 || ndev > (int)kMaxShards)
+    return fail(HCC_EINVAL, "shard count must be in [1, 64]");
+  hcc_ctx* c = nullptr;
+  if (int r = hcc_create(devices[0], &c)) return r;
+  for (int i = 0; i < ndev; ++i) {
+    hcc_ctx* sc = nullptr;
+    if (int r = hcc_create(devices[i], &sc)) {
+      hcc_destroy(c);
+      return r;
+    }
+    c->subs.push_back(sc);
+  }
+  // P2P between every pair of distinct devices: the merge kernel reads the
+  // peers' export buffers in place over NVLink
+  c->peer_access = 1;
+  for (int i = 0; i < ndev; ++i)
+    for (int j = 0; j < ndev; ++j) {
+      const int a = devices[i], b = devices[j];
+      if (a == b) continue;
+      int can = 0;
+      if (cudaDeviceCanAccessPeer(&can, a, b) != cudaSuccess || !can) {
+        cudaGetLastError();
+        hcc_destroy(c);
+        return fail(HCC_ENCCL, "no peer access from device " + std::to_string(a) + " to " +
+                                   std::to_string(b) + " (the merge reads peer memory)");
+      }
+      cudaSetDevice(a);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        hcc_destroy(c);
+        return fail(HCC_ENCCL, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+      }
+      cudaGetLastError();
+    }
+  cudaSetDevice(devices[0]);
+  *out = c;
+  return HCC_OK;
+}
+
+int hcc_ctx_shards(hcc_ctx* c, int* count) {
+  if (!c || !count) return fail(HCC_EINVAL, "null argument");
+  *count = c->subs.empty() ? 1 : (int)c->subs.size();
+  return HCC_OK;
+}
+
+int hcc_ctx_shard_metrics(hcc_ctx* c, hcc_shard_metrics* out, uint64_t cap, uint64_t* count) {
+  if (!c) return fail(HCC_EINVAL, "null context");
+  const u64 G = c->merge.size();
+  if (count) *count = G;
+  for (u64 r = 0; r < std::min<u64>(cap, G); ++r) {
+    const MergeShard& ms = c->merge[r];
+    hcc_shard_metrics x{};
+    x.total_ms = ms.local_ms + ms.merge_ms;
+    x.local_ms = ms.local_ms;
+    x.merge_ms = ms.merge_ms;
+    x.span_ms = ms.total_ms;
+    x.pairs_exported = ms.exported;
+    x.records_merged = ms.records;
+    x.rehook_passes = ms.passes;
+    x.bitmap_bytes = ms.bits_words * 4;
+    x.device = c->subs[r]->dev;
+    x.peer_access = c->peer_access;
+    out[r] = x;
+  }
+  return HCC_OK;
 }
 
 }  // extern "C"

@@ -84,12 +84,12 @@ __global__ void k_gen_erx(uint2* out, u64 first, u64 count, u64 n, u64 seed) {
   }
 }
 
-__global__ void k_checksum(const uint2* e, u64 m, u64* out) {
+__global__ void k_checksum(const uint2* e, u64 m, u64 base, u64* out) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
   u64 s = 0;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
     uint2 x = e[i];
-    s += checksum_term(i, x.x, x.y);
+    s += checksum_term(base + i, x.x, x.y);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);

@@ -43,6 +43,13 @@ constexpr int kHookCta = HCC_HOOK_CTA;
 #define HCC_HOOK_SUM_CTA 1024
 #endif
 constexpr int kHookSumCta = HCC_HOOK_SUM_CTA;  // k_hook_sum (one CTA per SM)
+// CAS-storing worklist hooks (k_hook_cas, k_hook_sum_cas): 768-thread CTAs
+// give them 80 registers instead of 64 (at 1024 threads ptxas spilled
+// 32 B / 12 B of stores per thread).
+#ifndef HCC_HOOK_CAS_CTA
+#define HCC_HOOK_CAS_CTA 768
+#endif
+constexpr int kHookCasCta = HCC_HOOK_CAS_CTA;
 constexpr u32 kS0fMaxBytes = HCC_S0F_MAX_BYTES;
 constexpr int kHookSlow = 4;
 // HookArgs.gate: k_hook_sum and k_hook are launched back to back for a
@@ -219,7 +226,7 @@ __global__ void k_gen_grid(uint2* out, u64 rows, u64 cols, u64 first, u64 count)
 __global__ void k_gen_rmatx(uint2* out, u64 first, u64 count, u32 scale,
                             u64 seed, u32 ta, u32 tab, u32 tabc);
 __global__ void k_gen_erx(uint2* out, u64 first, u64 count, u64 n, u64 seed);
-__global__ void k_checksum(const uint2* e, u64 m, u64* out);
+__global__ void k_checksum(const uint2* e, u64 m, u64 base, u64* out);
 
 // Verification (hcc_graph_kernels.cu).
 __global__ void k_verify_edges(const uint2* e, u64 m, const u32* pi, u64* bad);
@@ -230,6 +237,17 @@ __global__ void k_count_distinct(const u64* k, u64 n, int shift, u64* out);
 // Multi-GPU merge (hcc_multi.cu).
 __global__ void k_export(const u32* pi, u64 n, u32* bits, uint2* pairs, u64 cap,
                          u64* count);
+// Peer export buffers of a multi-device merge (device-resident table).
+constexpr u32 kMaxShards = 64;
+struct PeerTab {
+  u32 npeers;
+  const u32* bits[kMaxShards];    // export bitmap of rank r
+  const uint2* pairs[kMaxShards]; // export pairs of rank r
+  const u64* count[kMaxShards];   // pairs rank r produced (may exceed cap)
+  u64 cap[kMaxShards];
+};
+__global__ void k_merge_gather(const PeerTab* tab, u32 self, const u32* pi, u64 n, uint2* wl,
+                               u64* count, u64 cap, u32* err);
 __global__ void k_decode_bits(const u32* rows, u64 nrows, u64 stride, u64 skip, const u32* pi,
                               u64 n, uint2* wl, u64* count);
 

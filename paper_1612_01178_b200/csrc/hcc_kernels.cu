@@ -207,6 +207,9 @@ __device__ __forceinline__ void resolve_src(const HookArgs& a, const uint2*& src
     src = p ? a.wl1 : a.wl0;
     b = 0;
     e = c->wl_count[p];
+    // an overflowed list (device error bit 4; the host re-runs with full-size
+    // worklists) counts past its capacity: never read beyond it
+    if (e > a.wl_cap) e = a.wl_cap;
     out = p ^ 1u;
   }
 }
@@ -528,7 +531,10 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
       }
       if (a.append) {
         const u64 pos = atomicAdd(cnt_out, 1ull);
-        wl_out[pos] = make_uint2(h, l);
+        if (pos < a.wl_cap)
+          wl_out[pos] = make_uint2(h, l);
+        else
+          atomicOr(&ctrl->err, 4u);
         atomicAdd(&r->edges_out, 1ull);
       }
     }
@@ -560,7 +566,10 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
         any_change = 1;
         if (a.append) {
           u64 pos = atomicAdd(cnt_out, 1ull);
-          wl_out[pos] = make_uint2(h, l);
+          if (pos < a.wl_cap)
+            wl_out[pos] = make_uint2(h, l);
+          else
+            atomicOr(&ctrl->err, 4u);
           atomicAdd(&r->edges_out, 1ull);
           ctrl->dirty = 1;
         }
@@ -601,9 +610,13 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
     if (a.append) {
       u64 pos;
       if (block_reserve(__popc(act), cnt_out, pos, appended)) {
+        if (pos + __popc(act) <= a.wl_cap) {
 #pragma unroll
-        for (int k = 0; k < EPT; ++k)
-          if (act & (1u << k)) wl_out[pos++] = make_uint2(pu[k], pv[k]);
+          for (int k = 0; k < EPT; ++k)
+            if (act & (1u << k)) wl_out[pos++] = make_uint2(pu[k], pv[k]);
+        } else {
+          atomicOr(&ctrl->err, 4u);  // sized on the host; the host re-runs
+        }
       }
     } else {
       any_change |= act;
@@ -828,12 +841,12 @@ __global__ void __launch_bounds__(kHookCta, HCC_HOOK_MINB) k_hook_legacy(HookArg
 
 // CAS-storing variants (separate kernels: the runtime branch in k_hook cost
 // it spills).
-__global__ void __launch_bounds__(kHookCta, HCC_HOOK_MINB) k_hook_cas(HookArgs a) {
+__global__ void __launch_bounds__(kHookCasCta, 1) k_hook_cas(HookArgs a) {
   if (a.gate == kGateIfPlain && __ldg(&a.ctrl->use_sum)) return;
   hook_stream<kHookEPT, false, true>(a);
 }
 
-__global__ void __launch_bounds__(kHookSumCta, 1) k_hook_sum_cas(HookArgs a) {
+__global__ void __launch_bounds__(kHookCasCta, 1) k_hook_sum_cas(HookArgs a) {
   if (a.gate == kGateIfSum && !__ldg(&a.ctrl->use_sum)) return;
   hook_stream<kHookEPT, true, true>(a);
 }
@@ -959,6 +972,9 @@ constexpr int kStarChase = 32;
 __global__ void k_star_pick(const u32* pi, u64 n, DevCtrl* ctrl) {
   const u32 lane = threadIdx.x & 31u;
   if (threadIdx.x >= 32 || n == 0) return;
+  // A slot whose hook stored nothing skips its compress (kCompressIfDirty),
+  // so the bitmap keeps tracking the current star: it must not move.
+  if (__ldcg(&ctrl->dirty) == 0) return;
   u64 hsh = (u64)(lane + 1) * 0x9E3779B97F4A7C15ull;
   hsh ^= hsh >> 29;
   hsh *= 0xBF58476D1CE4E5B9ull;
@@ -1238,7 +1254,8 @@ __global__ void k_step_worklist(DevCtrl* c, DevRec* recs,
   c->passes += 1;
   c->dirty = 0;
   next_rec(c, recs);
-  const u32 cond = guard(c, produced > 0 ? 1u : 0u);
+  // a worklist overflow ends the run (the host re-runs with full-size lists)
+  const u32 cond = guard(c, produced > 0 && !(c->err & 4u) ? 1u : 0u);
   c->cond = cond;
   if (use_cond) cudaGraphSetConditional(h, cond);
 }

@@ -94,4 +94,101 @@ __global__ void k_decode_bits(const u32* rows, u64 nrows, u64 stride, u64 skip, 
   }
 }
 
+// Fused exchange + decode of the single-process multi-device merge
+// (hcc_create_multi): rank r's kernel reads every peer's export buffers
+// directly over NVLink (peer access; shards on the same device read plain
+// device memory), so no payload is staged and no host reads a size:
+//   * bitmaps  OR of the peers' rows, 32 words per warp round; set bits
+//              whose vertex is not yet in r's star of 0 -> (v, 0) records;
+//   * pairs    the peers' (v, parent) pairs, count read from peer memory;
+//              pairs already joined in r's forest (pi(v) == pi(parent): the
+//              forest is a set of stars after the local CC) are dropped.
+// Records go to r's worklist; the worklist engine then re-hooks them.
+__global__ void k_merge_gather(const PeerTab* tab, u32 self, const u32* pi, u64 n, uint2* wl,
+                               u64* count, u64 cap, u32* err) {
+  const u32 lane = threadIdx.x & 31u;
+  const u32 np = tab->npeers;
+  const u64 nwords = (n + 31) >> 5;
+  const u64 gwarp = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const u64 warps = ((u64)gridDim.x * blockDim.x) >> 5;
+  // 32 words per warp round: lane j ORs word w0 + j of every peer row (one
+  // 128-byte read per peer), then the warp decodes the words one by one
+  for (u64 w0 = gwarp * 32; w0 < nwords; w0 += warps * 32) {
+    u32 x = 0;
+    if (w0 + lane < nwords)
+      for (u32 r = 0; r < np; ++r)
+        if (r != self) x |= __ldcg(tab->bits[r] + w0 + lane);
+    // pass 1: lane k keeps word k's mask of vertices to record
+    // (eight words' pi reads in flight per group)
+    u32 mine = 0;
+    for (u32 k0 = 0; k0 < 32; k0 += 8) {
+      u32 b[8], p[8];
+#pragma unroll
+      for (u32 j = 0; j < 8; ++j) {
+        b[j] = __shfl_sync(0xffffffffu, x, k0 + j);
+        const u64 v = ((w0 + k0 + j) << 5) + lane;
+        p[j] = ((b[j] >> lane) & 1u) && v < n ? __ldcg(pi + v) : 0u;
+      }
+#pragma unroll
+      for (u32 j = 0; j < 8; ++j) {
+        const u32 mask = __ballot_sync(0xffffffffu, ((b[j] >> lane) & 1u) && p[j] != 0u &&
+                                                        ((w0 + k0 + j) << 5) + lane < n);
+        if (lane == k0 + j) mine = mask;
+      }
+    }
+    // pass 2: one reservation per warp round, then the stores
+    const u32 cnt = __popc(mine);
+    u32 incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (u32)o) incl += y;
+    }
+    const u32 total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) continue;
+    u64 base = 0;
+    if (lane == 0) base = atomicAdd(count, (u64)total);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (u32 k = 0; k < 32; ++k) {
+      const u32 mk = __shfl_sync(0xffffffffu, mine, k);
+      const u32 off = __shfl_sync(0xffffffffu, incl - cnt, k);
+      if (!((mk >> lane) & 1u)) continue;
+      const u64 pos = base + off + __popc(mk & ((1u << lane) - 1u));
+      if (pos < cap)
+        wl[pos] = make_uint2((u32)(((w0 + k) << 5) + lane), 0u);
+      else
+        atomicOr(err, 4u);
+    }
+  }
+  // pairs: one global index space over the peers' lists
+  const u64 tid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u32 r = 0; r < np; ++r) {
+    if (r == self) continue;
+    u64 k = __ldcg(tab->count[r]);
+    if (k > tab->cap[r]) k = tab->cap[r];  // the host detects the overflow
+    const uint2* pr = tab->pairs[r];
+    for (u64 i = tid; i < ((k + 31) & ~31ull); i += stride) {
+      uint2 x = make_uint2(0u, 0u);
+      bool want = false;
+      if (i < k) {
+        x = __ldcg(pr + i);
+        want = x.x < n && x.y < n && __ldcg(pi + x.x) != __ldcg(pi + x.y);
+      }
+      const u32 mask = __ballot_sync(0xffffffffu, want);
+      if (!mask) continue;
+      u64 base = 0;
+      if (lane == 0) base = atomicAdd(count, (u64)__popc(mask));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (want) {
+        const u64 pos = base + __popc(mask & ((1u << lane) - 1u));
+        if (pos < cap)
+          wl[pos] = x;
+        else
+          atomicOr(err, 4u);
+      }
+    }
+  }
+}
+
 }  // namespace hcc

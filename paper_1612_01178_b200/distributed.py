@@ -52,12 +52,15 @@ _BUFS: dict = {}
 
 
 def _buf(key, numel, dtype, device):
-    """Reusable receive buffers (per shape): the exchange runs every step."""
+    """Reusable receive buffers, one per (key, dtype, device), grown
+    geometrically: the exchange runs every step with varying pair counts."""
     import torch
-    t = _BUFS.get(key)
-    if t is None or t.numel() < numel or t.dtype != dtype or t.device != device:
-        t = torch.empty(numel, dtype=dtype, device=device)
-        _BUFS[key] = t
+    k = (key, dtype, str(device))
+    t = _BUFS.get(k)
+    if t is None or t.numel() < numel:
+        t = torch.empty(max(numel, (t.numel() * 3 // 2) if t is not None else 0),
+                        dtype=dtype, device=device)
+        _BUFS[k] = t
     return t[:numel]
 
 
@@ -92,7 +95,7 @@ def exchange(bits, pairs, group=None, sendbuf=None, pairs_buf=None):
         sendbuf = torch.zeros(off + 2, dtype=torch.int32, device=dev)
         sendbuf[:nw] = bits
     sendbuf[off:].view(torch.int64).fill_(k)
-    gathered = _buf(("bits", nw), world * (off + 2), torch.int32, dev)
+    gathered = _buf("bits", world * (off + 2), torch.int32, dev)
     dist.all_gather_into_tensor(gathered, sendbuf, group=group)
     gathered = gathered.view(world, off + 2)
     sizes_h = gathered[:, off:].contiguous().view(torch.int64).view(-1).cpu().tolist()
@@ -105,7 +108,7 @@ def exchange(bits, pairs, group=None, sendbuf=None, pairs_buf=None):
     else:
         send = torch.zeros((kmax, 2), dtype=pairs.dtype, device=dev)
         send[:k] = pairs
-    allp = _buf(("pairs", kmax), world * kmax * 2, pairs.dtype, dev)
+    allp = _buf("pairs", world * kmax * 2, pairs.dtype, dev)
     dist.all_gather_into_tensor(allp, send.contiguous().view(-1), group=group)
     allp = allp.view(world * kmax, 2)
     parts = [allp[r * kmax: r * kmax + sizes_h[r]] for r in range(world) if r != rank and sizes_h[r]]
@@ -185,6 +188,9 @@ class CudaBackend:
 
     def rehook(self, bits_or, remote):
         remote = remote.contiguous()
+        # the gathered buffers were written on torch's stream; the library
+        # reads them on its own stream
+        self.torch.cuda.current_stream().synchronize()
         return self.ctx.rehook(self.forest, bits_or.data_ptr(),
                                remote.data_ptr() if remote.shape[0] else None,
                                int(remote.shape[0]))
@@ -193,6 +199,7 @@ class CudaBackend:
         # rows: [world, nwords] view of the gathered buffer (row stride
         # send_offset(nwords) + 2)
         remote = remote.contiguous()
+        self.torch.cuda.current_stream().synchronize()
         return self.ctx.rehook_rows(self.forest, rows.data_ptr(), int(rows.shape[0]),
                                     int(rows.stride(0)), int(rank),
                                     remote.data_ptr() if remote.shape[0] else None,

@@ -49,7 +49,7 @@ def test_library_is_sm100a(capi):
 
 
 def test_abi_version(capi):
-    assert capi.lib().hcc_abi_version() == 3
+    assert capi.lib().hcc_abi_version() == capi.ABI_VERSION == 4
 
 
 @pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="GPU present")

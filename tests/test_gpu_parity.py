@@ -609,3 +609,46 @@ def test_async_upload_pipelined(ctx, oracle, capi):
         assert np.array_equal(lab, want[[0, 1, 1][i % 3]]), i
     for g in gs:
         g.close()
+
+
+def test_stale_star_after_a_slot_without_stores(ctx, oracle):
+    """Advisor finding (round 1): a middle adaptive slot whose hook stores
+    nothing skips its compress, so the star pick must not move the star the
+    bitmap tracks.  Slot 0 (m/128 edges) builds a component rooted at 1
+    holding half the vertices, slot 1 repeats it (intra-component only:
+    no store, no compress), and the rest are (0, x) edges that must pull
+    the isolated vertex 0 into that component."""
+    n, m = 1 << 16, 1 << 22
+    first = m >> 7
+    e = np.empty((m, 2), dtype=np.uint32)
+    e[:first, 0] = 1
+    e[:first, 1] = np.arange(2, first + 2, dtype=np.uint32)
+    e[first:5 * first] = np.tile(e[:first], (4, 1))
+    rest = m - 5 * first
+    e[5 * first:, 0] = 0
+    e[5 * first:, 1] = 2 + (np.arange(rest, dtype=np.uint32) % first)
+    want = oracle.cc(n, e)
+    assert want[1] == 0 and want[first + 1] == 0
+    g = ctx.graph_from_edges(e, n)
+    lab, mx = ctx.cc(g, "baseline-mj")
+    assert mx["star0_bitmap"]
+    assert np.array_equal(lab, want)
+    g.close()
+
+
+def test_graph_cache_survives_buffer_regrowth(ctx, oracle):
+    """Advisor finding (round 1): the two cached executable graphs bake the
+    worklists, star bitmap and summary into their arguments; a larger graph
+    that regrows those buffers must not leave the other cached graph
+    pointing at freed memory.  Small n, then larger n (same m), then the
+    small one again, several times over."""
+    ga = ctx.generate("rmatx:scale=16,ef=64,seed=3")      # n = 2^16, m = 2^22
+    gb = ctx.generate("erx:n=2097152,m=4194304,seed=5")   # n = 2^21, m = 2^22
+    wa = oracle.cc(ga.n, ga.edges())
+    wb = oracle.cc(gb.n, gb.edges())
+    for _ in range(3):
+        for g, w in ((ga, wa), (gb, wb)):
+            lab, _ = ctx.cc(g, "baseline-mj")
+            assert np.array_equal(lab, w)
+    ga.close()
+    gb.close()

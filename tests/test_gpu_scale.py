@@ -2,10 +2,10 @@
 
 RMAT-16 (reference generator), grid 4096^2, ER 2^24/2^28 and RMAT-24 are
 checked label-for-label against the oracle on the same edge arrays.  RMAT-28
-(2^32 edges) is beyond a quick CPU oracle, so it is checked through
-size-independent properties computed on the device (every edge intra-label,
-labels canonical min-rooted stars) plus exact agreement of two independent
-engines (the worklist engine and the CAS-based adaptive engine).
+(2^32 edges; 32 GiB packed) is checked against the digest of the streaming
+oracle (oracle_cc_stream: the reference's DSU oracle over the generator
+stream, never materialising the edges), committed in tests/golden/big.json,
+plus the device-side properties.
 """
 from __future__ import annotations
 
@@ -18,6 +18,12 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 GOLD = json.loads((Path(__file__).parent / "golden" / "golden.json").read_text())
+BIG = json.loads((Path(__file__).parent / "golden" / "big.json").read_text())
+
+
+def sha256_u32(a) -> str:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a, dtype="<u4").tobytes()).hexdigest()
 
 
 def digest(a) -> str:
@@ -63,20 +69,40 @@ def test_rmat16_reference_generator_exact(ctx, oracle):
         assert mx["components"] == 18893
 
 
-def test_rmat28_single_gpu_properties(ctx):
-    """4.3 billion edges on one B200: device-side properties + two engines agree."""
-    g = ctx.generate("rmatx:scale=28,ef=16,seed=1")
+def test_rmat28_single_gpu_exact(ctx):
+    """BASELINE configs[4] on one B200 (4.3 billion edges): labels bit-exact
+    against the streaming oracle's digest (tests/golden/big.json, made by
+    tests/golden/make_big.py from oracle_cc_stream), the generator pinned by
+    the full-size edge checksum, plus the device-side properties, for the
+    north-star engine and the paper's adaptive engine."""
+    gold = BIG["rmat28"]
+    g = ctx.generate(gold["spec"])
     assert g.m == 1 << 32
+    assert g.checksum() == gold["edges_checksum"]
     f = ctx.forest(g.n)
-    _, mx = ctx.cc(g, "baseline-mj", forest=f, labels=False)
-    assert ctx.verify(g, f) == (0, 0)
-    a = f.snapshot().astype(np.uint32)
-    f2 = ctx.forest(g.n)
-    _, mx2 = ctx.cc(g, "adaptive", segments=32, forest=f2, labels=False)
-    assert ctx.verify(g, f2) == (0, 0)
-    b = f2.snapshot().astype(np.uint32)
-    assert np.array_equal(a, b)
-    assert mx["components"] == mx2["components"]
+    for algo, seg in (("baseline-mj", 0), ("adaptive", 32)):
+        _, mx = ctx.cc(g, algo, segments=seg, forest=f, labels=False)
+        assert mx["components"] == gold["components"], algo
+        assert ctx.verify(g, f) == (0, 0)
+        lab = f.snapshot().astype(np.uint32)
+        assert [int(lab[i]) for i in gold["sample_idx"]] == gold["sample_labels"]
+        assert sha256_u32(lab) == gold["labels_sha256"], algo
+        del lab
+    f.close()
+    g.close()
+
+
+@pytest.mark.parametrize("name", ["rmat24", "er24"])
+def test_big_digests_match_live_oracle(ctx, name):
+    """The committed streaming-oracle digests agree with the device at the
+    sizes the live oracle also covers (pins make_big.py itself)."""
+    gold = BIG[name]
+    g = ctx.generate(gold["spec"])
+    assert g.checksum() == gold["edges_checksum"]
+    lab, mx = ctx.cc(g, "baseline-mj")
+    assert mx["components"] == gold["components"]
+    assert sha256_u32(lab) == gold["labels_sha256"]
+    g.close()
 
 
 def test_labels_compare_device(ctx):

@@ -296,3 +296,36 @@ def test_counter_generators_consistency(oracle):
     er = oracle.gen_erx(1000, 5, 0, 20000)
     assert int(er.max()) < 1000 and abs(float(er.mean()) - 499.5) < 10
     assert oracle.checksum_u32(full[:10], 0) != oracle.checksum_u32(full[1:11], 1) or True
+
+
+@pytest.mark.parametrize("spec,first,count", [
+    ("rmatx:scale=12,ef=16,seed=4", 0, None),
+    ("rmatx:scale=12,ef=16,seed=4", 1000, 20000),
+    ("erx:n=5000,m=30000,seed=9", 0, None),
+    # crosses the 2^25-edge chunk boundary of the streaming pipeline
+    ("rmatx:scale=21,ef=20,seed=1", 0, None),
+])
+def test_streaming_oracle_matches_materialised(oracle, spec, first, count):
+    """oracle_cc_stream (the RMAT-28 ground truth, tests/golden/make_big.py)
+    equals oracle_cc over the materialised edge array."""
+    kind, params = spec.split(":")
+    kv = dict(p.split("=") for p in params.split(","))
+    if kind == "rmatx":
+        n, m = 1 << int(kv["scale"]), int(kv["ef"]) << int(kv["scale"])
+        e = oracle.gen_rmatx(int(kv["scale"]), int(kv["seed"]), first,
+                             m - first if count is None else count)
+    else:
+        n, m = int(kv["n"]), int(kv["m"])
+        e = oracle.gen_erx(n, int(kv["seed"]), first, m - first if count is None else count)
+    lab, ck, comp = oracle.cc_stream(spec, first, count)
+    want = oracle.cc(n, e)
+    assert np.array_equal(lab, want)
+    assert ck == oracle.checksum_u32(e, first)
+    assert comp == int(np.sum(want == np.arange(n, dtype=np.uint32)))
+
+
+def test_big_golden_file_shape():
+    import json
+    big = json.loads((Path(__file__).parent / "golden" / "big.json").read_text())
+    assert {"rmat24", "er24", "rmat28"} <= set(big)
+    assert big["rmat28"]["n"] == 1 << 28 and big["rmat28"]["components"] > 0
