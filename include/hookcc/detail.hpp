@@ -7,8 +7,10 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <map>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "hookcc_c.h"
 
@@ -73,6 +75,26 @@ inline hcc_ctx* ctx() {
     check(hcc_create(default_device(), &h.c));
   }
   return h.c;
+}
+
+/// The calling thread's multi-device context for a device list (created on
+/// first use, kept for the thread's lifetime: the shard buffers and cached
+/// CUDA graphs are reused across calls).
+inline hcc_ctx* multi_ctx(const std::vector<int>& devices) {
+  struct Holder {
+    std::map<std::vector<int>, hcc_ctx*> m;
+    ~Holder() {
+      for (auto& kv : m) hcc_destroy(kv.second);
+    }
+  };
+  thread_local Holder h;
+  auto it = h.m.find(devices);
+  if (it != h.m.end()) return it->second;
+  ctx();  // ABI check
+  hcc_ctx* c = nullptr;
+  check(hcc_create_multi(devices.data(), static_cast<int>(devices.size()), &c));
+  h.m.emplace(devices, c);
+  return c;
 }
 
 }  // namespace detail

@@ -94,6 +94,10 @@ struct DriverOptions {
   // B200 options
   std::uint64_t first_pass_segments = 0;  // baseline-mj topology segments (0 = auto)
   std::uint32_t flags = 0;                // HCC_FLAG_*
+  // Edge-partitioned multi-GPU run (hcc_create_multi): one shard per entry
+  // (partition_edges(m, devices.size()), engines.hpp:43-58), local CC on
+  // every device, NVLink P2P merge.  Empty = the calling thread's device.
+  std::vector<int> devices;
 };
 
 struct DriverResult {
@@ -126,7 +130,7 @@ inline RunMetrics run_device(const Graph& g, int algo, const char* name,
     mx.outer_iterations = algo == HCC_ALGO_ADAPTIVE ? mx.s : 0;
     return mx;
   }
-  DeviceGraph dg(g);
+  DeviceGraph dg = opts.devices.empty() ? DeviceGraph(g) : DeviceGraph();
   hcc_opts o{};
   o.algo = algo;
   o.segments = segments;
@@ -138,6 +142,32 @@ inline RunMetrics run_device(const Graph& g, int algo, const char* name,
     o.observer_user = const_cast<void*>(static_cast<const void*>(&opts.phase_observer));
   }
   hcc_metrics hm{};
+  if (!opts.devices.empty()) {
+    // sharded over opts.devices; the merged labels are copied into pi
+    if (opts.phase_observer)
+      throw std::invalid_argument("phase_observer needs a single-device run");
+    hcc_ctx* mc = multi_ctx(opts.devices);
+    hcc_graph* mg = nullptr;
+    check(hcc_graph_from_edges_u64(mc, reinterpret_cast<const std::uint64_t*>(g.edges.data()),
+                                   g.edges.size(), g.n, &mg));
+    std::vector<std::uint64_t> lab(g.n);
+    const int st = hcc_cc_u64(mc, mg, &o, nullptr, lab.data(), &hm);
+    hcc_graph_free(mg);
+    check(st);
+    check(hcc_forest_upload_u64(pi.handle(), lab.data()));
+    mx.s = hm.s;
+    mx.segments_clamped = hm.segments_clamped != 0;
+    mx.total_ms = hm.total_ms;
+    mx.hook_ms = hm.hook_ms;
+    mx.compress_ms = hm.compress_ms;
+    mx.outer_iterations = hm.outer_iterations;
+    mx.counters = {hm.counters.hook_traversal_steps, hm.counters.cas_failures,
+                   hm.counters.jump_steps};
+    mx.passes = hm.passes;
+    mx.edges_processed = hm.edges_processed;
+    mx.device_loop = hm.used_device_loop != 0;
+    return mx;
+  }
   check(hcc_cc(ctx(), dg.handle(), &o, pi.handle(), nullptr, &hm));
   mx.s = hm.s;
   mx.segments_clamped = hm.segments_clamped != 0;

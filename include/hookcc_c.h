@@ -360,6 +360,35 @@ int hcc_ctx_shards(hcc_ctx* ctx, int* count);
 int hcc_ctx_shard_metrics(hcc_ctx* ctx, hcc_shard_metrics* out, uint64_t cap,
                           uint64_t* count);
 
+/* ---- multi-process merge over CUDA IPC (one process per GPU, e.g. under
+ * torchrun; paper_1612_01178_b200/distributed.py binds it) -----------------
+ * Per rank, once: hcc_peer_open allocates the export arena (pair count,
+ * bitmap, `cap` pairs) and an interprocess event and writes a handle blob of
+ * HCC_PEER_HANDLE_BYTES; the caller exchanges the blobs (any transport) and
+ * passes all of them, in rank order, to hcc_peer_connect, which maps the
+ * peers' arenas (lazy peer access).  Per run, after the local CC into `f`:
+ *   hcc_peer_export(ctx, f)   k_export into the arena + event record (async)
+ *   <host barrier across ranks: every record precedes every wait>
+ *   hcc_peer_merge(ctx, f, ..) device waits on the peers' events, then
+ *                             k_merge_gather reads their arenas over NVLink
+ *                             and the worklist engine re-hooks; synchronous.
+ * *overflow = 1 when some rank exported more pairs than its cap: the merge
+ * is then incomplete (but every relation applied is true) -- reopen with a
+ * larger cap, reconnect, export and merge again. */
+#define HCC_PEER_HANDLE_BYTES 256
+int hcc_peer_open(hcc_ctx* ctx, uint64_t n, uint64_t cap, int rank, int world,
+                  void* handle_out);
+int hcc_peer_connect(hcc_ctx* ctx, const void* handles);
+int hcc_peer_export(hcc_ctx* ctx, hcc_forest* f);
+/* metrics: total_ms = export start to merge end (device), edges_processed =
+ * remote relations re-hooked, m = pairs this rank exported, components. */
+int hcc_peer_merge(hcc_ctx* ctx, hcc_forest* f, hcc_metrics* out, int* overflow);
+/* Unmap the peers' arenas (keeps this rank's).  Every rank must disconnect
+ * (then meet at a barrier) before any rank closes or reopens, which frees
+ * the arena its peers map. */
+int hcc_peer_disconnect(hcc_ctx* ctx);
+int hcc_peer_close(hcc_ctx* ctx);
+
 #ifdef __cplusplus
 }  /* extern "C" */
 #endif

@@ -128,7 +128,15 @@ _SIGS = {
     "hcc_create_multi": (i32, [C.POINTER(i32), i32, C.POINTER(vp)]),
     "hcc_ctx_shards": (i32, [vp, C.POINTER(i32)]),
     "hcc_ctx_shard_metrics": (i32, [vp, vp, u64, C.POINTER(u64)]),
+    "hcc_peer_open": (i32, [vp, u64, u64, i32, i32, vp]),
+    "hcc_peer_connect": (i32, [vp, vp]),
+    "hcc_peer_export": (i32, [vp, vp]),
+    "hcc_peer_merge": (i32, [vp, vp, C.POINTER(Metrics), C.POINTER(i32)]),
+    "hcc_peer_disconnect": (i32, [vp]),
+    "hcc_peer_close": (i32, [vp]),
 }
+
+PEER_HANDLE_BYTES = 256
 
 
 def exported_symbols() -> list[str]:
@@ -268,6 +276,31 @@ class Context:
         check(lib().hcc_graph_generate_range(self.h, spec.encode(), default_seed, first, count,
                                              C.byref(h)))
         return Graph(self, h)
+
+    # -- multi-process merge over CUDA IPC (hcc_peer_*) --
+    def peer_open(self, n: int, cap: int, rank: int, world: int) -> bytes:
+        buf = C.create_string_buffer(PEER_HANDLE_BYTES)
+        check(lib().hcc_peer_open(self.h, n, cap, rank, world, buf))
+        return buf.raw
+
+    def peer_connect(self, handles: bytes) -> None:
+        buf = C.create_string_buffer(handles, len(handles))
+        check(lib().hcc_peer_connect(self.h, buf))
+
+    def peer_export(self, forest: "Forest") -> None:
+        check(lib().hcc_peer_export(self.h, forest.h))
+
+    def peer_merge(self, forest: "Forest") -> tuple[dict, bool]:
+        mx = Metrics()
+        ovf = i32()
+        check(lib().hcc_peer_merge(self.h, forest.h, C.byref(mx), C.byref(ovf)))
+        return metrics_dict(mx), bool(ovf.value)
+
+    def peer_disconnect(self) -> None:
+        check(lib().hcc_peer_disconnect(self.h))
+
+    def peer_close(self) -> None:
+        check(lib().hcc_peer_close(self.h))
 
     def export(self, forest: "Forest", dev_bits: int, dev_pairs: int, cap: int) -> int:
         """hcc_forest_export into caller device buffers; returns the pair count
@@ -427,6 +460,9 @@ class Forest:
         out = np.empty(self.n, dtype=np.uint64)
         check(lib().hcc_forest_download_u64(self.h, _ptr(out) if self.n else None))
         return out
+
+    def snapshot_u32(self) -> np.ndarray:
+        return self.download_u32(np.empty(self.n, dtype=np.uint32))
 
     def download_u32(self, out: np.ndarray) -> np.ndarray:
         """The labels as u32 into a caller buffer (pinned for full PCIe speed)."""

@@ -8,15 +8,25 @@ a full local forest (stars).  The merge is one exchange round (§8e shape 3):
   1. export   each rank encodes its forest as a bitmap of {v : pi(v) == 0}
               (the giant component's root on skewed graphs) plus sparse
               (v, pi(v)) pairs for the remaining non-self entries;
-  2. exchange all-gather of the bitmaps (OR-combined) and of the pair lists
-              (sizes first, then the padded payloads) over the process group
-              (NCCL on GPUs, gloo in the CPU tests);
+  2. exchange the peers' payloads reach every rank;
   3. re-hook  each rank hooks the remote relations as (v, pi_remote(v)) edges
               into its own forest with the worklist engine.
 
+Two transports for step 2:
+  * PeerMerge (default on GPUs): CUDA IPC.  Every rank maps its peers'
+    export arenas once (hcc_peer_open / hcc_peer_connect; the handle blobs
+    are all-gathered over the process group), and per run the merge kernel
+    (k_merge_gather) reads them in place over NVLink -- steps 2 and 3 are one
+    kernel plus the re-hook passes; the host only runs one barrier between
+    export and merge and a one-int all-reduce (pair-buffer overflow) after.
+    The same kernel serves the single-process multi-device context
+    (hcc_create_multi).
+  * merge_round (NCCL / gloo): all-gather of the bitmaps (OR-combined) and of
+    the pair lists (sizes first, then the padded payloads); the protocol is
+    testable on CPU with gloo.
+
 After the round every rank holds the union of all shards' relations, i.e. the
-global min-canonical labels.  The exchange is written against a tiny backend
-interface so that the protocol itself is testable without a GPU.
+global min-canonical labels.
 """
 from __future__ import annotations
 
@@ -207,3 +217,76 @@ class CudaBackend:
 
     def labels(self) -> np.ndarray:
         return self.forest.snapshot()
+
+
+class PeerMerge:
+    """Merge over CUDA IPC (hcc_peer_*): k_merge_gather reads the peers'
+    export arenas in place over NVLink.  Host traffic per run: one barrier
+    between export and merge (every export event is recorded before any
+    rank waits on it) and a one-int MAX all-reduce after the merge, which
+    also keeps a fast rank's next export from overwriting an arena a slow
+    rank is still reading.  A rank whose pair list overflowed its arena
+    makes every rank reopen with a larger one and repeat (the relations
+    already merged are true ones, so a repeat is exact)."""
+
+    def __init__(self, ctx, n: int, group=None, cap: int | None = None, device=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.ctx = ctx
+        self.n = n
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.cap = cap or max(1 << 16, n // 64)
+        self.device = device  # device of the flag tensor (NCCL); None = CPU (gloo)
+        self.reopens = 0
+        self._connect()
+
+    def _connect(self):
+        blob = self.ctx.peer_open(self.n, self.cap, self.rank, self.world)
+        blobs = [None] * self.world
+        self.dist.all_gather_object(blobs, blob, group=self.group)
+        self.ctx.peer_connect(b"".join(blobs))
+
+    def _any(self, flag: bool) -> bool:
+        import torch
+        t = torch.tensor([int(flag)], dtype=torch.int32, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return bool(t.item())
+
+    def merge(self, forest) -> dict:
+        for attempt in range(3):
+            self.ctx.peer_export(forest)
+            self.dist.barrier(group=self.group)
+            mx, overflow = self.ctx.peer_merge(forest)
+            if not self._any(overflow):
+                mx["reopens"] = self.reopens
+                return mx
+            self.cap = self.n if attempt >= 1 else min(self.n, 8 * self.cap)
+            self.reopens += 1
+            self._release()
+            self._connect()
+        raise RuntimeError("peer merge: pair arenas kept overflowing")
+
+    def _release(self):
+        # every rank unmaps its peers' arenas before any rank frees its own
+        self.ctx.peer_disconnect()
+        self.dist.barrier(group=self.group)
+
+    def close(self):
+        self._release()
+        self.ctx.peer_close()
+
+
+def merge_round_p2p(peer: PeerMerge, forest) -> MergeTimes:
+    """export -> barrier -> NVLink gather + re-hook on this rank."""
+    t = MergeTimes()
+    t0 = time.perf_counter()
+    mx = peer.merge(forest)
+    t.rehook_ms = 1e3 * (time.perf_counter() - t0)
+    t.extra = {"device_ms": mx["total_ms"], "reopens": mx["reopens"]}
+    t.pairs_sent = int(mx["m"])
+    t.pairs_received = int(mx["edges_processed"])
+    t.bits_bytes = 4 * ((peer.n + 31) // 32)
+    t.rehook_passes = int(mx["passes"])
+    return t

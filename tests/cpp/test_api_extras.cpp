@@ -51,3 +51,19 @@ TEST_CASE("CSR ingestion matches the edge list") {
   Graph back = d.to_host();
   CHECK(oracle_cc(back).label == oracle_cc(g).label);
 }
+
+TEST_CASE("edge-partitioned multi-GPU drivers (DriverOptions::devices)") {
+  // four shards on device 0 (the builder's single GPU): the same code path
+  // as four GPUs, minus the NVLink hop
+  Graph g = rmat(13, 8, 11);
+  const ComponentLabeling truth = oracle_cc(g);
+  DriverOptions opts;
+  opts.devices = {0, 0, 0, 0};
+  DriverResult a = baseline_mj_cc(g, opts);
+  CHECK(a.labels.label == truth.label);
+  DriverResult b = adaptive_cc(g, 0, opts);
+  CHECK(b.labels.label == truth.label);
+  ParentForest pi(g.n);
+  baseline_mj_cc_into(g, pi, opts);
+  CHECK(pi.snapshot() == truth.label);
+}

@@ -76,3 +76,15 @@ def test_cli_smoke_on_b200(tmp_path):
         assert r.returncode == 0, (algo, r.stderr)
         j = json.loads(r.stdout)
         assert j["verified"] and j["algo"] == algo and "gteps" in j
+
+
+@pytest.mark.gpu
+def test_cli_multi_gpu_run(tmp_path):
+    """`cc run --devices 0,0,0` / `--gpus 1`: the edge-partitioned path
+    through the C++ API (DriverOptions::devices -> hcc_create_multi)."""
+    for flag in (["--devices", "0,0,0"], ["--gpus", "1"]):
+        r = cc("run", "--gen", "rmat:scale=11,ef=8,seed=4", "--algo", "baseline-mj", *flag)
+        assert r.returncode == 0, r.stderr
+        j = json.loads(r.stdout)
+        assert j["verified"]
+    assert cc("run", "--gen", "grid:4x4", "--gpus", "0").returncode == 2

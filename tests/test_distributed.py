@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import os
 import socket
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -170,3 +171,121 @@ def test_gpu_emulated_ranks(ctx, oracle, G, spec):
                     bits_or |= b
             be.rehook(bits_or, remote)
         assert np.array_equal(be.labels(), want), (spec, G, r)
+
+
+# ------------------------------------------------------- CUDA-IPC merge protocol
+
+class FakePeerCtx:
+    """CPU stand-in for the hcc_peer_* entry points (test-only): the "arena"
+    of a rank is a file in a shared directory, the handle blob is its path.
+    Export truncates the pair list at the arena's capacity but records the
+    full count, like k_export; merge reads every peer's file (the IPC read)
+    and re-hooks with the oracle."""
+
+    def __init__(self, oracle, n, shard, root):
+        self.O, self.n, self.root = oracle, n, root
+        self.pi = oracle.cc(n, shard).astype(np.int64)
+        self.opens = 0
+
+    def peer_open(self, n, cap, rank, world):
+        self.cap, self.rank, self.world = cap, rank, world
+        self.opens += 1
+        self.path = os.path.join(self.root, f"arena{rank}.{self.opens}.npz")
+        return self.path.encode().ljust(256, b"\0")
+
+    def peer_connect(self, handles):
+        self.peers = [handles[i * 256:(i + 1) * 256].rstrip(b"\0").decode()
+                      for i in range(self.world)]
+
+    def peer_export(self, forest):
+        v = np.arange(self.n)
+        keep = (self.pi != v) & (self.pi != 0)
+        pairs = np.stack([v[keep], self.pi[keep]], 1)
+        np.savez(self.path, in0=v[(self.pi == 0) & (v != 0)], pairs=pairs[: self.cap],
+                 count=len(pairs), cap=self.cap)
+
+    def peer_merge(self, forest):
+        rels, overflow = [np.stack([np.arange(self.n), self.pi], 1)], False
+        for r, path in enumerate(self.peers):
+            d = np.load(path)
+            overflow |= int(d["count"]) > int(d["cap"])
+            if r != self.rank:
+                rels.append(np.stack([d["in0"], np.zeros_like(d["in0"])], 1))
+                rels.append(d["pairs"].reshape(-1, 2))
+        self.pi = self.O.cc(self.n, np.concatenate(rels).astype(np.uint64)).astype(np.int64)
+        return {"total_ms": 0.0, "m": 0, "edges_processed": 0, "passes": 1}, overflow
+
+    def peer_disconnect(self):
+        pass
+
+    def peer_close(self):
+        pass
+
+
+def _peer_worker(rank, world, port, spec, root, cap, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import oracle as O
+        from paper_1612_01178_b200.distributed import PeerMerge
+        kind, n, e = spec
+        first, count = edge_range(e.shape[0], world, rank)
+        fc = FakePeerCtx(O, n, e[first:first + count], root)
+        pm = PeerMerge(fc, n, cap=cap)
+        pm.merge(None)
+        q.put((rank, fc.pi.tolist(), pm.reopens))
+        dist.destroy_process_group()
+    except Exception as ex:  # surface errors to the parent
+        q.put((rank, repr(ex), 0))
+
+
+@pytest.mark.parametrize("world,gi,cap", [(2, 0, None), (3, 1, None), (2, 2, 4), (3, 0, 1)])
+def test_gloo_peer_merge_protocol(oracle, tmp_path, world, gi, cap):
+    """PeerMerge (the CUDA-IPC transport's host protocol: handle all-gather,
+    export -> barrier -> merge -> overflow all-reduce, reopen on overflow),
+    world 2 and 3 over gloo; tiny caps force the reopen path."""
+    spec = _graphs()[gi]
+    want = oracle.cc(spec[1], spec[2]).astype(np.int64)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, spec, str(tmp_path), cap, q))
+             for r in range(world)]
+    [p.start() for p in procs]
+    res = [q.get(timeout=180) for _ in range(world)]
+    [p.join(timeout=60) for p in procs]
+    for rank, labels, reopens in res:
+        assert not isinstance(labels, str), labels
+        assert np.array_equal(np.asarray(labels), want), (spec[0], world, rank)
+        if cap is not None:
+            assert reopens >= 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,cap", [(2, 0), (3, 0), (2, 16)])
+def test_gpu_ipc_merge_multiprocess(oracle, tmp_path, world, cap):
+    """The CUDA-IPC transport end to end: `world` processes (torchrun, gloo
+    for the host collectives) share device 0, map each other's export arenas
+    and merge with k_merge_gather; every rank's labels equal the oracle's.
+    cap=16 forces the overflow -> reopen path.  Several runs per process
+    exercise the arena reuse between runs."""
+    import hashlib
+    import json
+    import subprocess
+    import sys
+    spec = "rmatx:scale=16,ef=16,seed=5"
+    e = oracle.gen_rmatx(16, 5, 0, 16 << 16)
+    want = oracle.cc(1 << 16, e).astype(np.uint32)
+    out = tmp_path / "res"
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        f"--nproc-per-node={world}", "--master-addr=127.0.0.1",
+                        f"--master-port={_free_port()}",
+                        str(Path(__file__).parent / "ipc_worker.py"), spec, str(out), str(cap), "3"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    for rank in range(world):
+        res = json.loads(Path(f"{out}.{rank}").read_text())
+        assert res["sha"] == hashlib.sha256(want.tobytes()).hexdigest(), res
+        assert res["components"] == int(np.sum(want == np.arange(1 << 16, dtype=np.uint32)))
+        if cap:
+            assert res["reopens"] >= 1

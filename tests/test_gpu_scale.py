@@ -84,7 +84,7 @@ def test_rmat28_single_gpu_exact(ctx):
         _, mx = ctx.cc(g, algo, segments=seg, forest=f, labels=False)
         assert mx["components"] == gold["components"], algo
         assert ctx.verify(g, f) == (0, 0)
-        lab = f.snapshot().astype(np.uint32)
+        lab = f.snapshot_u32()
         assert [int(lab[i]) for i in gold["sample_idx"]] == gold["sample_labels"]
         assert sha256_u32(lab) == gold["labels_sha256"], algo
         del lab

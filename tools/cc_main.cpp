@@ -21,7 +21,7 @@ enum Exit { kOk = 0, kVerify = 1, kUsage = 2, kIo = 3 };
 struct Flags {
   std::string input, format = "edgelist", gen, algo = "adaptive", segments = "auto",
                      workers = "max", labels_out, metrics_out, report = "json",
-                     sweep_segments;
+                     sweep_segments, devices;
   bool header = false, no_verify = false;
   std::uint64_t seed = 1, reps = 1, first_pass_segments = 0;
   std::vector<std::string> positional;
@@ -37,6 +37,7 @@ const char* kHelp =
     "                 [--algo baseline|baseline-mj|atomic|adaptive] [--segments auto|N]\n"
     "                 [--workers max|N] [--reps N] [--labels-out F] [--metrics-out F]\n"
     "                 [--report json|csv] [--no-verify] [--first-pass-segments N]\n"
+    "                 [--gpus N | --devices d0,d1,..]  (edge-partitioned multi-GPU run)\n"
     "       cc sweep  [input flags] [--sweep-segments a,b,..] [--workers] [--reps]\n"
     "                 [--metrics-out F] [--report json|csv]\n"
     "       cc verify [input flags] LABELS\n"
@@ -58,9 +59,10 @@ void member(const std::string& flag, const std::string& v, std::set<std::string>
 Flags parse(const std::string& cmd, int argc, char** argv, int first) {
   static const std::map<std::string, std::set<std::string>> value_flags = {
       {"run", {"--input", "--format", "--gen", "--seed", "--algo", "--segments", "--workers",
-               "--reps", "--labels-out", "--metrics-out", "--report", "--first-pass-segments"}},
+               "--reps", "--labels-out", "--metrics-out", "--report", "--first-pass-segments",
+               "--gpus", "--devices"}},
       {"sweep", {"--input", "--format", "--gen", "--seed", "--sweep-segments", "--workers",
-                 "--reps", "--metrics-out", "--report"}},
+                 "--reps", "--metrics-out", "--report", "--gpus", "--devices"}},
       {"verify", {"--input", "--format", "--gen", "--seed"}},
       {"gen", {"--seed"}}};
   static const std::map<std::string, std::set<std::string>> bool_flags = {
@@ -102,6 +104,14 @@ Flags parse(const std::string& cmd, int argc, char** argv, int first) {
     else if (a == "--report") member(a, f.report = val, {"json", "csv"});
     else if (a == "--sweep-segments") f.sweep_segments = val;
     else if (a == "--first-pass-segments") f.first_pass_segments = to_u64(a, val);
+    else if (a == "--gpus") {
+      const std::uint64_t k = to_u64(a, val);
+      if (k == 0 || k > 64) throw Usage("--gpus must be in [1, 64]");
+      f.devices.clear();
+      for (std::uint64_t d = 0; d < k; ++d) f.devices += (d ? "," : "") + std::to_string(d);
+    } else if (a == "--devices") {
+      f.devices = val;
+    }
   }
   const std::size_t max_pos = cmd == "verify" ? 1 : cmd == "gen" ? 2 : 0;
   const std::size_t min_pos = cmd == "verify" || cmd == "gen" ? 1 : 0;
@@ -139,6 +149,9 @@ hookcc::RunConfig to_config(const Flags& f) {
   cfg.labels_out = f.labels_out;
   cfg.metrics_out = f.metrics_out;
   cfg.first_pass_segments = f.first_pass_segments;
+  std::istringstream ds(f.devices);
+  for (std::string tok; std::getline(ds, tok, ',');)
+    if (!tok.empty()) cfg.devices.push_back(static_cast<int>(to_u64("--devices", tok)));
   return cfg;
 }
 
