@@ -89,6 +89,9 @@ constexpr u64 kMaxUnrolledSegments = 64;
 // (ER's forming slots need 16: at 8 their deferrals inflate the store ratio).
 constexpr int kDefaultWalk = 16;
 constexpr int kDefaultWalkLast = 4;
+// Fig. 3's walk runs until it links (the streaming CAS hook of the adaptive
+// engine has no worklist to defer to).
+constexpr int kUnboundedWalk = 1 << 30;
 // First adaptive topology segment = m >> kAdaptShift (HCC_PLAN=adapt:<k>).
 constexpr u32 kAdaptShift = 7;
 // Unrolled adaptive slots (HCC_PLAN=adapt:<k>:<slots>); the last takes every
@@ -440,6 +443,7 @@ struct Plan {
   u32 forming_pct;          // store ratio (%) above which a segment is forming
   unsigned grid_hook, block_hook, grid_vert, block_vert;
   unsigned grid_cas = 1;    // k_hook_cas grid (kHookCasCta threads per CTA)
+  bool cas_stream = false;  // atomic / adaptive on the streaming CAS hook
 };
 
 HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
@@ -705,6 +709,28 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
       break;
     }
     default: {  // ATOMIC / ADAPTIVE
+      if (P.cas_stream) {
+        // the paper's engine on the streaming machinery: per segment, the
+        // CAS-storing streaming hook (16-byte edge loads, star-bitmap
+        // lookups, lockstep walks that CAS only where they meet a root,
+        // walks unbounded as in Fig. 3, no worklist), then the star pick and
+        // the bitmap-building Multi-Jump compress (skipped when the segment
+        // linked nothing)
+        q.loop([&](cudaGraphConditionalHandle h, int u) {
+          HookArgs a = hook_args(c, P, kSrcSegment, 0);
+          a.walk = kUnboundedWalk;
+          a.cas = 1;
+          a.chunked = 1;
+          a.s0b = c->s0b;
+          k_hook_cas<<<P.grid_cas, kHookCasCta, 0, q.s()>>>(a);
+          q.phase_done(HCC_PHASE_HOOK);
+          k_star_pick<<<1, 32, 0, q.s()>>>(P.pi, P.n, ctrl);
+          launch_compress_s0b(c, P, q.s());
+          q.phase_done(HCC_PHASE_COMPRESS);
+          k_step_segment<<<1, 1, 0, q.s()>>>(ctrl, recs, h, u);
+        });
+        break;
+      }
       q.loop([&](cudaGraphConditionalHandle h, int u) {
         k_cas_hook<<<P.grid_hook, P.block_hook, 0, q.s()>>>(
             hook_args(c, P, kSrcSegment, 0));
@@ -1679,7 +1705,12 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   const bool uses_wl =
       o->algo == HCC_ALGO_BASELINE_MJ && !(o->flags & HCC_FLAG_FULL_PASSES);
   if (uses_wl && o->max_threads != 0) ensure_wl(c, m);  // exact block appends
-  bool s0b = uses_wl && o->max_threads == 0 && n >= (1ull << 16);
+  // atomic / adaptive on the streaming CAS hook (HCC_CAS_STREAM=0: the
+  // scalar k_cas_hook + k_compress of the one-thread reference schedule)
+  bool cas_stream = (o->algo == HCC_ALGO_ADAPTIVE || o->algo == HCC_ALGO_ATOMIC) &&
+                    o->max_threads == 0 && n >= (1ull << 16);
+  if (const char* e = std::getenv("HCC_CAS_STREAM")) cas_stream = cas_stream && std::atoi(e) != 0;
+  bool s0b = (uses_wl || cas_stream) && o->max_threads == 0 && n >= (1ull << 16);
   if (const char* e = std::getenv("HCC_S0B")) s0b = s0b && std::atoi(e) != 0;
 
   Plan P;
@@ -1693,7 +1724,8 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   P.wl1 = uses_wl ? c->wl[1] : nullptr;
   P.nseg = nseg;
   P.bounds = bounds;
-  P.s0b = s0b && !bounds.empty();
+  P.s0b = s0b && (!bounds.empty() || cas_stream);
+  P.cas_stream = cas_stream && P.s0b;
   P.adapt = adapt;
   P.adapt_shift = adapt_shift;
   P.adapt_first = adapt_first;
@@ -1704,6 +1736,8 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
                                                   : kAdaptFormingPct;
   if (P.s0b) {
     ensure_s0b(c, (n + 31) / 32);
+  }
+  if (P.s0b && uses_wl) {
     // star-0 summary: the smallest group (2^shift bitmap words per bit)
     // whose table fits the hook's shared-memory budget; groups larger than
     // a compress block's 64 words are not built
@@ -1815,6 +1849,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   key.plan = key.plan * 7 + (P.small_slots ? 1 : 0);
   key.plan = key.plan * 131 + (u64)P.walk_last;
   key.plan = key.plan * 5 + (u64)P.cas_mode;
+  key.plan = key.plan * 3 + (P.cas_stream ? 1 : 0);
   key.plan = key.plan * 31 + (P.adapt ? 1000 + P.adapt_shift + 100000ull * P.forming_pct : 0);
   key.plan = key.plan * 1000003ull + P.adapt_first;
   for (u64 x : P.bounds) key.plan = key.plan * 1000003ull + x;
@@ -1972,7 +2007,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
         k += wl;
       }
     } else {
-      k += 3 * iters;  // hook/compress(or jump)/step per record
+      k += (P.cas_stream ? 4 : 3) * iters;  // hook/(pick)/compress(or jump)/step per record
     }
     out.kernels = k;
   }

@@ -339,7 +339,8 @@ __global__ void k_init_pi(u32* pi, u64 n, u32* bits) {
 // hook tile).  Returns the mask of edges whose (h, l) pair in (pu, pv)
 // must be appended to the worklist (stored links and deferred walks).
 template <int S, bool SUM, bool BOTH = false, bool CAS = false>
-__device__ __forceinline__ u32 resolve_edges(const HookArgs& a, u32& links, const u32* bits,
+__device__ __forceinline__ u32 resolve_edges(const HookArgs& a, u32& links, u32& tries,
+                                             const u32* bits,
                                              const u32* s_sum, u32 star,
                                              const uint2 (&ed)[S], u32 (&pu)[S],
                                              u32 (&pv)[S]) {
@@ -433,6 +434,7 @@ __device__ __forceinline__ u32 resolve_edges(const HookArgs& a, u32& links, cons
           // link made this way is never lost, so it is not recorded and no
           // further pass has to re-check it
           const u32 old = atomicCAS(pi + pu[k], pu[k], pv[k]);
+          ++tries;
           if (old == pu[k]) {
             ++links;
             act &= ~(1u << k);
@@ -605,8 +607,9 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
     }
     if (t + gridDim.x < ntiles) load_tile(t + gridDim.x, nq);
     u32 pu[EPT], pv[EPT];
-    u32 links_unused = 0;
-    const u32 act = resolve_edges<EPT, SUM, BOTH>(a, links_unused, bits, s_sum, star, ed, pu, pv);
+    u32 links_unused = 0, tries_unused = 0;
+    const u32 act = resolve_edges<EPT, SUM, BOTH>(a, links_unused, tries_unused, bits, s_sum, star,
+                                                  ed, pu, pv);
     if (a.append) {
       u64 pos;
       if (block_reserve(__popc(act), cnt_out, pos, appended)) {
@@ -724,7 +727,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
   uint2* s_q = reinterpret_cast<uint2*>(s_sum + ((a.s0f_words + 3u) & ~3u)) +
                (size_t)warp * (32 * EPT);
   WarpOut wo;
-  u32 links = 0;  // CAS links made by this thread
+  u32 links = 0, tries = 0;  // CAS links made / CAS attempts of this thread
 
   // head / tail edges that do not fill a 16-byte pair: warp 0 of block 0
   u64 b2 = b + (b & 1ull);
@@ -735,7 +738,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
     if (lane == 0 && b2 != b) ed[0] = src[b];
     if (lane == 1 && ((e - b2) & 1ull)) ed[0] = src[e - 1];
     u32 h[1], l[1];
-    const u32 act = resolve_edges<1, false, false, CAS>(a, links, bits, s_sum, star, ed, h, l);
+    const u32 act = resolve_edges<1, false, false, CAS>(a, links, tries, bits, s_sum, star, ed, h, l);
     warp_emit<1>(a, wo, wl_out, cnt_out, lane, act, h, l);
   }
 
@@ -763,7 +766,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
     if (t + gridDim.x < ntiles) load_tile(t + gridDim.x, nq);
     if (!SUM) {
       u32 h[EPT], l[EPT];
-      const u32 act = resolve_edges<EPT, false, false, CAS>(a, links, bits, s_sum, star, ed, h, l);
+      const u32 act = resolve_edges<EPT, false, false, CAS>(a, links, tries, bits, s_sum, star, ed, h, l);
       warp_emit<EPT>(a, wo, wl_out, cnt_out, lane, act, h, l);
       continue;
     }
@@ -798,7 +801,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
         q2[j] = idx < total ? s_q[idx] : make_uint2(0u, 0u);
       }
       u32 h[S], l[S];
-      const u32 act = resolve_edges<S, true, false, CAS>(a, links, bits, s_sum, star, q2, h, l);
+      const u32 act = resolve_edges<S, true, false, CAS>(a, links, tries, bits, s_sum, star, q2, h, l);
       warp_emit<S>(a, wo, wl_out, cnt_out, lane, act, h, l);
     }
     __syncwarp();
@@ -807,6 +810,10 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
   // as stores for the plan and need a compress too)
   for (u64 i = wo.pos + lane; i < wo.end; i += 32) wl_out[i] = make_uint2(0u, 0u);
   if (CAS) {
+    // reference KernelCounters (forest.hpp:65-75): a CAS attempt is one
+    // traversal step, a CAS that did not link is a failure
+    add_counter(&r->traversal, tries);
+    add_counter(&r->cas_fail, tries - links);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) links += __shfl_xor_sync(0xffffffffu, links, o);
   }
