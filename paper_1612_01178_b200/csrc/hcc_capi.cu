@@ -92,6 +92,9 @@ constexpr int kDefaultWalkLast = 4;
 // Fig. 3's walk runs until it links (the streaming CAS hook of the adaptive
 // engine has no worklist to defer to).
 constexpr int kUnboundedWalk = 1 << 30;
+// Unrolled adaptive chains run the star pick in segments 1..kAdaptivePicks
+// (the giant has formed by then; HCC_ADAPT_PICKS overrides).
+constexpr int kAdaptivePicks = 4;
 // First adaptive topology segment = m >> kAdaptShift (HCC_PLAN=adapt:<k>).
 constexpr u32 kAdaptShift = 7;
 // Unrolled adaptive slots (HCC_PLAN=adapt:<k>:<slots>); the last takes every
@@ -467,6 +470,10 @@ HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
   a.cas = 0;
   a.ctrl = c->d_ctrl;
   a.recs = c->d_recs;
+  a.n = P.n;
+  a.rec_idx = -1;
+  a.dslot = -1;
+  a.pick = 0;
   return a;
 }
 
@@ -498,10 +505,11 @@ bool slot_small(const Plan& P, u64 sgi) {
 
 // Star-bitmap compress over the full grid (a persistent grid with cp.async
 // prefetch was slower: DESIGN.md §3.2).
-void launch_compress_s0b(hcc_ctx* c, const Plan& P, cudaStream_t s) {
+void launch_compress_s0b(hcc_ctx* c, const Plan& P, cudaStream_t s, int rec_idx = -1,
+                         int dslot = -1) {
   k_compress_s0b<<<grid_for((P.n + 7) / 8, kVertThreads, 0x7fffffffull), kVertThreads, 0, s>>>(
       P.pi, P.n, c->d_ctrl, c->d_recs, c->s0b, kCompressIfDirty, P.sum ? c->s0f : nullptr,
-      P.sum_words, P.sum_shift);
+      P.sum_words, P.sum_shift, rec_idx, dslot);
 }
 
 // Preferred shared-memory carveout (percent) of the forming-slot hook.  RMAT's
@@ -709,6 +717,33 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
       break;
     }
     default: {  // ATOMIC / ADAPTIVE
+      if (P.cas_stream && P.nseg <= kMaxUnrolledSegments && P.bounds.size() == P.nseg + 1) {
+        // unrolled: two launches per segment.  The hook's last block runs
+        // the star pick of the early segments, the compress clears the next
+        // segment's dirty flag, records are indexed by segment: no pick or
+        // step launches, no loop node (31 segments on RMAT-24: 125 -> 63
+        // kernels)
+        int picks = kAdaptivePicks;
+        if (const char* e = std::getenv("HCC_ADAPT_PICKS")) picks = std::atoi(e);
+        for (u64 i = 0; i < P.nseg; ++i) {
+          HookArgs a = hook_args(c, P, kSrcRange, 0);
+          a.b = P.bounds[i];
+          a.e = P.bounds[i + 1];
+          a.walk = kUnboundedWalk;
+          a.cas = 1;
+          a.chunked = 1;
+          a.s0b = c->s0b;
+          a.rec_idx = (int)i;
+          a.dslot = (int)(i & 1);
+          a.pick = i >= 1 && (int)i <= picks && i + 1 < P.nseg ? 1 : 0;
+          c->slot_kernel.push_back(HCC_HOOK_KERNEL_CAS);
+          k_hook_cas<<<P.grid_cas, kHookCasCta, 0, q.s()>>>(a);
+          q.phase_done(HCC_PHASE_HOOK);
+          launch_compress_s0b(c, P, q.s(), (int)i, (int)(i & 1));
+          q.phase_done(HCC_PHASE_COMPRESS);
+        }
+        break;
+      }
       if (P.cas_stream) {
         // the paper's engine on the streaming machinery: per segment, the
         // CAS-storing streaming hook (16-byte edge loads, star-bitmap
@@ -1934,14 +1969,15 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   HCC_CUDA(cudaMemcpyAsync(c->h_ctrl, c->d_ctrl, sizeof(DevCtrl),
                            cudaMemcpyDeviceToHost, c->stream));
   HCC_CUDA(cudaStreamSynchronize(c->stream));
-  const u64 nrec = std::min<u64>(c->h_ctrl->rec, kMaxRecs);
+  const bool chain = P.cas_stream && P.nseg <= kMaxUnrolledSegments && P.bounds.size() == P.nseg + 1;
+  const u64 nrec = chain ? std::min<u64>(nseg, kMaxRecs) : std::min<u64>(c->h_ctrl->rec, kMaxRecs);
   if (nrec)
     HCC_CUDA(cudaMemcpyAsync(c->h_recs, c->d_recs, nrec * sizeof(DevRec),
                              cudaMemcpyDeviceToHost, c->stream));
   HCC_CUDA(cudaStreamSynchronize(c->stream));
   const DevCtrl& hc = *c->h_ctrl;
   out.components = hc.components;
-  out.passes = hc.passes;
+  out.passes = chain ? nseg : hc.passes;
   out.edges_processed = hc.edges_processed;
   out.records = nrec;
   c->last_recs.resize(nrec);
@@ -2007,7 +2043,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
         k += wl;
       }
     } else {
-      k += (P.cas_stream ? 4 : 3) * iters;  // hook/(pick)/compress(or jump)/step per record
+      k += (chain ? 2 : P.cas_stream ? 4 : 3) * iters;  // hook/(pick)/compress(or jump)/step
     }
     out.kernels = k;
   }

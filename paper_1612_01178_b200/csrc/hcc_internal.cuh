@@ -110,6 +110,11 @@ struct DevCtrl {
   u32 star;          // its root at the last compress: bit v of the bitmap
                      // means pi(v) == star (k_compress_s0b)
   u32 use_bits;      // next plain hook looks the bitmap up (k_step_adapt)
+  // unrolled segment chains without step kernels (the adaptive engine):
+  // segment i's hook sets dirtyp[i & 1], its compress reads it and clears
+  // the other slot for segment i + 1
+  u32 dirtyp[2];
+  u32 pick_count;    // blocks of a hook that finished (last one runs the pick)
 };
 
 // k_compress_s0b modes.
@@ -141,6 +146,7 @@ constexpr u32 kAdaptFormingPct = 20;
 struct HookArgs {
   const uint2* edges;
   u64 m;
+  u64 n;             // vertices (the in-kernel star pick)
   u64 b, e;
   int mode;
   int append;        // append (H, L) of every write to the next worklist
@@ -163,6 +169,9 @@ struct HookArgs {
   uint2* wl1;
   DevCtrl* ctrl;
   DevRec* recs;
+  int rec_idx;       // record of this launch (-1: ctrl->rec)
+  int dslot;         // dirty flag: -1 ctrl->dirty, else ctrl->dirtyp[dslot]
+  int pick;          // the hook's last block runs the star pick (no k_star_pick node)
 };
 
 // Launch shape chosen on the host.
@@ -189,7 +198,7 @@ __global__ void k_compress(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
                            int skip_if_clean);
 __global__ void k_compress_s0b(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
                                u32* bits, int skip_if_clean, u32* sum, u32 sum_words,
-                               u32 sum_shift);
+                               u32 sum_shift, int rec_idx, int dslot);
 __global__ void k_start(u32* pi, u64 n, u32* bits, DevCtrl* ctrl, DevRec* recs, u64 nseg,
                         u64 m, u64 plan_first, u32* sum, u32 sum_words);
 __global__ void k_jump(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs);

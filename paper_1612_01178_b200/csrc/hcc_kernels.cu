@@ -141,6 +141,18 @@ __device__ __forceinline__ DevRec* cur_rec(DevCtrl* c, DevRec* recs) {
   return recs + (i < (u32)kMaxRecs ? i : (u32)kMaxRecs - 1);
 }
 
+// Record of a launch: explicit (unrolled chains) or the control block's.
+__device__ __forceinline__ DevRec* rec_of(DevCtrl* c, DevRec* recs, int idx) {
+  return idx >= 0 ? recs + (idx < kMaxRecs ? idx : kMaxRecs - 1) : cur_rec(c, recs);
+}
+
+__device__ __forceinline__ void set_dirty(DevCtrl* c, int dslot) {
+  if (dslot < 0)
+    c->dirty = 1;
+  else
+    c->dirtyp[dslot] = 1;
+}
+
 __device__ __forceinline__ void next_rec(DevCtrl* c, DevRec* recs) {
   if (c->rec + 1 < (u32)kMaxRecs) {
     c->rec += 1;
@@ -306,6 +318,10 @@ __global__ void k_start(u32* pi, u64 n, u32* bits, DevCtrl* ctrl, DevRec* recs, 
   }
   const u64 tid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   const u64 stride = (u64)gridDim.x * blockDim.x;
+  // records of the unrolled segments (chains without step kernels index
+  // them directly)
+  for (u64 i = 1 + tid; i < (nseg < (u64)kMaxRecs ? nseg : (u64)kMaxRecs); i += stride)
+    rec_clear(recs[i]);
   if (bits)
     for (u64 w = tid; w < ((n + 31) >> 5); w += stride) bits[w] = w == 0 ? 1u : 0u;
   if (sum)
@@ -637,6 +653,29 @@ __device__ __forceinline__ void hook_impl(const HookArgs& a) {
 }
 
 
+__device__ void star_pick_warp(const u32* pi, u64 n, DevCtrl* ctrl, u32 dirty);
+
+// The hook's last block to finish runs the star pick (the kernel's stores
+// are all visible to it: each block fences before it counts itself), so an
+// unrolled chain needs no k_star_pick launch between hook and compress.
+__device__ __forceinline__ void last_block_pick(const HookArgs& a) {
+  // (__syncthreads_or broadcasts the verdict: no static shared memory, so
+  // the plain streaming hook keeps its full-L1 configuration)
+  int last = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&a.ctrl->pick_count, 1u) == gridDim.x - 1;
+  }
+  if (!__syncthreads_or(last)) return;
+  __threadfence();
+  if (threadIdx.x < 32) {
+    const u32 d = a.dslot < 0 ? __ldcg(&a.ctrl->dirty) : __ldcg(&a.ctrl->dirtyp[a.dslot]);
+    if (d != 0 && a.n) star_pick_warp(a.pi, a.n, a.ctrl, d);
+  }
+  if (threadIdx.x == 0) a.ctrl->pick_count = 0;
+}
+
 // Per-warp output of the streaming hook: the warp's current chunk of the
 // output worklist [pos, end), its real appends and its change flag (all
 // warp-uniform).
@@ -708,7 +747,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
   u32 out;
   resolve_src(a, src, b, e, out);
   DevCtrl* ctrl = a.ctrl;
-  DevRec* r = cur_rec(ctrl, a.recs);
+  DevRec* r = rec_of(ctrl, a.recs, a.rec_idx);
   // root of the star the bitmap tracks (set by the last compress), and
   // whether the last step found the bitmap worth a lookup
   const u32 star = a.s0b ? __ldg(&ctrl->star) : 0u;
@@ -820,13 +859,14 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
   if (lane == 0) {
     if (wo.appended || links) {
       atomicAdd(&r->edges_out, (u64)wo.appended + links);
-      ctrl->dirty = 1;
+      set_dirty(ctrl, a.dslot);
     }
     if (wo.changed) {
       ctrl->changed = 1;
-      ctrl->dirty = 1;
+      set_dirty(ctrl, a.dslot);
     }
   }
+  if (a.pick) last_block_pick(a);
   block_t1(&r->hook_t1);
 }
 
@@ -976,12 +1016,20 @@ __global__ void __launch_bounds__(kVertThreads)
 // isolated; any graph whose vertex 0 is isolated), the hint moves to it.
 constexpr int kStarChase = 32;
 
+__device__ void star_pick_warp(const u32* pi, u64 n, DevCtrl* ctrl, u32 dirty);
+
 __global__ void k_star_pick(const u32* pi, u64 n, DevCtrl* ctrl) {
-  const u32 lane = threadIdx.x & 31u;
   if (threadIdx.x >= 32 || n == 0) return;
-  // A slot whose hook stored nothing skips its compress (kCompressIfDirty),
-  // so the bitmap keeps tracking the current star: it must not move.
-  if (__ldcg(&ctrl->dirty) == 0) return;
+  star_pick_warp(pi, n, ctrl, __ldcg(&ctrl->dirty));
+}
+
+// The pick itself (one full warp).  `dirty`: the slot's hook stored
+// something; a slot that stored nothing skips its compress
+// (kCompressIfDirty), so the bitmap keeps tracking the current star: it must
+// not move.
+__device__ void star_pick_warp(const u32* pi, u64 n, DevCtrl* ctrl, u32 dirty) {
+  const u32 lane = threadIdx.x & 31u;
+  if (dirty == 0) return;
   u64 hsh = (u64)(lane + 1) * 0x9E3779B97F4A7C15ull;
   hsh ^= hsh >> 29;
   hsh *= 0xBF58476D1CE4E5B9ull;
@@ -1186,9 +1234,15 @@ __device__ __forceinline__ void emit_bits(u64 chunk, u64 n, u64 v0, u32 byte, u3
 #endif
 __global__ void __launch_bounds__(kVertThreads, HCC_COMP_MINB)
     k_compress_s0b(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs, u32* bits,
-                   int mode, u32* sum, u32 sum_words, u32 sum_shift) {
-  if (mode && __ldg(&ctrl->dirty) == 0) return;
-  DevRec* r = cur_rec(ctrl, recs);
+                   int mode, u32* sum, u32 sum_words, u32 sum_shift, int rec_idx, int dslot) {
+  if (dslot >= 0) {
+    // unrolled chain: this segment's flag; clear the next segment's
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->dirtyp[dslot ^ 1] = 0;
+    if (mode && __ldg(&ctrl->dirtyp[dslot]) == 0) return;
+  } else if (mode && __ldg(&ctrl->dirty) == 0) {
+    return;
+  }
+  DevRec* r = rec_of(ctrl, recs, rec_idx);
   block_t0(&r->comp_t0);
   u64 steps = 0;
   // Two 16-byte reads and eight parent gathers in flight before any chase

@@ -652,3 +652,45 @@ def test_graph_cache_survives_buffer_regrowth(ctx, oracle):
             assert np.array_equal(lab, w)
     ga.close()
     gb.close()
+
+
+@pytest.mark.parametrize("spec", ["rmatx:scale=20,ef=16,seed=7", "erx:n=1100000,m=9000000,seed=3",
+                                  "grid:1100x1000", "erx:n=70001,m=40000,seed=9"])
+def test_adaptive_streaming_cas_engine(ctx, oracle, spec):
+    """The paper's engine on the streaming CAS hook (n >= 2^16): unrolled
+    two-launch chains (s <= 64, star pick in the hook's last block, dirty
+    flags by segment parity), the device loop (s > 64), the scalar reference
+    path (HCC_CAS_STREAM=0) and atomic (s = 1): identical labels."""
+    import os
+    g = ctx.generate(spec)
+    want = oracle.cc(g.n, g.edges())
+    for s in (0, 1, 2, 7, 64, 65, 300):
+        lab, mx = ctx.cc(g, "adaptive", segments=s)
+        assert np.array_equal(lab, want), (spec, s)
+        assert mx["components"] == int(np.sum(want == np.arange(g.n, dtype=np.uint32)))
+    lab, _ = ctx.cc(g, "atomic")
+    assert np.array_equal(lab, want)
+    for env in ({"HCC_ADAPT_PICKS": "0"}, {"HCC_ADAPT_PICKS": "64"}, {"HCC_CAS_STREAM": "0"},
+                {"HCC_S0B": "0"}):
+        os.environ.update(env)
+        try:
+            lab, _ = ctx.cc(g, "adaptive", segments=9)
+            assert np.array_equal(lab, want), (spec, env)
+        finally:
+            for k in env:
+                os.environ.pop(k, None)
+    g.close()
+
+
+@pytest.mark.parametrize("shift", [1, 977])
+def test_adaptive_star_moves_off_vertex0(ctx, oracle, shift):
+    """Vertex 0 isolated: the adaptive chain's in-hook star pick must move the
+    bitmap to the giant's root (or leave it empty) and stay exact."""
+    n = 1 << 21
+    e = oracle.gen_erx(n - shift, 5, 0, 12 * n).astype(np.uint64) + shift
+    g = ctx.graph_from_edges(e.astype(np.uint32), n)
+    want = oracle.cc(n, e)
+    for s in (0, 4, 31):
+        lab, _ = ctx.cc(g, "adaptive", segments=s)
+        assert np.array_equal(lab, want), s
+    g.close()

@@ -34,6 +34,11 @@ def main():
     ap.add_argument("--devices", default="")
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--timeline", action="store_true")
+    ap.add_argument("--ipc", type=int, default=0,
+                    help="1: open a world-1 peer arena; 2: also export + merge every rep")
+    ap.add_argument("--ballast", type=int, default=0, help="GiB of extra device memory held")
+    ap.add_argument("--smi", action="store_true", help="poll nvidia-smi like bench.py's sampler")
+    ap.add_argument("--gloo", action="store_true", help="gloo barrier before every rep")
     a = ap.parse_args()
     import torch
     devs = [int(x) for x in a.devices.split(",") if x]
@@ -41,14 +46,32 @@ def main():
     g = ctx.generate(a.spec)
     f = ctx.forest(g.n) if a.forest else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda:0")
+    ballast = torch.empty(a.ballast << 30, dtype=torch.uint8, device="cuda:0") if a.ballast else None
+    if a.ipc:
+        blob = ctx.peer_open(g.n, max(1 << 16, g.n // 64), 0, 1)
+        ctx.peer_connect(blob)
     times = []
     mx = None
+    if a.smi:
+        from bench import ClockSampler
+        sampler = ClockSampler(0)
+        sampler.start()
+    if a.gloo:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=0, world_size=1, init_method="tcp://127.0.0.1:29533")
     for i in range(a.reps + 2):
         flush.add_(1)
         torch.cuda.synchronize()
+        if a.gloo:
+            dist.barrier()
         _, mx = ctx.cc(g, a.algo, segments=a.segments, flags=a.flags, forest=f, labels=False)
         if i >= 2:
             times.append(mx["total_ms"])
+        if a.ipc == 2:
+            ctx.peer_export(f)
+            ctx.peer_merge(f)
+    if a.smi:
+        print(json.dumps(sampler.stop()))
     out = {"spec": a.spec, "algo": a.algo, "ms_mean": round(statistics.mean(times), 4),
            "ms_min": round(min(times), 4), "gteps": round(g.m / statistics.mean(times) / 1e6, 2),
            "s": mx["s"], "kernels": mx["kernels"], "components": mx["components"],
