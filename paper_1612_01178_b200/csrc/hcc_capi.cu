@@ -539,6 +539,16 @@ void launch_hook(const Plan& P, cudaStream_t s, const HookArgs& a) {
   }
 }
 
+// Segment hook of the adaptive / atomic engines (no appends).  HCC_SEG_CAS=0
+// uses the worklist passes' 768-thread k_hook_cas instead.
+void launch_seg_cas(const Plan& P, cudaStream_t s, const HookArgs& a) {
+  static const int v = std::getenv("HCC_SEG_CAS") ? std::atoi(std::getenv("HCC_SEG_CAS")) : 1;
+  if (v)
+    k_hook_seg_cas<<<P.grid_hook, kHookCta, 0, s>>>(a);
+  else
+    k_hook_cas<<<P.grid_cas, kHookCasCta, 0, s>>>(a);
+}
+
 // The summary hook (one CTA per SM, the summary and queues in shared memory).
 void launch_hook_sum(hcc_ctx* c, cudaStream_t s, const HookArgs& a) {
   if (a.cas)
@@ -737,7 +747,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           a.dslot = (int)(i & 1);
           a.pick = i >= 1 && (int)i <= picks && i + 1 < P.nseg ? 1 : 0;
           c->slot_kernel.push_back(HCC_HOOK_KERNEL_CAS);
-          k_hook_cas<<<P.grid_cas, kHookCasCta, 0, q.s()>>>(a);
+          launch_seg_cas(P, q.s(), a);
           q.phase_done(HCC_PHASE_HOOK);
           launch_compress_s0b(c, P, q.s(), (int)i, (int)(i & 1));
           q.phase_done(HCC_PHASE_COMPRESS);
@@ -757,7 +767,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           a.cas = 1;
           a.chunked = 1;
           a.s0b = c->s0b;
-          k_hook_cas<<<P.grid_cas, kHookCasCta, 0, q.s()>>>(a);
+          launch_seg_cas(P, q.s(), a);
           q.phase_done(HCC_PHASE_HOOK);
           k_star_pick<<<1, 32, 0, q.s()>>>(P.pi, P.n, ctrl);
           launch_compress_s0b(c, P, q.s());

@@ -83,6 +83,32 @@ __device__ __forceinline__ u32 ld_bits(const u32* p) {
   u32 r;
   asm volatile("ld.global.nc.L1::evict_last.u32 %0, [%1];" : "=r"(r) : "l"(p));
   return r;
+#elif HCC_BITLOAD == 2
+  // L2 evict-last: keep the (32 MiB at RMAT-28) bitmap resident against
+  // the random pi sectors of the large-pi regime
+  u32 r;
+  u64 pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+#else
+  return *p;
+#endif
+}
+
+// First pi gather of an endpoint outside the star: in the large-pi regime
+// (pi >> L2) these sectors are rarely reused; HCC_PIGATHER=1 tags them L2
+// evict-first.
+#ifndef HCC_PIGATHER
+#define HCC_PIGATHER 0
+#endif
+__device__ __forceinline__ u32 ld_pi_gather(const u32* p) {
+#if HCC_PIGATHER == 1
+  u32 r;
+  u64 pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
 #else
   return *p;
 #endif
@@ -378,8 +404,8 @@ __device__ __forceinline__ u32 resolve_edges(const HookArgs& a, u32& links, u32&
     }
 #pragma unroll
     for (int k = 0; k < S; ++k) {
-      pu[k] = (wu[k] >> (ed[k].x & 31u)) & 1u ? star : ld_pi(pi + ed[k].x);
-      pv[k] = (wv[k] >> (ed[k].y & 31u)) & 1u ? star : ld_pi(pi + ed[k].y);
+      pu[k] = (wu[k] >> (ed[k].x & 31u)) & 1u ? star : ld_pi_gather(pi + ed[k].x);
+      pv[k] = (wv[k] >> (ed[k].y & 31u)) & 1u ? star : ld_pi_gather(pi + ed[k].y);
     }
   } else {
 #pragma unroll
@@ -726,6 +752,17 @@ __device__ __forceinline__ void warp_emit(const HookArgs& a, WarpOut& w, uint2* 
   w.appended += total;
 }
 
+// warp_emit, or (a launch that appends nothing: the adaptive engine's CAS
+// segments) only the change flag.
+template <int N, bool APPEND>
+__device__ __forceinline__ void emit(const HookArgs& a, WarpOut& w, uint2* wl_out, u64* cnt_out,
+                                     u32 lane, u32 act, const u32 (&h)[N], const u32 (&l)[N]) {
+  if (APPEND)
+    warp_emit<N>(a, w, wl_out, cnt_out, lane, act, h, l);
+  else if (__any_sync(0xffffffffu, act != 0))
+    w.changed = 1;
+}
+
 // Streaming hook for full-warp launches: no block barriers after the
 // prologue; appends go to per-warp chunks of the output worklist (one
 // global atomic per kWlChunk records; a chunk's unused tail is padded with
@@ -739,7 +776,7 @@ __device__ __forceinline__ void warp_emit(const HookArgs& a, WarpOut& w, uint2* 
 // lane per round.  Otherwise (k_hook: no shared memory, so L1 keeps its full
 // size for the bitmap's hot words; e.g. RMAT, whose isolated vertices break
 // most words) every edge takes the bitmap / gather path directly.
-template <int EPT, bool SUM, bool CAS = false>
+template <int EPT, bool SUM, bool CAS = false, bool APPEND = true>
 __device__ __forceinline__ void hook_stream(const HookArgs& a) {
   constexpr int S = kHookSlow;
   const uint2* src;
@@ -778,35 +815,42 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
     if (lane == 1 && ((e - b2) & 1ull)) ed[0] = src[e - 1];
     u32 h[1], l[1];
     const u32 act = resolve_edges<1, false, false, CAS>(a, links, tries, bits, s_sum, star, ed, h, l);
-    warp_emit<1>(a, wo, wl_out, cnt_out, lane, act, h, l);
+    emit<1, APPEND>(a, wo, wl_out, cnt_out, lane, act, h, l);
   }
 
   const uint4* s4 = reinterpret_cast<const uint4*>(src + b2);
   const u64 pol = policy_evict_first();
-  const u64 tile = (u64)blockDim.x * (EPT / 2);
+  // Warp tiles: 32 lanes x EPT/2 16-byte loads (256 edges), the block's
+  // warps on consecutive tiles (a 128 KB stretch per block and round).  A
+  // warp that runs out of tiles frees its SM's issue slots to the others, so
+  // a short launch (an adaptive segment: ~7 block tiles per SM) no longer
+  // idles whole blocks behind the last round's stragglers.
+  const u64 tile = 32ull * (EPT / 2);
   const u64 ntiles = (n4 + tile - 1) / tile;
+  const u64 wpb = blockDim.x >> 5;
+  const u64 gw = (u64)blockIdx.x * wpb + warp, wstride = (u64)gridDim.x * wpb;
   // Out-of-range slots become the self-loop (0,0): a no-op hook.
   auto load_tile = [&](u64 t, uint4* q) {
 #pragma unroll
     for (int j = 0; j < EPT / 2; ++j) {
-      const u64 i = t * tile + (u64)j * blockDim.x + threadIdx.x;
+      const u64 i = t * tile + (u64)j * 32 + lane;
       q[j] = i < n4 ? ld_stream16(s4 + i, pol) : make_uint4(0u, 0u, 0u, 0u);
     }
   };
   uint4 nq[EPT / 2];
-  if ((u64)blockIdx.x < ntiles) load_tile(blockIdx.x, nq);
-  for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  if (gw < ntiles) load_tile(gw, nq);
+  for (u64 t = gw; t < ntiles; t += wstride) {
     uint2 ed[EPT];
 #pragma unroll
     for (int j = 0; j < EPT / 2; ++j) {
       ed[2 * j] = make_uint2(nq[j].x, nq[j].y);
       ed[2 * j + 1] = make_uint2(nq[j].z, nq[j].w);
     }
-    if (t + gridDim.x < ntiles) load_tile(t + gridDim.x, nq);
+    if (t + wstride < ntiles) load_tile(t + wstride, nq);
     if (!SUM) {
       u32 h[EPT], l[EPT];
       const u32 act = resolve_edges<EPT, false, false, CAS>(a, links, tries, bits, s_sum, star, ed, h, l);
-      warp_emit<EPT>(a, wo, wl_out, cnt_out, lane, act, h, l);
+      emit<EPT, APPEND>(a, wo, wl_out, cnt_out, lane, act, h, l);
       continue;
     }
     // fast path: both endpoints in summary-covered words (or a self loop)
@@ -841,7 +885,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
       }
       u32 h[S], l[S];
       const u32 act = resolve_edges<S, true, false, CAS>(a, links, tries, bits, s_sum, star, q2, h, l);
-      warp_emit<S>(a, wo, wl_out, cnt_out, lane, act, h, l);
+      emit<S, APPEND>(a, wo, wl_out, cnt_out, lane, act, h, l);
     }
     __syncwarp();
   }
@@ -896,6 +940,12 @@ __global__ void __launch_bounds__(kHookCasCta, 1) k_hook_cas(HookArgs a) {
 __global__ void __launch_bounds__(kHookCasCta, 1) k_hook_sum_cas(HookArgs a) {
   if (a.gate == kGateIfSum && !__ldg(&a.ctrl->use_sum)) return;
   hook_stream<kHookEPT, true, true>(a);
+}
+
+// Segment hook of the adaptive / atomic engines: CAS stores, unbounded
+// walks, nothing appended (no chunk state), so it fits 1024-thread CTAs.
+__global__ void __launch_bounds__(kHookCta, HCC_HOOK_MINB) k_hook_seg_cas(HookArgs a) {
+  hook_stream<kHookEPT, false, true, false>(a);
 }
 
 // Streaming hook with the star-0 summary in shared memory (full warps,
