@@ -203,6 +203,7 @@ struct hcc_ctx {
   std::vector<int> slot_kernel, exec_slot_kernel;
   int wl_kernel = 0, exec_wl_kernel = 0;
   u32* s0b = nullptr;  // star-0 bitmap
+  u32* s0b_base = nullptr;  // its allocation
   u64 s0b_words = 0;
   u32* s0f = nullptr;  // star-0 summary (one bit per group of bitmap words)
   u64 s0f_words = 0;
@@ -303,10 +304,14 @@ void ensure_wl(hcc_ctx* c, u64 cap) {
 void ensure_s0b(hcc_ctx* c, u64 nwords) {
   if (c->s0b_words >= nwords) return;
   drop_exec(c);
-  if (c->s0b) HCC_CUDA(cudaFree(c->s0b));
-  c->s0b = nullptr;
+  if (c->s0b_base) HCC_CUDA(cudaFree(c->s0b_base));
+  c->s0b = c->s0b_base = nullptr;
   c->s0b_words = 0;
-  HCC_CUDA(cudaMalloc(&c->s0b, std::max<u64>(nwords, 1) * sizeof(u32)));
+  // HCC_S0B_PAD (bytes, experiment): offset of the bitmap inside its
+  // allocation (L2 set aliasing against pi)
+  const u64 pad = std::getenv("HCC_S0B_PAD") ? std::strtoull(std::getenv("HCC_S0B_PAD"), nullptr, 0) : 0;
+  HCC_CUDA(cudaMalloc(&c->s0b_base, std::max<u64>(nwords, 1) * sizeof(u32) + pad));
+  c->s0b = reinterpret_cast<u32*>(reinterpret_cast<char*>(c->s0b_base) + (pad & ~15ull));
   c->s0b_words = nwords;
 }
 
@@ -447,6 +452,7 @@ struct Plan {
   unsigned grid_hook, block_hook, grid_vert, block_vert;
   unsigned grid_cas = 1;    // k_hook_cas grid (kHookCasCta threads per CTA)
   bool cas_stream = false;  // atomic / adaptive on the streaming CAS hook
+  bool dyn = true;          // streaming hooks take tiles dynamically (HCC_DYN=0: static)
 };
 
 HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
@@ -474,6 +480,7 @@ HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
   a.rec_idx = -1;
   a.dslot = -1;
   a.pick = 0;
+  a.dyn = 0;
   return a;
 }
 
@@ -638,6 +645,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
                            kHookThreads, 0, q.s()>>>(ha);
           } else {
             ha.chunked = P.chunked ? 1 : 0;
+            ha.dyn = P.dyn && P.chunked ? 1 : 0;
             ha.cas = P.cas_mode >= 2 && sgi + 1 == P.nseg ? 1 : 0;
             if (P.adapt && sgi + 1 == P.nseg) ha.walk = P.walk_last;
             HookArgs hp = ha;  // plain streaming hook: bitmap only, full L1
@@ -701,6 +709,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
         HookArgs wa = hook_args(c, P, kSrcWorklist, 1);
         if (P.s0b && !P.bounds.empty()) use_s0b(c, P, wa);
         wa.chunked = P.chunked ? 1 : 0;
+        wa.dyn = P.dyn && P.chunked ? 1 : 0;
         wa.cas = P.cas_mode >= 1 && P.chunked ? 1 : 0;
         c->wl_kernel = wa.cas ? HCC_HOOK_KERNEL_CAS
                               : (P.chunked ? HCC_HOOK_KERNEL_STREAM : HCC_HOOK_KERNEL_LEGACY);
@@ -745,6 +754,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           a.s0b = c->s0b;
           a.rec_idx = (int)i;
           a.dslot = (int)(i & 1);
+          a.dyn = P.dyn ? 1 : 0;
           a.pick = i >= 1 && (int)i <= picks && i + 1 < P.nseg ? 1 : 0;
           c->slot_kernel.push_back(HCC_HOOK_KERNEL_CAS);
           launch_seg_cas(P, q.s(), a);
@@ -767,6 +777,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           a.cas = 1;
           a.chunked = 1;
           a.s0b = c->s0b;
+          a.dyn = P.dyn ? 1 : 0;
           launch_seg_cas(P, q.s(), a);
           q.phase_done(HCC_PHASE_HOOK);
           k_star_pick<<<1, 32, 0, q.s()>>>(P.pi, P.n, ctrl);
@@ -1091,7 +1102,7 @@ int hcc_destroy(hcc_ctx* c) {
   cudaFree(c->scratch_pi);
   cudaFree(c->wl[0]);
   cudaFree(c->wl[1]);
-  cudaFree(c->s0b);
+  cudaFree(c->s0b_base);
   cudaFree(c->s0f);
   for (cudaEvent_t ev : c->seg_ev) cudaEventDestroy(ev);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -1777,6 +1788,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   P.hook_events = (o->flags & HCC_FLAG_HOOK_EVENTS) != 0;
   if (const char* e = std::getenv("HCC_HOOK_SMALL")) P.small_slots = std::atoi(e) != 0;
   if (const char* e = std::getenv("HCC_HOOK_CAS")) P.cas_mode = std::atoi(e);
+  if (const char* e = std::getenv("HCC_DYN")) P.dyn = std::atoi(e) != 0;
   P.forming_pct = std::getenv("HCC_FORMING_PCT") ? (u32)std::atoi(std::getenv("HCC_FORMING_PCT"))
                                                   : kAdaptFormingPct;
   if (P.s0b) {
@@ -1858,6 +1870,21 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
                           !(o->flags & (HCC_FLAG_HOST_LOOP | HCC_FLAG_NO_GRAPH));
   out.used_device_loop = graph_mode ? 1 : 0;
 
+  // HCC_APW=1 (experiment): persisting L2 access-policy window over the star
+  // bitmap on the launch stream (applies to eager launches)
+  if (const char* e = std::getenv("HCC_APW")) {
+    if (std::atoi(e) && P.s0b) {
+      const size_t bytes = (size_t)((n + 31) / 32) * 4;
+      HCC_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes));
+      cudaStreamAttrValue v = {};
+      v.accessPolicyWindow.base_ptr = c->s0b;
+      v.accessPolicyWindow.num_bytes = bytes;
+      v.accessPolicyWindow.hitRatio = 1.0f;
+      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      HCC_CUDA(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v));
+    }
+  }
   Seq q;
   q.c = c;
   q.graph_mode = graph_mode;
@@ -1895,6 +1922,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   key.plan = key.plan * 131 + (u64)P.walk_last;
   key.plan = key.plan * 5 + (u64)P.cas_mode;
   key.plan = key.plan * 3 + (P.cas_stream ? 1 : 0);
+  key.plan = key.plan * 3 + (P.dyn ? 1 : 0);
   key.plan = key.plan * 31 + (P.adapt ? 1000 + P.adapt_shift + 100000ull * P.forming_pct : 0);
   key.plan = key.plan * 1000003ull + P.adapt_first;
   for (u64 x : P.bounds) key.plan = key.plan * 1000003ull + x;
@@ -2554,12 +2582,16 @@ namespace {
 
 // fn(r) on one host thread per shard; the first failure's message is moved
 // to the calling thread (g_err is thread-local).
+// HCC_MULTI_SERIAL=1 runs the shards one after another on one thread: on a
+// single GPU hosting every shard, each shard's phases then run alone, which
+// is the per-rank cost an N-GPU run would see (tools/scale_model.py).
 int for_shards(int G, const std::function<int(int)>& fn) {
   std::vector<int> rc(G, 0);
   std::vector<std::string> msg(G);
   std::vector<std::thread> th;
   th.reserve(G);
-  for (int r = 0; r < G; ++r)
+  static const bool serial = std::getenv("HCC_MULTI_SERIAL") && std::atoi(std::getenv("HCC_MULTI_SERIAL"));
+  for (int r = 0; r < G; ++r) {
     th.emplace_back([&, r] {
       try {
         rc[r] = fn(r);
@@ -2572,7 +2604,10 @@ int for_shards(int G, const std::function<int(int)>& fn) {
       }
       if (rc[r]) msg[r] = g_err;
     });
-  for (std::thread& t : th) t.join();
+    if (serial) th.back().join();
+  }
+  for (std::thread& t : th)
+    if (t.joinable()) t.join();
   for (int r = 0; r < G; ++r)
     if (rc[r]) {
       g_err = msg[r];

@@ -115,6 +115,8 @@ struct DevCtrl {
   // the other slot for segment i + 1
   u32 dirtyp[2];
   u32 pick_count;    // blocks of a hook that finished (last one runs the pick)
+  u32 tile_ctr;      // next warp tile of a dynamically scheduled hook; every
+                     // compress (and k_start) resets it for the next hook
 };
 
 // k_compress_s0b modes.
@@ -172,6 +174,8 @@ struct HookArgs {
   int rec_idx;       // record of this launch (-1: ctrl->rec)
   int dslot;         // dirty flag: -1 ctrl->dirty, else ctrl->dirtyp[dslot]
   int pick;          // the hook's last block runs the star pick (no k_star_pick node)
+  int dyn;           // warps take tiles from ctrl->tile_ctr (reset by the next
+                     // compress) instead of a static round-robin
 };
 
 // Launch shape chosen on the host.

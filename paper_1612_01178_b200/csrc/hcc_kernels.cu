@@ -826,27 +826,51 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
   // a short launch (an adaptive segment: ~7 block tiles per SM) no longer
   // idles whole blocks behind the last round's stragglers.
   const u64 tile = 32ull * (EPT / 2);
-  const u64 ntiles = (n4 + tile - 1) / tile;
-  const u64 wpb = blockDim.x >> 5;
-  const u64 gw = (u64)blockIdx.x * wpb + warp, wstride = (u64)gridDim.x * wpb;
+  // tile indices fit 32 bits (a tile is 256 edges)
+  const u32 ntiles = (u32)((n4 + tile - 1) / tile);
+  const u32 wpb = blockDim.x >> 5;
+  const u32 gw = blockIdx.x * wpb + warp, wstride = gridDim.x * wpb;
   // Out-of-range slots become the self-loop (0,0): a no-op hook.
-  auto load_tile = [&](u64 t, uint4* q) {
+  auto load_tile = [&](u32 t, uint4* q) {
 #pragma unroll
     for (int j = 0; j < EPT / 2; ++j) {
-      const u64 i = t * tile + (u64)j * 32 + lane;
+      const u64 i = (u64)t * tile + (u64)j * 32 + lane;
       q[j] = i < n4 ? ld_stream16(s4 + i, pol) : make_uint4(0u, 0u, 0u, 0u);
     }
   };
+  // Dynamic schedule (a.dyn, launches of >= 32 tiles per warp): each warp
+  // starts on a static chunk of kch tiles, then takes further chunks from a
+  // global counter; the next chunk is requested halfway through the current
+  // one, so the atomic's latency hides behind work and the requests of a
+  // launch's warps do not arrive as one burst.  A static round-robin let
+  // warps on slow SMs trail: RMAT-28's steady hook ran 5.5 ms past its
+  // median block for some placements of the star bitmap.
+  const u32 tpw = ntiles / wstride;
+  const bool dyn = a.dyn && tpw >= 32;
+  const u32 kch = tpw / 16 < 4 ? 4 : tpw / 16 > 64 ? 64 : tpw / 16;
+  u32 cbase = gw * kch;  // current chunk
+  u32 nreq = 0;          // lane 0: reply for the next chunk
+  auto next_of = [&](u32 t) -> u32 {
+    if (!dyn) return t + wstride;
+    const u32 k = t + 1 - cbase;
+    if (k == kch / 2 && lane == 0) nreq = atomicAdd(&ctrl->tile_ctr, kch);
+    if (k < kch) return t + 1;
+    cbase = wstride * kch + __shfl_sync(0xffffffffu, nreq, 0);
+    return cbase;
+  };
+  const u32 t0 = dyn ? cbase : gw;
   uint4 nq[EPT / 2];
-  if (gw < ntiles) load_tile(gw, nq);
-  for (u64 t = gw; t < ntiles; t += wstride) {
+  if (t0 < ntiles) load_tile(t0, nq);
+  for (u32 t = t0; t < ntiles;) {
     uint2 ed[EPT];
 #pragma unroll
     for (int j = 0; j < EPT / 2; ++j) {
       ed[2 * j] = make_uint2(nq[j].x, nq[j].y);
       ed[2 * j + 1] = make_uint2(nq[j].z, nq[j].w);
     }
-    if (t + wstride < ntiles) load_tile(t + wstride, nq);
+    const u32 tn = next_of(t);
+    if (tn < ntiles) load_tile(tn, nq);
+    t = tn;
     if (!SUM) {
       u32 h[EPT], l[EPT];
       const u32 act = resolve_edges<EPT, false, false, CAS>(a, links, tries, bits, s_sum, star, ed, h, l);
@@ -1006,6 +1030,7 @@ __global__ void __launch_bounds__(kHookCta) k_cas_hook(HookArgs a) {
 // whose lanes are all in that state exit the chase loop together.
 __global__ void __launch_bounds__(kVertThreads)
     k_compress(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs, int skip_if_clean) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->tile_ctr = 0;  // next hook's schedule
   if (skip_if_clean && __ldg(&ctrl->dirty) == 0) return;
   DevRec* r = cur_rec(ctrl, recs);
   block_t0(&r->comp_t0);
@@ -1285,6 +1310,7 @@ __device__ __forceinline__ void emit_bits(u64 chunk, u64 n, u64 v0, u32 byte, u3
 __global__ void __launch_bounds__(kVertThreads, HCC_COMP_MINB)
     k_compress_s0b(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs, u32* bits,
                    int mode, u32* sum, u32 sum_words, u32 sum_shift, int rec_idx, int dslot) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->tile_ctr = 0;  // next hook's schedule
   if (dslot >= 0) {
     // unrolled chain: this segment's flag; clear the next segment's
     if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->dirtyp[dslot ^ 1] = 0;

@@ -39,9 +39,13 @@ def main():
     ap.add_argument("--ballast", type=int, default=0, help="GiB of extra device memory held")
     ap.add_argument("--smi", action="store_true", help="poll nvidia-smi like bench.py's sampler")
     ap.add_argument("--gloo", action="store_true", help="gloo barrier before every rep")
+    ap.add_argument("--noflush", action="store_true", help="no L2 flush between reps")
+    ap.add_argument("--thread", action="store_true", help="run each CC on a fresh host thread")
+    ap.add_argument("--extractx", action="store_true", help="create a second context first")
     a = ap.parse_args()
     import torch
     devs = [int(x) for x in a.devices.split(",") if x]
+    extra = capi.Context(0) if a.extractx else None
     ctx = capi.Context(devices=devs) if devs else capi.Context(0)
     g = ctx.generate(a.spec)
     f = ctx.forest(g.n) if a.forest else None
@@ -60,11 +64,21 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("gloo", rank=0, world_size=1, init_method="tcp://127.0.0.1:29533")
     for i in range(a.reps + 2):
-        flush.add_(1)
+        if not a.noflush:
+            flush.add_(1)
         torch.cuda.synchronize()
         if a.gloo:
             dist.barrier()
-        _, mx = ctx.cc(g, a.algo, segments=a.segments, flags=a.flags, forest=f, labels=False)
+        if a.thread:
+            import threading
+            box = {}
+            th = threading.Thread(target=lambda: box.update(
+                r=ctx.cc(g, a.algo, segments=a.segments, flags=a.flags, forest=f, labels=False)))
+            th.start()
+            th.join()
+            _, mx = box["r"]
+        else:
+            _, mx = ctx.cc(g, a.algo, segments=a.segments, flags=a.flags, forest=f, labels=False)
         if i >= 2:
             times.append(mx["total_ms"])
         if a.ipc == 2:
@@ -90,6 +104,8 @@ def main():
             import oracle as O
             out["exact"] = bool(np.array_equal(lab, O.cc(g.n, g.edges())))
     print(json.dumps(out), flush=True)
+    if devs:
+        out["shards"] = ctx.shard_metrics()
     if a.timeline and not devs:
         for r in ctx.segments():
             print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()}),
