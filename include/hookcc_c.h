@@ -349,6 +349,8 @@ typedef struct hcc_shard_metrics {
   uint64_t records_merged;  /* remote relations this shard re-hooked         */
   uint64_t rehook_passes;
   uint64_t bitmap_bytes;    /* exported bitmap size                          */
+  uint64_t roots_linked;    /* local roots the gather linked to 0 in place
+                               (peers' star-of-0 members this shard lacked) */
   int device;
   int peer_access;          /* 1: exports read over P2P                      */
 } hcc_shard_metrics;

@@ -67,7 +67,8 @@ class GraphStats(C.Structure):
 class ShardMetrics(C.Structure):
     _fields_ = [("total_ms", C.c_double), ("local_ms", C.c_double), ("merge_ms", C.c_double),
                 ("span_ms", C.c_double), ("pairs_exported", u64), ("records_merged", u64),
-                ("rehook_passes", u64), ("bitmap_bytes", u64), ("device", i32),
+                ("rehook_passes", u64), ("bitmap_bytes", u64), ("roots_linked", u64),
+                ("device", i32),
                 ("peer_access", i32)]
 
 

@@ -138,7 +138,7 @@ struct MergeShard {
   cudaEvent_t ev_exp = nullptr, ev_t0 = nullptr, ev_m0 = nullptr, ev_t1 = nullptr;
   hcc_forest* forest = nullptr;  // local forest (shard 0 may use the caller's)
   double local_ms = 0, merge_ms = 0, total_ms = 0;
-  u64 passes = 0, records = 0, exported = 0;
+  u64 passes = 0, records = 0, exported = 0, linked = 0;
 };
 
 struct GraphKey {
@@ -2694,14 +2694,15 @@ void merge_shard(hcc_ctx* c, int r, hcc_forest* f, u64 records_cap) {
   k_begin<<<1, 1, 0, sc->stream>>>(sc->d_ctrl, sc->d_recs, 1);
   k_merge_gather<<<std::max<unsigned>(1u, (unsigned)sc->sms * 8u), 256, 0, sc->stream>>>(
       ms.tab, (u32)r, f->d_pi, n, sc->wl[0], &sc->d_ctrl->wl_count[0], sc->wl_cap,
-      &sc->d_ctrl->err);
+      &sc->d_ctrl->err, &sc->d_ctrl->dirty, &sc->d_ctrl->merged_links);
   HCC_CUDA(cudaGetLastError());
   rehook_loop(sc, P);
+  HCC_CUDA(cudaEventRecord(ms.ev_t1, sc->stream));
+  // components (metrics only, after the timed region)
   if (r == 0)
     k_count_roots<<<grid_for(n, 256, (u64)sc->sms * 16), 256, 0, sc->stream>>>(f->d_pi, n,
                                                                               sc->d_ctrl);
   HCC_CUDA(cudaGetLastError());
-  HCC_CUDA(cudaEventRecord(ms.ev_t1, sc->stream));
   HCC_CUDA(cudaMemcpyAsync(sc->h_ctrl, sc->d_ctrl, sizeof(DevCtrl), cudaMemcpyDeviceToHost,
                            sc->stream));
   HCC_CUDA(cudaMemcpyAsync(sc->h_recs, sc->d_recs, sizeof(DevRec), cudaMemcpyDeviceToHost,
@@ -2715,6 +2716,7 @@ void merge_shard(hcc_ctx* c, int r, hcc_forest* f, u64 records_cap) {
   ms.total_ms = ms_total;
   ms.passes += sc->h_ctrl->passes;
   ms.records += sc->h_recs[0].edges_in;
+  ms.linked += sc->h_ctrl->merged_links;
 }
 
 }  // namespace
@@ -2860,7 +2862,7 @@ static int multi_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o_in, hcc_fo
         if (int st = hcc_forest_create(c->subs[r], n, &ms.forest)) return st;
       }
       ms.local_ms = ms.merge_ms = ms.total_ms = 0;
-      ms.passes = ms.records = ms.exported = 0;
+      ms.passes = ms.records = ms.exported = ms.linked = 0;
     }
   } catch (const CudaFail& fl) {
     return fl.code;
@@ -3029,6 +3031,7 @@ int hcc_ctx_shard_metrics(hcc_ctx* c, hcc_shard_metrics* out, uint64_t cap, uint
     x.records_merged = ms.records;
     x.rehook_passes = ms.passes;
     x.bitmap_bytes = ms.bits_words * 4;
+    x.roots_linked = ms.linked;
     x.device = c->subs[r]->dev;
     x.peer_access = c->peer_access;
     out[r] = x;
@@ -3222,13 +3225,14 @@ int hcc_peer_merge(hcc_ctx* c, hcc_forest* f, hcc_metrics* mx, int* overflow) {
   k_begin<<<1, 1, 0, c->stream>>>(c->d_ctrl, c->d_recs, 1);
   k_merge_gather<<<std::max<unsigned>(1u, (unsigned)c->sms * 8u), 256, 0, c->stream>>>(
       p->d_tab, (u32)p->rank, f->d_pi, n, c->wl[0], &c->d_ctrl->wl_count[0], c->wl_cap,
-      &c->d_ctrl->err);
+      &c->d_ctrl->err, &c->d_ctrl->dirty, &c->d_ctrl->merged_links);
   HCC_CUDA(cudaGetLastError());
   rehook_loop(c, P);
+  HCC_CUDA(cudaEventRecord(p->ev_m1, c->stream));
+  // components (metrics only, after the timed region)
   k_count_roots<<<grid_for(n, 256, (u64)c->sms * 16), 256, 0, c->stream>>>(f->d_pi, n,
                                                                          c->d_ctrl);
   HCC_CUDA(cudaGetLastError());
-  HCC_CUDA(cudaEventRecord(p->ev_m1, c->stream));
   HCC_CUDA(cudaMemcpyAsync(c->h_ctrl, c->d_ctrl, sizeof(DevCtrl), cudaMemcpyDeviceToHost,
                            c->stream));
   HCC_CUDA(cudaMemcpyAsync(c->h_recs, c->d_recs, sizeof(DevRec), cudaMemcpyDeviceToHost,

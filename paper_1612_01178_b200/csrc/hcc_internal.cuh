@@ -115,6 +115,7 @@ struct DevCtrl {
   // the other slot for segment i + 1
   u32 dirtyp[2];
   u32 pick_count;    // blocks of a hook that finished (last one runs the pick)
+  u64 merged_links;  // roots a multi-GPU merge linked to 0 in place
   u32 tile_ctr;      // next warp tile of a dynamically scheduled hook; every
                      // compress (and k_start) resets it for the next hook
 };
@@ -260,8 +261,8 @@ struct PeerTab {
   const u64* count[kMaxShards];   // pairs rank r produced (may exceed cap)
   u64 cap[kMaxShards];
 };
-__global__ void k_merge_gather(const PeerTab* tab, u32 self, const u32* pi, u64 n, uint2* wl,
-                               u64* count, u64 cap, u32* err);
+__global__ void k_merge_gather(const PeerTab* tab, u32 self, u32* pi, u64 n, uint2* wl,
+                               u64* count, u64 cap, u32* err, u32* dirty, u64* linked);
 __global__ void k_decode_bits(const u32* rows, u64 nrows, u64 stride, u64 skip, const u32* pi,
                               u64 n, uint2* wl, u64* count);
 

@@ -41,13 +41,18 @@ def main():
     ap.add_argument("--gloo", action="store_true", help="gloo barrier before every rep")
     ap.add_argument("--noflush", action="store_true", help="no L2 flush between reps")
     ap.add_argument("--thread", action="store_true", help="run each CC on a fresh host thread")
+    ap.add_argument("--range", default="", help="first,count: one shard of the spec")
     ap.add_argument("--extractx", action="store_true", help="create a second context first")
     a = ap.parse_args()
     import torch
     devs = [int(x) for x in a.devices.split(",") if x]
     extra = capi.Context(0) if a.extractx else None
     ctx = capi.Context(devices=devs) if devs else capi.Context(0)
-    g = ctx.generate(a.spec)
+    if a.range:
+        first, count = (int(x) for x in a.range.split(","))
+        g = ctx.generate_range(a.spec, first, count)
+    else:
+        g = ctx.generate(a.spec)
     f = ctx.forest(g.n) if a.forest else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda:0")
     ballast = torch.empty(a.ballast << 30, dtype=torch.uint8, device="cuda:0") if a.ballast else None

@@ -55,6 +55,7 @@ def main():
             per.append({"shard": r, "local_ms": round(loc, 3), "merge_ms": round(mer, 3),
                         "nvlink_ms": round(nvl, 3), "records_merged": steps[-1][r]["records_merged"],
                         "rehook_passes": steps[-1][r]["rehook_passes"],
+                        "roots_linked": steps[-1][r]["roots_linked"],
                         "pairs_exported": steps[-1][r]["pairs_exported"]})
         t = max(p["local_ms"] + p["merge_ms"] + p["nvlink_ms"] for p in per)
         row = {"n_gpus": N, "spec": a.spec, "m": g.m, "pred_ms_per_step": round(t, 3),
