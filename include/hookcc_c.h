@@ -168,6 +168,7 @@ typedef struct hcc_segment_rec {
 #define HCC_HOOK_KERNEL_SUM    3  /* k_hook_sum: + shared-memory star summary */
 #define HCC_HOOK_KERNEL_CAS    4  /* k_hook_cas / k_hook_sum_cas (worklist)   */
 #define HCC_HOOK_KERNEL_LEGACY 5  /* k_hook_legacy / k_cas_hook                */
+#define HCC_HOOK_KERNEL_SUMD   6  /* k_hook_sumd: summary-predicated lookups  */
 
 /* Reference GraphStats (graph.hpp:33-40), computed on the device. */
 typedef struct hcc_graph_stats {

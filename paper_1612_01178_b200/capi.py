@@ -23,7 +23,7 @@ FLAG_FULL_PASSES, FLAG_HOST_LOOP, FLAG_NO_GRAPH, FLAG_CHECK_STAR = 0x1, 0x2, 0x4
 FLAG_HOOK_EVENTS = 0x10
 ABI_VERSION = 4  # HCC_ABI_VERSION of include/hookcc_c.h
 HOOK_KERNELS = {1: "k_hook_small", 2: "k_hook", 3: "k_hook_sum", 4: "k_hook_cas",
-                5: "k_hook_legacy"}
+                5: "k_hook_legacy", 6: "k_hook_sumd"}
 PHASE_HOOK, PHASE_COMPRESS = 0, 1
 
 u64, u32, i32 = C.c_uint64, C.c_uint32, C.c_int

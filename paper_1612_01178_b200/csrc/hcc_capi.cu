@@ -178,7 +178,8 @@ struct hcc_ctx {
   uint2* wl[2] = {nullptr, nullptr};
   u64 wl_cap = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  int occ_hook = 1, occ_vert = 1, occ_hook_sum = 1, occ_hook_cas = 1, occ_hook_sum_cas = 1;
+  int occ_hook = 1, occ_vert = 1, occ_hook_sum = 1, occ_hook_cas = 1, occ_hook_sum_cas = 1,
+      occ_hook_sumd = 1;
   // cached executable graph for repeated calls with identical arguments,
   // plus the previous one (two graphs used alternately, e.g. a pipelined
   // upload into one while the other runs, keep both instantiated)
@@ -453,6 +454,14 @@ struct Plan {
   unsigned grid_cas = 1;    // k_hook_cas grid (kHookCasCta threads per CTA)
   bool cas_stream = false;  // atomic / adaptive on the streaming CAS hook
   bool dyn = true;          // streaming hooks take tiles dynamically (HCC_DYN=0: static)
+  bool wide_compress = false;  // k_compress_s0b_w (n >= 2^26; HCC_COMP_WIDE overrides)
+  // The steady slot's hook: k_hook_sumd (summary-predicated lookups: RMAT-24
+  // 1.59 -> 1.47 ms, ER 2.19 -> 2.06, grid unchanged) instead of the device
+  // vote between k_hook_sum and the plain k_hook (HCC_SUM_VOTE=1 restores
+  // the vote, HCC_SUMD=0 the plain hook; 2: sumd in every streaming slot
+  // after the first, measured slower).
+  int sumd = 1;
+  bool sum_vote = false;
 };
 
 HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
@@ -514,9 +523,14 @@ bool slot_small(const Plan& P, u64 sgi) {
 // prefetch was slower: DESIGN.md §3.2).
 void launch_compress_s0b(hcc_ctx* c, const Plan& P, cudaStream_t s, int rec_idx = -1,
                          int dslot = -1) {
-  k_compress_s0b<<<grid_for((P.n + 7) / 8, kVertThreads, 0x7fffffffull), kVertThreads, 0, s>>>(
-      P.pi, P.n, c->d_ctrl, c->d_recs, c->s0b, kCompressIfDirty, P.sum ? c->s0f : nullptr,
-      P.sum_words, P.sum_shift, rec_idx, dslot);
+  if (P.wide_compress)
+    k_compress_s0b_w<<<grid_for((P.n + 7) / 8, kVertThreadsWide, 0x7fffffffull), kVertThreadsWide,
+                       0, s>>>(P.pi, P.n, c->d_ctrl, c->d_recs, c->s0b, kCompressIfDirty,
+                               P.sum ? c->s0f : nullptr, P.sum_words, P.sum_shift, rec_idx, dslot);
+  else
+    k_compress_s0b<<<grid_for((P.n + 7) / 8, kVertThreads, 0x7fffffffull), kVertThreads, 0, s>>>(
+        P.pi, P.n, c->d_ctrl, c->d_recs, c->s0b, kCompressIfDirty, P.sum ? c->s0f : nullptr,
+        P.sum_words, P.sum_shift, rec_idx, dslot);
 }
 
 // Preferred shared-memory carveout (percent) of the forming-slot hook.  RMAT's
@@ -544,6 +558,16 @@ void launch_hook(const Plan& P, cudaStream_t s, const HookArgs& a) {
   } else {
     k_hook_legacy<<<P.grid_hook, P.block_hook, 0, s>>>(a);
   }
+}
+
+// Summary-predicated streaming hook (the summary in shared memory, no
+// queues); the dynamic-schedule build for large forests.
+void launch_hook_sumd(hcc_ctx* c, const Plan& P, cudaStream_t s, const HookArgs& a) {
+  const size_t smem = (size_t)((a.s0f_words + 3u) & ~3u) * 4;
+  if (P.dyn && P.n >= (1ull << 26))
+    k_hook_sumd_dyn<<<c->sms * c->occ_hook_sumd, kHookSumdCta, smem, s>>>(a);
+  else
+    k_hook_sumd<<<c->sms * c->occ_hook_sumd, kHookSumdCta, smem, s>>>(a);
 }
 
 // Segment hook of the adaptive / atomic engines (no appends).  HCC_SEG_CAS=0
@@ -633,6 +657,8 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           if (P.s0b && sgi >= 1) use_s0b(c, P, ha);
           if (P.hook_events) q.record(c->seg_ev[2 * sgi]);
           c->slot_kernel.push_back(slot_small(P, sgi) ? HCC_HOOK_KERNEL_SMALL
+                                   : sum_slot(P, sgi) && !P.sum_vote
+                                       ? (P.sumd ? HCC_HOOK_KERNEL_SUMD : HCC_HOOK_KERNEL_STREAM)
                                    : sum_slot(P, sgi)   ? HCC_HOOK_KERNEL_SUM
                                    : P.chunked          ? HCC_HOOK_KERNEL_STREAM
                                                         : HCC_HOOK_KERNEL_LEGACY);
@@ -650,14 +676,33 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
             if (P.adapt && sgi + 1 == P.nseg) ha.walk = P.walk_last;
             HookArgs hp = ha;  // plain streaming hook: bitmap only, full L1
             hp.s0f = nullptr;
-            if (sum_slot(P, sgi)) {
+            if (sum_slot(P, sgi) && !P.sum_vote) {
+              // the steady slot: summary-predicated lookups (k_hook_sumd)
+              HookArgs hd = ha;
+              hd.gate = kGateAlways;
+              if (P.sumd)
+                launch_hook_sumd(c, P, q.s(), hd);
+              else
+                launch_hook(P, q.s(), hp);
+            } else if (sum_slot(P, sgi)) {
               // the previous step's device vote picks the summary hook or
               // the plain one; the other launch exits at entry (cheaper
               // than an IF/ELSE graph node, measured ~20 us per slot)
               ha.gate = kGateIfSum;
               hp.gate = kGateIfPlain;
               launch_hook_sum(c, q.s(), ha);
-              launch_hook(P, q.s(), hp);
+              if (P.sumd) {
+                // the plain choice with summary-predicated lookups
+                HookArgs hd = ha;
+                hd.gate = kGateIfPlain;
+                launch_hook_sumd(c, P, q.s(), hd);
+              } else {
+                launch_hook(P, q.s(), hp);
+              }
+            } else if (P.sumd >= 2 && P.sum && sgi >= 1 && !ha.cas) {
+              HookArgs hd = ha;
+              hd.gate = kGateAlways;
+              launch_hook_sumd(c, P, q.s(), hd);
             } else {
               launch_hook(P, q.s(), hp);
             }
@@ -681,7 +726,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
             // the next hook's summary vote rides on the step kernel (the
             // worklist passes reuse the last one: coverage only grows)
             // and so does the bitmap-use decision (a 2048-endpoint sample)
-            const bool vote = sgi + 1 < P.nseg && sum_slot(P, sgi + 1);
+            const bool vote = sgi + 1 < P.nseg && sum_slot(P, sgi + 1) && P.sum_vote;
             if (P.s0b)
               k_step_adapt<<<1, 1024, 0, q.s()>>>(ctrl, recs, P.m, P.forming_pct,
                                                  vote ? c->s0f : nullptr, P.sum_words,
@@ -713,7 +758,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
         wa.cas = P.cas_mode >= 1 && P.chunked ? 1 : 0;
         c->wl_kernel = wa.cas ? HCC_HOOK_KERNEL_CAS
                               : (P.chunked ? HCC_HOOK_KERNEL_STREAM : HCC_HOOK_KERNEL_LEGACY);
-        if (wa.s0f && P.adapt) {
+        if (wa.s0f && P.adapt && P.sum_vote) {
           HookArgs wp = wa;
           wa.gate = kGateIfSum;
           wp.gate = kGateIfPlain;
@@ -1041,6 +1086,13 @@ int hcc_create(int device, hcc_ctx** out) {
                                 (int)kHookSmemMax));
   HCC_CUDA(cudaFuncSetAttribute(k_hook_sum_cas, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kHookSmemMax));
+  HCC_CUDA(cudaFuncSetAttribute(k_hook_sumd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kS0fMaxBytes));
+  HCC_CUDA(cudaFuncSetAttribute(k_hook_sumd_dyn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kS0fMaxBytes));
+  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_sumd, kHookSumdCta,
+                                                          kS0fMaxBytes));
+  c->occ_hook_sumd = std::max(occ, 1);
   HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_sum, kHookSumCta,
                                                           kHookSmemMax));
   c->occ_hook_sum = std::max(occ, 1);
@@ -1789,6 +1841,10 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   if (const char* e = std::getenv("HCC_HOOK_SMALL")) P.small_slots = std::atoi(e) != 0;
   if (const char* e = std::getenv("HCC_HOOK_CAS")) P.cas_mode = std::atoi(e);
   if (const char* e = std::getenv("HCC_DYN")) P.dyn = std::atoi(e) != 0;
+  P.wide_compress = false;  // measured: no gain at n = 2^28 (33.89 vs 33.81 ms)
+  if (const char* e = std::getenv("HCC_COMP_WIDE")) P.wide_compress = std::atoi(e) != 0;
+  if (const char* e = std::getenv("HCC_SUMD")) P.sumd = std::atoi(e);
+  if (const char* e = std::getenv("HCC_SUM_VOTE")) P.sum_vote = std::atoi(e) != 0;
   P.forming_pct = std::getenv("HCC_FORMING_PCT") ? (u32)std::atoi(std::getenv("HCC_FORMING_PCT"))
                                                   : kAdaptFormingPct;
   if (P.s0b) {
@@ -1844,8 +1900,9 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
     const u64 warps = std::max<u64>(
         std::max<u64>((u64)P.grid_hook * (P.block_hook / 32),
                       (u64)c->sms * c->occ_hook_sum * (kHookSumCta / 32)),
-        std::max<u64>((u64)P.grid_cas * (kHookCasCta / 32),
-                      (u64)c->sms * c->occ_hook_sum_cas * (kHookCasCta / 32)));
+        std::max<u64>(std::max<u64>((u64)P.grid_cas * (kHookCasCta / 32),
+                                    (u64)c->sms * c->occ_hook_sum_cas * (kHookCasCta / 32)),
+                      (u64)c->sms * c->occ_hook_sumd * (kHookSumdCta / 32)));
     const u64 launches = (P.nseg <= kMaxUnrolledSegments ? P.nseg : 0) + 2;
     // Records: every store of the topology slots plus deferred walks, all
     // slots into one list.  Stores link distinct roots up to benign races,
@@ -1923,6 +1980,9 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   key.plan = key.plan * 5 + (u64)P.cas_mode;
   key.plan = key.plan * 3 + (P.cas_stream ? 1 : 0);
   key.plan = key.plan * 3 + (P.dyn ? 1 : 0);
+  key.plan = key.plan * 3 + (P.wide_compress ? 1 : 0);
+  key.plan = key.plan * 3 + (u64)P.sumd;
+  key.plan = key.plan * 3 + (P.sum_vote ? 1 : 0);
   key.plan = key.plan * 31 + (P.adapt ? 1000 + P.adapt_shift + 100000ull * P.forming_pct : 0);
   key.plan = key.plan * 1000003ull + P.adapt_first;
   for (u64 x : P.bounds) key.plan = key.plan * 1000003ull + x;

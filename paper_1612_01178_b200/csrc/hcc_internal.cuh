@@ -50,6 +50,11 @@ constexpr int kHookSumCta = HCC_HOOK_SUM_CTA;  // k_hook_sum (one CTA per SM)
 #define HCC_HOOK_CAS_CTA 768
 #endif
 constexpr int kHookCasCta = HCC_HOOK_CAS_CTA;
+// Summary-predicated streaming hook (k_hook_sumd).
+#ifndef HCC_HOOK_SUMD_CTA
+#define HCC_HOOK_SUMD_CTA 1024
+#endif
+constexpr int kHookSumdCta = HCC_HOOK_SUMD_CTA;
 constexpr u32 kS0fMaxBytes = HCC_S0F_MAX_BYTES;
 constexpr int kHookSlow = 4;
 // HookArgs.gate: k_hook_sum and k_hook are launched back to back for a
@@ -64,6 +69,7 @@ constexpr u32 kWlChunk = HCC_WL_CHUNK;  // worklist records a warp reserves at o
 #endif
 constexpr int kHookEPT = HCC_HOOK_EPT;  // edges per thread per tile (4 x uint4)
 constexpr int kVertThreads = 256;
+constexpr int kVertThreadsWide = 512;  // k_compress_s0b_w (n >= 2^26)
 
 // One record per hook+compress phase pair (segment, outer iteration or
 // worklist pass).  Times are %globaltimer nanoseconds (first block start,
@@ -198,6 +204,8 @@ __global__ void k_hook_legacy(HookArgs a);
 __global__ void k_hook_cas(HookArgs a);
 __global__ void k_hook_sum_cas(HookArgs a);
 __global__ void k_hook_seg_cas(HookArgs a);
+__global__ void k_hook_sumd(HookArgs a);
+__global__ void k_hook_sumd_dyn(HookArgs a);
 __global__ void k_star_pick(const u32* pi, u64 n, DevCtrl* ctrl);
 __global__ void k_cas_hook(HookArgs a);
 __global__ void k_compress(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
@@ -205,6 +213,9 @@ __global__ void k_compress(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
 __global__ void k_compress_s0b(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
                                u32* bits, int skip_if_clean, u32* sum, u32 sum_words,
                                u32 sum_shift, int rec_idx, int dslot);
+__global__ void k_compress_s0b_w(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
+                                 u32* bits, int skip_if_clean, u32* sum, u32 sum_words,
+                                 u32 sum_shift, int rec_idx, int dslot);
 __global__ void k_start(u32* pi, u64 n, u32* bits, DevCtrl* ctrl, DevRec* recs, u64 nseg,
                         u64 m, u64 plan_first, u32* sum, u32 sum_words);
 __global__ void k_jump(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs);

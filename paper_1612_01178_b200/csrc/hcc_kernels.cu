@@ -776,7 +776,8 @@ __device__ __forceinline__ void emit(const HookArgs& a, WarpOut& w, uint2* wl_ou
 // lane per round.  Otherwise (k_hook: no shared memory, so L1 keeps its full
 // size for the bitmap's hot words; e.g. RMAT, whose isolated vertices break
 // most words) every edge takes the bitmap / gather path directly.
-template <int EPT, bool SUM, bool CAS = false, bool APPEND = true>
+template <int EPT, bool SUM, bool CAS = false, bool APPEND = true, bool SUMD = false,
+          bool DYNOK = true>
 __device__ __forceinline__ void hook_stream(const HookArgs& a) {
   constexpr int S = kHookSlow;
   const uint2* src;
@@ -799,7 +800,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
   const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
 
   extern __shared__ u32 s_sum[];
-  if (SUM) load_summary(a, s_sum);
+  if (SUM || SUMD) load_summary(a, s_sum);
   uint2* s_q = reinterpret_cast<uint2*>(s_sum + ((a.s0f_words + 3u) & ~3u)) +
                (size_t)warp * (32 * EPT);
   WarpOut wo;
@@ -846,7 +847,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
   // warps on slow SMs trail: RMAT-28's steady hook ran 5.5 ms past its
   // median block for some placements of the star bitmap.
   const u32 tpw = ntiles / wstride;
-  const bool dyn = a.dyn && tpw >= 32;
+  const bool dyn = DYNOK && a.dyn && tpw >= 32;
   const u32 kch = tpw / 16 < 4 ? 4 : tpw / 16 > 64 ? 64 : tpw / 16;
   u32 cbase = gw * kch;  // current chunk
   u32 nreq = 0;          // lane 0: reply for the next chunk
@@ -871,6 +872,29 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
     const u32 tn = next_of(t);
     if (tn < ntiles) load_tile(tn, nq);
     t = tn;
+    if (SUMD) {
+      // summary-predicated lookups, no compaction: a lane whose endpoint's
+      // 32-vertex word is all in the star (one shared-memory load) skips
+      // its bitmap gather, so the gather instruction touches fewer lines
+#if HCC_SUMD_HALVES
+      // (two halves of EPT/2 edges: fewer live registers)
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        uint2 e2[EPT / 2];
+#pragma unroll
+        for (int k = 0; k < EPT / 2; ++k) e2[k] = ed[hf * (EPT / 2) + k];
+        u32 h[EPT / 2], l[EPT / 2];
+        const u32 act =
+            resolve_edges<EPT / 2, true, false, CAS>(a, links, tries, bits, s_sum, star, e2, h, l);
+        emit<EPT / 2, APPEND>(a, wo, wl_out, cnt_out, lane, act, h, l);
+      }
+#else
+      u32 h[EPT], l[EPT];
+      const u32 act = resolve_edges<EPT, true, false, CAS>(a, links, tries, bits, s_sum, star, ed, h, l);
+      emit<EPT, APPEND>(a, wo, wl_out, cnt_out, lane, act, h, l);
+#endif
+      continue;
+    }
     if (!SUM) {
       u32 h[EPT], l[EPT];
       const u32 act = resolve_edges<EPT, false, false, CAS>(a, links, tries, bits, s_sum, star, ed, h, l);
@@ -970,6 +994,25 @@ __global__ void __launch_bounds__(kHookCasCta, 1) k_hook_sum_cas(HookArgs a) {
 // walks, nothing appended (no chunk state), so it fits 1024-thread CTAs.
 __global__ void __launch_bounds__(kHookCta, HCC_HOOK_MINB) k_hook_seg_cas(HookArgs a) {
   hook_stream<kHookEPT, false, true, false>(a);
+}
+
+#ifndef HCC_SUMD_HALVES
+#define HCC_SUMD_HALVES 0
+#endif
+// Streaming hook with summary-predicated lookups (the summary in shared
+// memory, no slow-path queues: 64 KB instead of 128 KB of shared memory).
+// Static schedule: the dynamic one's state made it spill 40 B (measured on
+// RMAT-24's steady slot: the static schedule is as fast there).
+__global__ void __launch_bounds__(kHookSumdCta, 1) k_hook_sumd(HookArgs a) {
+  if (a.gate == kGateIfPlain && __ldg(&a.ctrl->use_sum)) return;
+  hook_stream<kHookEPT, false, false, true, true, false>(a);
+}
+
+// Dynamic schedule (large forests, n >= 2^26: placement-dependent
+// stragglers, §3.2); spills 40 B.
+__global__ void __launch_bounds__(kHookSumdCta, 1) k_hook_sumd_dyn(HookArgs a) {
+  if (a.gate == kGateIfPlain && __ldg(&a.ctrl->use_sum)) return;
+  hook_stream<kHookEPT, false, false, true, true, true>(a);
 }
 
 // Streaming hook with the star-0 summary in shared memory (full warps,
@@ -1275,10 +1318,14 @@ __device__ __forceinline__ void emit_bits(u64 chunk, u64 n, u64 v0, u32 byte, u3
   }
   if (lane == 0) s_full[threadIdx.x >> 5] = b8;
   __syncthreads();
-  if (threadIdx.x == 0 && blockDim.x == kVertThreads) {
+  // a 64-word chunk is 8 warps (256 threads); a wider block holds several,
+  // the first lane of each chunk's first warp assembles it
+  if ((threadIdx.x & 255u) == 0 && (blockDim.x & 255u) == 0) {
+    const u32 c8 = threadIdx.x >> 5;
+    chunk = chunk * (blockDim.x >> 8) + (threadIdx.x >> 8);
     u64 f = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) f |= (u64)s_full[i] << (8 * i);
+    for (int i = 0; i < 8; ++i) f |= (u64)s_full[c8 + i] << (8 * i);
     const u32 g = 1u << sum_shift, nb = 64u >> sum_shift;
     u64 bitsg = 0;
     for (u32 i = 0; i < nb; ++i) {
@@ -1307,9 +1354,33 @@ __device__ __forceinline__ void emit_bits(u64 chunk, u64 n, u64 v0, u32 byte, u3
 #ifndef HCC_COMP_MINB
 #define HCC_COMP_MINB 6
 #endif
+template <int BS>
+__device__ __forceinline__ void compress_s0b_body(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
+                                                  u32* bits, int mode, u32* sum, u32 sum_words,
+                                                  u32 sum_shift, int rec_idx, int dslot);
+
 __global__ void __launch_bounds__(kVertThreads, HCC_COMP_MINB)
     k_compress_s0b(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs, u32* bits,
                    int mode, u32* sum, u32 sum_words, u32 sum_shift, int rec_idx, int dslot) {
+  compress_s0b_body<kVertThreads>(pi, n, ctrl, recs, bits, mode, sum, sum_words, sum_shift,
+                                  rec_idx, dslot);
+}
+
+// 512-thread blocks, half as many (HCC_COMP_WIDE=1; off by default): at
+// n = 2^28 a compress is 131 K blocks of 256 threads that each read 8 KB of
+// pi, which suggested block turnover as the bound; measured, it is not
+// (RMAT-28 33.89 vs 33.81 ms, adaptive 41.7 vs 40.7 ms).
+__global__ void __launch_bounds__(kVertThreadsWide, 3)
+    k_compress_s0b_w(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs, u32* bits,
+                     int mode, u32* sum, u32 sum_words, u32 sum_shift, int rec_idx, int dslot) {
+  compress_s0b_body<kVertThreadsWide>(pi, n, ctrl, recs, bits, mode, sum, sum_words, sum_shift,
+                                      rec_idx, dslot);
+}
+
+template <int BS>
+__device__ __forceinline__ void compress_s0b_body(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
+                                                  u32* bits, int mode, u32* sum, u32 sum_words,
+                                                  u32 sum_shift, int rec_idx, int dslot) {
   if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->tile_ctr = 0;  // next hook's schedule
   if (dslot >= 0) {
     // unrolled chain: this segment's flag; clear the next segment's
@@ -1341,7 +1412,7 @@ __global__ void __launch_bounds__(kVertThreads, HCC_COMP_MINB)
   // a compress never moves a root, so the answer holds for the whole pass
   const bool star_root = star < n && ld_pi(pi + star) == star;
   const u32 byte = compress8(pi, n, v0, whole, pa, pb, star, star_root, steps);
-  __shared__ u32 s_full[8];
+  __shared__ u32 s_full[BS / 32];
   emit_bits(blockIdx.x, n, v0, byte, bits, sum, sum_words, sum_shift, s_full);
   add_counter(&r->jump_stripe[blockIdx.x & (kJumpStripes - 1)], steps);
   block_t1(&r->comp_t1);

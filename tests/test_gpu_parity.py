@@ -551,7 +551,8 @@ def test_hook_events_flag_and_timeline(ctx, oracle, capi):
         # each record names the hook kernel that ran its pass
         kinds = [s["hook_kernel"] for s in segs]
         assert kinds[0] in ("k_hook_small", "k_hook")
-        assert all(k in ("k_hook_small", "k_hook", "k_hook_sum") for k in kinds[1:mx["s"]])
+        assert all(k in ("k_hook_small", "k_hook", "k_hook_sum", "k_hook_sumd")
+                   for k in kinds[1:mx["s"]])
         assert all(k == "k_hook_cas" for k in kinds[mx["s"]:])
     g.close()
 
@@ -693,4 +694,44 @@ def test_adaptive_star_moves_off_vertex0(ctx, oracle, shift):
     for s in (0, 4, 31):
         lab, _ = ctx.cc(g, "adaptive", segments=s)
         assert np.array_equal(lab, want), s
+    g.close()
+
+
+@pytest.mark.parametrize("spec", ["rmatx:scale=20,ef=16,seed=7", "erx:n=16777217,m=67108864,seed=2",
+                                  "grid:1100x1000", "erx:n=70001,m=40000,seed=9"])
+def test_wide_compress_blocks(ctx, oracle, spec):
+    """512-thread compress blocks (k_compress_s0b_w, the default from n = 2^26)
+    forced on smaller graphs: two 64-word summary chunks per block (shift 0 and,
+    at n = 2^24 + 1, shift 1 with shared summary words), partial last block."""
+    import os
+    g = ctx.generate(spec)
+    want = oracle.cc(g.n, g.edges())
+    os.environ["HCC_COMP_WIDE"] = "1"
+    try:
+        for algo in ("baseline-mj", "adaptive"):
+            lab, _ = ctx.cc(g, algo)
+            assert np.array_equal(lab, want), (spec, algo)
+    finally:
+        os.environ.pop("HCC_COMP_WIDE", None)
+    g.close()
+
+
+@pytest.mark.parametrize("spec", ["rmatx:scale=20,ef=16,seed=7", "erx:n=16777217,m=67108864,seed=2",
+                                  "grid:1100x1000", "erx:n=1048579,m=8000000,seed=5"])
+def test_steady_hook_variants(ctx, oracle, spec):
+    """The steady slot's hook choices give identical labels: k_hook_sumd
+    (default), the k_hook_sum / k_hook device vote (HCC_SUM_VOTE=1), the plain
+    hook (HCC_SUMD=0), sumd in every streaming slot (HCC_SUMD=2)."""
+    import os
+    g = ctx.generate(spec)
+    want = oracle.cc(g.n, g.edges())
+    for env in ({}, {"HCC_SUM_VOTE": "1"}, {"HCC_SUMD": "0"}, {"HCC_SUMD": "2"},
+                {"HCC_SUMD": "1", "HCC_DYN": "0"}):
+        os.environ.update(env)
+        try:
+            lab, _ = ctx.cc(g, "baseline-mj")
+            assert np.array_equal(lab, want), (spec, env)
+        finally:
+            for k in env:
+                os.environ.pop(k, None)
     g.close()
