@@ -462,6 +462,7 @@ struct Plan {
   // after the first, measured slower).
   int sumd = 1;
   bool sum_vote = false;
+  bool sum_prefix = false;     // truncated prefix summary (HCC_S0F_PREFIX)
 };
 
 HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
@@ -508,9 +509,10 @@ void use_s0b(hcc_ctx* c, const Plan& P, HookArgs& a) {
 // of 32 * kHookEPT edges per warp (hook_stream).
 size_t hook_smem(const HookArgs& a, unsigned block) {
   if (!a.s0f) return 0;
-  return (size_t)((a.s0f_words + 3u) & ~3u) * 4 + (size_t)((block + 31) / 32) * 32 * kHookEPT * 8;
+  return (size_t)sum_region_words(a.s0f_words) * 4 + (size_t)((block + 31) / 32) * 32 * kHookEPT * 8;
 }
-constexpr size_t kHookSmemMax = kS0fMaxBytes + (size_t)kHookSumCta * kHookEPT * 8;
+constexpr size_t kHookSmemMax =
+    (size_t)sum_region_words(kS0fMaxBytes / 4) * 4 + (size_t)kHookSumCta * kHookEPT * 8;
 
 // Unrolled topology slot that runs the small-segment hook (forming regime).
 bool slot_small(const Plan& P, u64 sgi) {
@@ -563,8 +565,10 @@ void launch_hook(const Plan& P, cudaStream_t s, const HookArgs& a) {
 // Summary-predicated streaming hook (the summary in shared memory, no
 // queues); the dynamic-schedule build for large forests.
 void launch_hook_sumd(hcc_ctx* c, const Plan& P, cudaStream_t s, const HookArgs& a) {
-  const size_t smem = (size_t)((a.s0f_words + 3u) & ~3u) * 4;
-  if (P.dyn && P.n >= (1ull << 26))
+  const size_t smem = (size_t)sum_region_words(a.s0f_words) * 4;
+  if (P.sum_prefix)
+    k_hook_sumd_pfx<<<c->sms * c->occ_hook_sumd, kHookSumdCta, smem, s>>>(a);
+  else if (P.dyn && P.n >= (1ull << 26))
     k_hook_sumd_dyn<<<c->sms * c->occ_hook_sumd, kHookSumdCta, smem, s>>>(a);
   else
     k_hook_sumd<<<c->sms * c->occ_hook_sumd, kHookSumdCta, smem, s>>>(a);
@@ -594,6 +598,17 @@ void launch_hook_sum(hcc_ctx* c, cudaStream_t s, const HookArgs& a) {
 // groups, and a voted slot costs a second (gated) launch.
 bool sum_slot(const Plan& P, u64 sgi) {
   return P.sum && P.adapt && sgi >= 1 && sgi + 1 == P.nseg && !slot_small(P, sgi);
+}
+
+// Unrolled adaptive-plan slot whose hook is chosen on the device between the
+// summary-predicated k_hook_sumd (the slot that takes every remaining edge)
+// and the plain k_hook (forming slots).
+// Only with a one-bit-per-word summary (n <= 2^24): a coarser one covers
+// little of RMAT's lookups, and its 64 KB of shared memory then only costs
+// L1 (RMAT-28's steady slot 27.4 -> 32.4 ms, RMAT-26 7.3 -> 8.5 ms).
+bool remainder_slot(const Plan& P, u64 sgi) {
+  return P.sumd == 1 && !P.sum_vote && P.sum && P.sum_shift == 0 && !P.sum_prefix && P.adapt &&
+         P.chunked && sgi >= 1 && !slot_small(P, sgi) && !(P.cas_mode >= 2 && sgi + 1 == P.nseg);
 }
 
 // Enqueue one full CC run (pi init through convergence) on seq.
@@ -656,9 +671,9 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           ha.e = P.bounds[sgi + 1];
           if (P.s0b && sgi >= 1) use_s0b(c, P, ha);
           if (P.hook_events) q.record(c->seg_ev[2 * sgi]);
-          c->slot_kernel.push_back(slot_small(P, sgi) ? HCC_HOOK_KERNEL_SMALL
-                                   : sum_slot(P, sgi) && !P.sum_vote
-                                       ? (P.sumd ? HCC_HOOK_KERNEL_SUMD : HCC_HOOK_KERNEL_STREAM)
+          c->slot_kernel.push_back(slot_small(P, sgi)       ? HCC_HOOK_KERNEL_SMALL
+                                   : remainder_slot(P, sgi) ? HCC_HOOK_KERNEL_SUMD
+                                   : sum_slot(P, sgi) && !P.sum_vote ? HCC_HOOK_KERNEL_STREAM
                                    : sum_slot(P, sgi)   ? HCC_HOOK_KERNEL_SUM
                                    : P.chunked          ? HCC_HOOK_KERNEL_STREAM
                                                         : HCC_HOOK_KERNEL_LEGACY);
@@ -676,14 +691,18 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
             if (P.adapt && sgi + 1 == P.nseg) ha.walk = P.walk_last;
             HookArgs hp = ha;  // plain streaming hook: bitmap only, full L1
             hp.s0f = nullptr;
-            if (sum_slot(P, sgi) && !P.sum_vote) {
-              // the steady slot: summary-predicated lookups (k_hook_sumd)
+            if (remainder_slot(P, sgi)) {
+              // the slot that takes every remaining edge (decided on the
+              // device by the previous step, which sets use_sum) streams
+              // with summary-predicated lookups (k_hook_sumd), any other
+              // with the plain hook; the one not chosen exits at entry
               HookArgs hd = ha;
-              hd.gate = kGateAlways;
-              if (P.sumd)
-                launch_hook_sumd(c, P, q.s(), hd);
-              else
-                launch_hook(P, q.s(), hp);
+              hd.gate = kGateIfSum;
+              hp.gate = kGateIfPlain;
+              launch_hook_sumd(c, P, q.s(), hd);
+              launch_hook(P, q.s(), hp);
+            } else if (sum_slot(P, sgi) && !P.sum_vote) {
+              launch_hook(P, q.s(), hp);
             } else if (sum_slot(P, sgi)) {
               // the previous step's device vote picks the summary hook or
               // the plain one; the other launch exits at entry (cheaper
@@ -727,13 +746,14 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
             // worklist passes reuse the last one: coverage only grows)
             // and so does the bitmap-use decision (a 2048-endpoint sample)
             const bool vote = sgi + 1 < P.nseg && sum_slot(P, sgi + 1) && P.sum_vote;
+            const int rvote = sgi + 1 < P.nseg && remainder_slot(P, sgi + 1) ? 1 : 0;
             if (P.s0b)
               k_step_adapt<<<1, 1024, 0, q.s()>>>(ctrl, recs, P.m, P.forming_pct,
                                                  vote ? c->s0f : nullptr, P.sum_words,
-                                                 P.edges, c->s0b);
+                                                 P.edges, c->s0b, rvote);
             else
               k_step_adapt<<<1, 1, 0, q.s()>>>(ctrl, recs, P.m, P.forming_pct, nullptr, 0,
-                                              nullptr, nullptr);
+                                              nullptr, nullptr, 0);
           } else
             k_step_segment<<<1, 1, 0, q.s()>>>(ctrl, recs, 0, 0);
         }
@@ -1086,12 +1106,15 @@ int hcc_create(int device, hcc_ctx** out) {
                                 (int)kHookSmemMax));
   HCC_CUDA(cudaFuncSetAttribute(k_hook_sum_cas, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kHookSmemMax));
+  const int sumd_smem = (int)sum_region_words(kS0fMaxBytes / 4) * 4;
   HCC_CUDA(cudaFuncSetAttribute(k_hook_sumd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)kS0fMaxBytes));
+                                sumd_smem));
   HCC_CUDA(cudaFuncSetAttribute(k_hook_sumd_dyn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)kS0fMaxBytes));
+                                sumd_smem));
+  HCC_CUDA(cudaFuncSetAttribute(k_hook_sumd_pfx, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                sumd_smem));
   HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_sumd, kHookSumdCta,
-                                                          kS0fMaxBytes));
+                                                          sumd_smem));
   c->occ_hook_sumd = std::max(occ, 1);
   HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_sum, kHookSumCta,
                                                           kHookSmemMax));
@@ -1844,7 +1867,6 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   P.wide_compress = false;  // measured: no gain at n = 2^28 (33.89 vs 33.81 ms)
   if (const char* e = std::getenv("HCC_COMP_WIDE")) P.wide_compress = std::atoi(e) != 0;
   if (const char* e = std::getenv("HCC_SUMD")) P.sumd = std::atoi(e);
-  if (const char* e = std::getenv("HCC_SUM_VOTE")) P.sum_vote = std::atoi(e) != 0;
   P.forming_pct = std::getenv("HCC_FORMING_PCT") ? (u32)std::atoi(std::getenv("HCC_FORMING_PCT"))
                                                   : kAdaptFormingPct;
   if (P.s0b) {
@@ -1859,13 +1881,29 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
     while (((nwords + (1ull << sh) - 1) >> sh) > (u64)kS0fMaxBytes * 8) ++sh;
     bool sum_ok = sh <= 6;
     if (const char* e = std::getenv("HCC_S0F")) sum_ok = sum_ok && std::atoi(e) != 0;
+    // HCC_S0F_PREFIX=1 (experiment): for n > 2^24, one bit per word over the
+    // first 2^19 words (vertices < 2^24, RMAT's hot prefix) instead of one
+    // bit per 2^shift words over all of them
+    const bool prefix = sh > 0 && std::getenv("HCC_S0F_PREFIX") &&
+                        std::atoi(std::getenv("HCC_S0F_PREFIX")) != 0;
+    if (prefix) {
+      sh = 0;
+      sum_ok = true;
+      P.sum_prefix = true;
+    }
     if (sum_ok) {
       P.sum = true;
       P.sum_shift = sh;
-      P.sum_words = (u32)((((nwords + (1ull << sh) - 1) >> sh) + 31) / 32);
+      P.sum_words = (u32)std::min<u64>((((nwords + (1ull << sh) - 1) >> sh) + 31) / 32,
+                                       kS0fMaxBytes / 4);
       ensure_s0f(c, P.sum_words);
     }
   }
+  // with a coarse summary (shift > 0: n > 2^24) the summary hook still
+  // pays where the giant fills whole words (ER with n = 2^24 + 1: 3.0 ms on
+  // the plain hook), so the device vote between it and the plain hook stays
+  P.sum_vote = P.sum && P.sum_shift > 0;
+  if (const char* e = std::getenv("HCC_SUM_VOTE")) P.sum_vote = std::atoi(e) != 0;
   {
     const char* w = std::getenv("HCC_WALK");
     P.walk = w ? std::atoi(w) : kDefaultWalk;
@@ -1983,6 +2021,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   key.plan = key.plan * 3 + (P.wide_compress ? 1 : 0);
   key.plan = key.plan * 3 + (u64)P.sumd;
   key.plan = key.plan * 3 + (P.sum_vote ? 1 : 0);
+  key.plan = key.plan * 1000003ull + P.sum_words * 64ull + P.sum_shift;
   key.plan = key.plan * 31 + (P.adapt ? 1000 + P.adapt_shift + 100000ull * P.forming_pct : 0);
   key.plan = key.plan * 1000003ull + P.adapt_first;
   for (u64 x : P.bounds) key.plan = key.plan * 1000003ull + x;
@@ -2106,6 +2145,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
         sr.hook_kernel = c->slot_kernel[i];
         if (sr.hook_kernel == HCC_HOOK_KERNEL_SUM && !hc.use_sum)
           sr.hook_kernel = HCC_HOOK_KERNEL_STREAM;  // the vote chose the plain hook
+        if (r.kind) sr.hook_kernel = (int32_t)r.kind;  // what actually ran
       } else if (o->algo == HCC_ALGO_BASELINE_MJ && !P.full_passes) {
         sr.hook_kernel = c->wl_kernel;
       }

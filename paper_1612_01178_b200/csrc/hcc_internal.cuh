@@ -56,6 +56,9 @@ constexpr int kHookCasCta = HCC_HOOK_CAS_CTA;
 #endif
 constexpr int kHookSumdCta = HCC_HOOK_SUMD_CTA;
 constexpr u32 kS0fMaxBytes = HCC_S0F_MAX_BYTES;
+// Shared-memory words the staged summary of `w` words occupies: whole
+// 32-word rows (the swizzle permutes within a row) plus the zero sentinel's.
+__host__ __device__ constexpr u32 sum_region_words(u32 w) { return ((w >> 5) + 1) << 5; }
 constexpr int kHookSlow = 4;
 // HookArgs.gate: k_hook_sum and k_hook are launched back to back for a
 // voted slot and the one not chosen (DevCtrl.use_sum) exits at entry.
@@ -85,6 +88,7 @@ struct DevRec {
   u64 hook_t0, hook_t1, comp_t0, comp_t1;
   u64 traversal, cas_fail, jump_steps;
   u64 edges_in, edges_out;
+  u64 kind;          // HCC_HOOK_KERNEL_* of the hook that did this record's pass
   u64 jump_stripe[kJumpStripes];
   u64 jump_total() const {
     u64 t = jump_steps;
@@ -206,6 +210,7 @@ __global__ void k_hook_sum_cas(HookArgs a);
 __global__ void k_hook_seg_cas(HookArgs a);
 __global__ void k_hook_sumd(HookArgs a);
 __global__ void k_hook_sumd_dyn(HookArgs a);
+__global__ void k_hook_sumd_pfx(HookArgs a);
 __global__ void k_star_pick(const u32* pi, u64 n, DevCtrl* ctrl);
 __global__ void k_cas_hook(HookArgs a);
 __global__ void k_compress(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
@@ -225,7 +230,7 @@ __global__ void k_step_segment(DevCtrl* ctrl, DevRec* recs,
                                cudaGraphConditionalHandle h, int use_cond);
 __global__ void k_step_adapt(DevCtrl* ctrl, DevRec* recs, u64 m, u32 forming_pct,
                              const u32* sum, u32 sum_words, const uint2* edges,
-                             const u32* bits);
+                             const u32* bits, int remainder_vote);
 __global__ void k_step_outer(DevCtrl* ctrl, DevRec* recs,
                              cudaGraphConditionalHandle h, int use_cond);
 __global__ void k_step_jump(DevCtrl* ctrl, cudaGraphConditionalHandle h,

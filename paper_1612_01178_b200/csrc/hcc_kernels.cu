@@ -123,9 +123,14 @@ __device__ __forceinline__ u32 sum_swz(u32 i) {
 }
 
 // Vertex x's group is all in star 0 (summary bit of bitmap word x >> 5).
-__device__ __forceinline__ bool sum_covered(const u32* s_sum, u32 x, u32 shift) {
+// PFX: a truncated table (HCC_S0F_PREFIX) covering only the first
+// words * 32 groups; later groups read the zero sentinel word past its end.
+// (Bounding every lookup made the default kernels spill, so it is a
+// separate instantiation.)
+template <bool PFX = false>
+__device__ __forceinline__ bool sum_covered(const u32* s_sum, u32 x, u32 shift, u32 words) {
   const u32 g = x >> (5u + shift);
-  return (s_sum[sum_swz(g >> 5)] >> (g & 31u)) & 1u;
+  return (s_sum[sum_swz(PFX ? min(g >> 5, words) : g >> 5)] >> (g & 31u)) & 1u;
 }
 
 // Control words a kernel reads at entry (dirty, star, use_sum) are written
@@ -159,6 +164,7 @@ __device__ __forceinline__ void rec_clear(DevRec& r) {
   r.comp_t1 = 0;
   r.traversal = r.cas_fail = r.jump_steps = 0;
   r.edges_in = r.edges_out = 0;
+  r.kind = 0;
   for (int i = 0; i < kJumpStripes; ++i) r.jump_stripe[i] = 0;
 }
 
@@ -380,7 +386,7 @@ __global__ void k_init_pi(u32* pi, u64 n, u32* bits) {
 // Lookups, root walk and stores for S edges of one thread (the body of a
 // hook tile).  Returns the mask of edges whose (h, l) pair in (pu, pv)
 // must be appended to the worklist (stored links and deferred walks).
-template <int S, bool SUM, bool BOTH = false, bool CAS = false>
+template <int S, bool SUM, bool BOTH = false, bool CAS = false, bool PFX = false>
 __device__ __forceinline__ u32 resolve_edges(const HookArgs& a, u32& links, u32& tries,
                                              const u32* bits,
                                              const u32* s_sum, u32 star,
@@ -395,8 +401,8 @@ __device__ __forceinline__ u32 resolve_edges(const HookArgs& a, u32& links, u32&
     for (int k = 0; k < S; ++k) {
       const u32 xu = ed[k].x >> 5, xv = ed[k].y >> 5;
       if (SUM) {
-        wu[k] = sum_covered(s_sum, ed[k].x, a.s0f_shift) ? ~0u : ld_bits(bits + xu);
-        wv[k] = sum_covered(s_sum, ed[k].y, a.s0f_shift) ? ~0u : ld_bits(bits + xv);
+        wu[k] = sum_covered<PFX>(s_sum, ed[k].x, a.s0f_shift, a.s0f_words) ? ~0u : ld_bits(bits + xu);
+        wv[k] = sum_covered<PFX>(s_sum, ed[k].y, a.s0f_shift, a.s0f_words) ? ~0u : ld_bits(bits + xv);
       } else {
         wu[k] = ld_bits(bits + xu);
         wv[k] = ld_bits(bits + xv);
@@ -516,6 +522,7 @@ __device__ __forceinline__ u32 resolve_edges(const HookArgs& a, u32& links, u32&
 // Copy the star-0 summary into shared memory (swizzled rows).
 __device__ __forceinline__ void load_summary(const HookArgs& a, u32* s_sum) {
   for (u32 i = threadIdx.x; i < a.s0f_words; i += blockDim.x) s_sum[sum_swz(i)] = a.s0f[i];
+  if (threadIdx.x == 0) s_sum[sum_swz(a.s0f_words)] = 0u;  // sentinel (sum_covered)
   __syncthreads();
 }
 
@@ -777,7 +784,7 @@ __device__ __forceinline__ void emit(const HookArgs& a, WarpOut& w, uint2* wl_ou
 // size for the bitmap's hot words; e.g. RMAT, whose isolated vertices break
 // most words) every edge takes the bitmap / gather path directly.
 template <int EPT, bool SUM, bool CAS = false, bool APPEND = true, bool SUMD = false,
-          bool DYNOK = true>
+          bool DYNOK = true, bool PFX = false>
 __device__ __forceinline__ void hook_stream(const HookArgs& a) {
   constexpr int S = kHookSlow;
   const uint2* src;
@@ -791,9 +798,15 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
   const u32 star = a.s0b ? __ldg(&ctrl->star) : 0u;
   const u32* bits = (a.s0b && (SUM || __ldg(&ctrl->use_bits))) ? a.s0b : nullptr;
   block_t0(&r->hook_t0);
-  if (blockIdx.x == 0 && threadIdx.x == 0 && e > b) {
-    atomicAdd(&r->edges_in, e - b);
-    atomicAdd(&ctrl->edges_processed, e - b);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    r->kind = SUMD ? HCC_HOOK_KERNEL_SUMD
+              : CAS ? HCC_HOOK_KERNEL_CAS
+              : SUM ? HCC_HOOK_KERNEL_SUM
+                    : HCC_HOOK_KERNEL_STREAM;
+    if (e > b) {
+      atomicAdd(&r->edges_in, e - b);
+      atomicAdd(&ctrl->edges_processed, e - b);
+    }
   }
   uint2* wl_out = out ? a.wl1 : a.wl0;
   u64* cnt_out = &ctrl->wl_count[out];
@@ -801,7 +814,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
 
   extern __shared__ u32 s_sum[];
   if (SUM || SUMD) load_summary(a, s_sum);
-  uint2* s_q = reinterpret_cast<uint2*>(s_sum + ((a.s0f_words + 3u) & ~3u)) +
+  uint2* s_q = reinterpret_cast<uint2*>(s_sum + sum_region_words(a.s0f_words)) +
                (size_t)warp * (32 * EPT);
   WarpOut wo;
   u32 links = 0, tries = 0;  // CAS links made / CAS attempts of this thread
@@ -890,7 +903,8 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
       }
 #else
       u32 h[EPT], l[EPT];
-      const u32 act = resolve_edges<EPT, true, false, CAS>(a, links, tries, bits, s_sum, star, ed, h, l);
+      const u32 act =
+          resolve_edges<EPT, true, false, CAS, PFX>(a, links, tries, bits, s_sum, star, ed, h, l);
       emit<EPT, APPEND>(a, wo, wl_out, cnt_out, lane, act, h, l);
 #endif
       continue;
@@ -906,8 +920,8 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
       const bool done = ed[k].x == ed[k].y ||
-                        (sum_covered(s_sum, ed[k].x, a.s0f_shift) &&
-                         sum_covered(s_sum, ed[k].y, a.s0f_shift));
+                        (sum_covered(s_sum, ed[k].x, a.s0f_shift, a.s0f_words) &&
+                         sum_covered(s_sum, ed[k].y, a.s0f_shift, a.s0f_words));
       need |= done ? 0u : 1u << k;
     }
     const u32 nneed = __popc(need);
@@ -1005,6 +1019,7 @@ __global__ void __launch_bounds__(kHookCta, HCC_HOOK_MINB) k_hook_seg_cas(HookAr
 // RMAT-24's steady slot: the static schedule is as fast there).
 __global__ void __launch_bounds__(kHookSumdCta, 1) k_hook_sumd(HookArgs a) {
   if (a.gate == kGateIfPlain && __ldg(&a.ctrl->use_sum)) return;
+  if (a.gate == kGateIfSum && !__ldg(&a.ctrl->use_sum)) return;
   hook_stream<kHookEPT, false, false, true, true, false>(a);
 }
 
@@ -1012,7 +1027,15 @@ __global__ void __launch_bounds__(kHookSumdCta, 1) k_hook_sumd(HookArgs a) {
 // stragglers, §3.2); spills 40 B.
 __global__ void __launch_bounds__(kHookSumdCta, 1) k_hook_sumd_dyn(HookArgs a) {
   if (a.gate == kGateIfPlain && __ldg(&a.ctrl->use_sum)) return;
+  if (a.gate == kGateIfSum && !__ldg(&a.ctrl->use_sum)) return;
   hook_stream<kHookEPT, false, false, true, true, true>(a);
+}
+
+// The large-forest build over a truncated (prefix) summary.
+__global__ void __launch_bounds__(kHookSumdCta, 1) k_hook_sumd_pfx(HookArgs a) {
+  if (a.gate == kGateIfPlain && __ldg(&a.ctrl->use_sum)) return;
+  if (a.gate == kGateIfSum && !__ldg(&a.ctrl->use_sum)) return;
+  hook_stream<kHookEPT, false, false, true, true, true, true>(a);
 }
 
 // Streaming hook with the star-0 summary in shared memory (full warps,
@@ -1484,7 +1507,7 @@ __global__ void k_step_segment(DevCtrl* c, DevRec* recs,
 // store ratio (records are per segment).
 __global__ void k_step_adapt(DevCtrl* c, DevRec* recs, u64 m, u32 forming_pct,
                              const u32* sum, u32 sum_words, const uint2* edges,
-                             const u32* bits) {
+                             const u32* bits, int remainder_vote) {
   // Every thread derives the next range from the pass-start control words
   // (same addresses: broadcast reads), so the sample loads below issue
   // without waiting for thread 0's bookkeeping; thread 0 writes after the
@@ -1517,6 +1540,10 @@ __global__ void k_step_adapt(DevCtrl* c, DevRec* recs, u64 m, u32 forming_pct,
     c->seg_b = s_b;
     c->seg_e = s_e;
     c->seg = seg + 1;
+    // the summary-predicated hook streams the slot that takes every
+    // remaining edge (the steady regime: the forming slots' summaries cover
+    // little); the plain hook the others
+    if (remainder_vote) c->use_sum = (s_e == m && s_e > s_b) ? 1u : 0u;
     c->passes += (len > 0);
     c->dirty = 0;
     next_rec(c, recs);
