@@ -576,12 +576,18 @@ void launch_hook_sumd(hcc_ctx* c, const Plan& P, cudaStream_t s, const HookArgs&
 
 // Segment hook of the adaptive / atomic engines (no appends).  HCC_SEG_CAS=0
 // uses the worklist passes' 768-thread k_hook_cas instead.
+// With a one-bit-per-word star summary, the summary-predicated build
+// (k_hook_seg_cas_sumd; HCC_SEG_SUMD=0 disables).
 void launch_seg_cas(const Plan& P, cudaStream_t s, const HookArgs& a) {
   static const int v = std::getenv("HCC_SEG_CAS") ? std::atoi(std::getenv("HCC_SEG_CAS")) : 1;
-  if (v)
+  static const int sd = std::getenv("HCC_SEG_SUMD") ? std::atoi(std::getenv("HCC_SEG_SUMD")) : 1;
+  if (v && sd && P.sum && P.sum_shift == 0 && a.s0f) {
+    k_hook_seg_cas_sumd<<<P.grid_hook, kHookCta, (size_t)sum_region_words(a.s0f_words) * 4, s>>>(a);
+  } else if (v) {
     k_hook_seg_cas<<<P.grid_hook, kHookCta, 0, s>>>(a);
-  else
+  } else {
     k_hook_cas<<<P.grid_cas, kHookCasCta, 0, s>>>(a);
+  }
 }
 
 // The summary hook (one CTA per SM, the summary and queues in shared memory).
@@ -820,6 +826,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           a.rec_idx = (int)i;
           a.dslot = (int)(i & 1);
           a.dyn = P.dyn ? 1 : 0;
+          if (P.sum) use_s0b(c, P, a);
           a.pick = i >= 1 && (int)i <= picks && i + 1 < P.nseg ? 1 : 0;
           c->slot_kernel.push_back(HCC_HOOK_KERNEL_CAS);
           launch_seg_cas(P, q.s(), a);
@@ -843,6 +850,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           a.chunked = 1;
           a.s0b = c->s0b;
           a.dyn = P.dyn ? 1 : 0;
+          if (P.sum) use_s0b(c, P, a);
           launch_seg_cas(P, q.s(), a);
           q.phase_done(HCC_PHASE_HOOK);
           k_star_pick<<<1, 32, 0, q.s()>>>(P.pi, P.n, ctrl);
@@ -1112,6 +1120,8 @@ int hcc_create(int device, hcc_ctx** out) {
   HCC_CUDA(cudaFuncSetAttribute(k_hook_sumd_dyn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 sumd_smem));
   HCC_CUDA(cudaFuncSetAttribute(k_hook_sumd_pfx, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                sumd_smem));
+  HCC_CUDA(cudaFuncSetAttribute(k_hook_seg_cas_sumd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 sumd_smem));
   HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_sumd, kHookSumdCta,
                                                           sumd_smem));
@@ -1872,7 +1882,7 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   if (P.s0b) {
     ensure_s0b(c, (n + 31) / 32);
   }
-  if (P.s0b && uses_wl) {
+  if (P.s0b && (uses_wl || cas_stream)) {
     // star-0 summary: the smallest group (2^shift bitmap words per bit)
     // whose table fits the hook's shared-memory budget; groups larger than
     // a compress block's 64 words are not built

@@ -1013,6 +1013,11 @@ __global__ void __launch_bounds__(kHookCta, HCC_HOOK_MINB) k_hook_seg_cas(HookAr
 #ifndef HCC_SUMD_HALVES
 #define HCC_SUMD_HALVES 0
 #endif
+// Adaptive / atomic segment hook with summary-predicated lookups.
+__global__ void __launch_bounds__(kHookCta, 1) k_hook_seg_cas_sumd(HookArgs a) {
+  hook_stream<kHookEPT, false, true, false, true, false>(a);
+}
+
 // Streaming hook with summary-predicated lookups (the summary in shared
 // memory, no slow-path queues: 64 KB instead of 128 KB of shared memory).
 // Static schedule: the dynamic one's state made it spill 40 B (measured on
