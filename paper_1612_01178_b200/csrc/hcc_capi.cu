@@ -1,5 +1,7 @@
 // C-ABI implementation of libhookcc_cuda.so: contexts, graph handles,
-// device forests and the CC engines.
+// device forests and the CC engines.  (Multi-device contexts:
+// hcc_multi_host.cu; the multi-process IPC merge: hcc_peer.cu; shared
+// handles and helpers: hcc_host.cuh.)
 //
 // Engines (reference drivers, /root/reference/proj/include/hookcc/engines.hpp):
 //   BASELINE     (123-179)  loop { hook all edges ; loop { jump } } until no
@@ -32,15 +34,15 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include "hookcc_gen.h"
-#include "hcc_internal.cuh"
-#include "hookcc_c.h"
+#include "hcc_host.cuh"
 
-using namespace hcc;
+using namespace hcc::host;
 
 // ---------------------------------------------------------------------------
 // errors
 
-namespace {
+namespace hcc {
+namespace host {
 
 thread_local std::string g_err;
 
@@ -49,37 +51,11 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
-struct CudaFail {
-  int code;
-};
+}  // namespace host
+}  // namespace hcc
 
-#define HCC_CUDA(call)                                                       \
-  do {                                                                       \
-    cudaError_t e_ = (call);                                                 \
-    if (e_ != cudaSuccess) {                                                 \
-      g_err = std::string(#call) + ": " + cudaGetErrorString(e_);            \
-      throw CudaFail{e_ == cudaErrorMemoryAllocation ? HCC_ENOMEM           \
-                                                      : HCC_ECUDA};         \
-    }                                                                        \
-  } while (0)
+namespace {
 
-#define HCC_GUARD_BEGIN try {
-#define HCC_GUARD_END                                                        \
-  }                                                                          \
-  catch (const CudaFail& f) {                                                \
-    return f.code;                                                           \
-  }                                                                          \
-  catch (const std::bad_alloc&) {                                            \
-    return fail(HCC_ENOMEM, "host allocation failed");                       \
-  }                                                                          \
-  catch (const std::exception& ex) {                                         \
-    return fail(HCC_ECUDA, ex.what());                                       \
-  }
-
-// Device-side narrowing works on 32-bit ids.
-constexpr u64 kMaxN = 0xffffffffull;
-// Topology segments unrolled into the root graph (with per-launch events).
-constexpr u64 kMaxUnrolledSegments = 64;
 // Root-walk steps of the atomic-free hook before an unconditional store
 // (HCC_WALK overrides, for tuning).
 // Root-walk bound (HCC_WALK) and the steady slot's (HCC_WALK_LAST).  In
@@ -123,128 +99,8 @@ int usable_devices() {
 
 }  // namespace
 
-// ---------------------------------------------------------------------------
-// handles
-
-// Per-shard state of a multi-device merge (hcc_create_multi).
-struct MergeShard {
-  u32* bits = nullptr;       // export bitmap, ceil(n/32) words
-  u64 bits_words = 0;
-  uint2* pairs = nullptr;    // export pairs
-  u64 cap = 0;
-  u64* cnt = nullptr;        // device: pairs the export produced
-  PeerTab* tab = nullptr;    // device: every shard's export buffers
-  bool tab_dirty = true;
-  cudaEvent_t ev_exp = nullptr, ev_t0 = nullptr, ev_m0 = nullptr, ev_t1 = nullptr;
-  hcc_forest* forest = nullptr;  // local forest (shard 0 may use the caller's)
-  double local_ms = 0, merge_ms = 0, total_ms = 0;
-  u64 passes = 0, records = 0, exported = 0, linked = 0;
-};
-
-struct GraphKey {
-  int algo = -1;
-  const void* edges = nullptr;
-  const void* pi = nullptr;
-  const void* wl0 = nullptr;
-  const void* wl1 = nullptr;
-  const void* s0b = nullptr;
-  const void* s0f = nullptr;
-  u64 wl_cap = 0;
-  u64 n = 0, m = 0, nseg = 0, max_threads = 0;
-  u32 flags = 0;
-  int walk = 0;
-  u64 plan = 0;
-  bool s0b_on = false;
-  bool sum = false;
-  bool operator==(const GraphKey& o) const {
-    return algo == o.algo && edges == o.edges && pi == o.pi && wl0 == o.wl0 &&
-           wl1 == o.wl1 && s0b == o.s0b && s0f == o.s0f && wl_cap == o.wl_cap &&
-           n == o.n && m == o.m && nseg == o.nseg &&
-           max_threads == o.max_threads && flags == o.flags && walk == o.walk &&
-           plan == o.plan && s0b_on == o.s0b_on && sum == o.sum;
-  }
-};
-
-struct hcc_ctx {
-  int dev = 0;
-  int sms = 148;
-  cudaStream_t stream = nullptr;
-  DevCtrl* d_ctrl = nullptr;
-  DevRec* d_recs = nullptr;
-  DevCtrl* h_ctrl = nullptr;  // pinned
-  DevRec* h_recs = nullptr;   // pinned
-  u32* scratch_pi = nullptr;
-  u64 scratch_n = 0;
-  uint2* wl[2] = {nullptr, nullptr};
-  u64 wl_cap = 0;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  int occ_hook = 1, occ_vert = 1, occ_hook_sum = 1, occ_hook_cas = 1, occ_hook_sum_cas = 1,
-      occ_hook_sumd = 1;
-  // cached executable graph for repeated calls with identical arguments,
-  // plus the previous one (two graphs used alternately, e.g. a pipelined
-  // upload into one while the other runs, keep both instantiated)
-  cudaGraphExec_t exec = nullptr;
-  GraphKey key;
-  cudaGraphExec_t alt_exec = nullptr;
-  GraphKey alt_key;
-  u64 alt_seg_ev = 0;
-  std::vector<int> alt_slot_kernel;
-  int alt_wl_kernel = 0;
-  cudaStream_t copy_stream = nullptr;  // hcc_graph_upload_async
-  cudaEvent_t order_ev = nullptr;      // copy stream after the context stream
-  cudaStream_t check_stream = nullptr; // endpoint checks of landed chunks
-  std::vector<cudaEvent_t> chunk_ev;   // one per in-flight upload chunk
-  std::vector<hcc_segment_rec> last_recs;
-  // CUDA events around the unrolled topology hook launches
-  std::vector<cudaEvent_t> seg_ev;   // 2 per segment
-  u64 seg_ev_used = 0;
-  u64 exec_seg_ev = 0;  // seg_ev_used of the cached executable graph
-  // hook kernel per unrolled slot (HCC_HOOK_KERNEL_*; SUM means "voted:
-  // summary or streaming") and of the worklist passes, as enqueued
-  std::vector<int> slot_kernel, exec_slot_kernel;
-  int wl_kernel = 0, exec_wl_kernel = 0;
-  u32* s0b = nullptr;  // star-0 bitmap
-  u32* s0b_base = nullptr;  // its allocation
-  u64 s0b_words = 0;
-  u32* s0f = nullptr;  // star-0 summary (one bit per group of bitmap words)
-  u64 s0f_words = 0;
-  // a worklist overflowed once: size the lists to m from now on
-  bool wl_full = false;
-  // multi-device context (hcc_create_multi): one sub-context per edge
-  // shard (devices may repeat), merge buffers per shard
-  std::vector<hcc_ctx*> subs;
-  std::vector<MergeShard> merge;
-  int peer_access = 0;
-  // multi-process merge over CUDA IPC (hcc_peer_*)
-  struct hcc_peer_state* peer = nullptr;
-};
-
-struct hcc_graph {
-  hcc_ctx* ctx = nullptr;
-  u64 n = 0, m = 0;
-  u64 first = 0;  // global index of edge 0 (ranged / shard graphs)
-  // multi-device graph: shard r (partition_edges(m, shards)) on ctx->subs[r]
-  std::vector<hcc_graph*> shards;
-  std::vector<u64> bounds;
-  uint2* d_edges = nullptr;
-  bool has_stats = false;
-  hcc_graph_stats stats{};
-  // hcc_graph_upload_async: copy + endpoint check in flight on the
-  // context's copy stream; every reader waits for it (graph_ready)
-  mutable bool pending = false;
-  cudaEvent_t up_ev = nullptr;
-  u32* d_err = nullptr;  // device endpoint-check flag
-  u32* h_err = nullptr;  // pinned copy of it
-};
-
-struct hcc_forest {
-  hcc_ctx* ctx = nullptr;
-  int dev = 0;
-  u64 n = 0;
-  u32* d_pi = nullptr;
-};
-
-namespace {
+namespace hcc {
+namespace host {
 
 // Per-host-thread scratch for element operations (ParentForest API):
 // results travel through a pinned buffer on the thread's default stream.
@@ -1052,280 +908,19 @@ void rehook_loop(hcc_ctx* c, const Plan& P) {
   });
 }
 
-}  // namespace
+// (plan + host-stepped loop: the multi-GPU merges)
+void enqueue_rehook(hcc_ctx* c, u32* pi, u64 n) { rehook_loop(c, rehook_plan(c, pi, n)); }
 
-// Multi-device contexts (single process, one sub-context per edge shard;
-// implemented at the end of this file).
-static int multi_from_edges(hcc_ctx* c, const void* uv, bool wide, u64 m, u64 n,
-                            hcc_graph** out);
-static int multi_generate(hcc_ctx* c, const char* spec, u64 seed, u64 n, u64 first, u64 count,
-                          hcc_graph** out);
-static int multi_range_io(hcc_ctx* c, hcc_graph* g, uint32_t* uv, u64 first, u64 count, int op);
-static int multi_stats(hcc_ctx* c, const hcc_graph* g, hcc_graph_stats* out);
-static int multi_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o, hcc_forest* f,
-                    uint32_t* lab32, uint64_t* lab64, hcc_metrics* mx);
+}  // namespace host
+}  // namespace hcc
 
-// ===========================================================================
-// C-ABI
-
-extern "C" {
-
-int hcc_abi_version(void) { return HCC_ABI_VERSION; }
-
-const char* hcc_last_error(void) { return g_err.c_str(); }
-
-int hcc_device_count(void) { return usable_devices(); }
-
-int hcc_create(int device, hcc_ctx** out) {
-  if (!out) return fail(HCC_EINVAL, "null output");
-  *out = nullptr;
-  int count = 0;
-  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
-    cudaGetLastError();
-    return fail(HCC_ENODEV, "no CUDA device visible (libhookcc_cuda has no "
-                            "CPU fallback)");
-  }
-  if (device < 0 || device >= count)
-    return fail(HCC_EINVAL, "device index out of range");
-  cudaDeviceProp prop;
-  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess)
-    return fail(HCC_ECUDA, "cudaGetDeviceProperties failed");
-  if (prop.major != 10)
-    return fail(HCC_ENODEV, std::string("device ") + prop.name +
-                                " is not sm_100 (this build targets sm_100a)");
-  hcc_ctx* c = new hcc_ctx;
-  HCC_GUARD_BEGIN
-  c->dev = device;
-  HCC_CUDA(cudaSetDevice(device));
-  c->sms = prop.multiProcessorCount;
-  HCC_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-  HCC_CUDA(cudaMalloc(&c->d_ctrl, sizeof(DevCtrl)));
-  HCC_CUDA(cudaMalloc(&c->d_recs, sizeof(DevRec) * kMaxRecs));
-  HCC_CUDA(cudaMallocHost(&c->h_ctrl, sizeof(DevCtrl)));
-  HCC_CUDA(cudaMallocHost(&c->h_recs, sizeof(DevRec) * kMaxRecs));
-  HCC_CUDA(cudaMemset(c->d_ctrl, 0, sizeof(DevCtrl)));
-  HCC_CUDA(cudaEventCreate(&c->ev0));
-  HCC_CUDA(cudaEventCreate(&c->ev1));
-  int occ = 0;
-  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook, kHookCta, 0));
-  c->occ_hook = std::max(occ, 1);
-  // the summary hook stages the star-0 summary and its slow-path queues
-  HCC_CUDA(cudaFuncSetAttribute(k_hook_sum, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)kHookSmemMax));
-  HCC_CUDA(cudaFuncSetAttribute(k_hook_sum_cas, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)kHookSmemMax));
-  const int sumd_smem = (int)sum_region_words(kS0fMaxBytes / 4) * 4;
-  HCC_CUDA(cudaFuncSetAttribute(k_hook_sumd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                sumd_smem));
-  HCC_CUDA(cudaFuncSetAttribute(k_hook_sumd_dyn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                sumd_smem));
-  HCC_CUDA(cudaFuncSetAttribute(k_hook_sumd_pfx, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                sumd_smem));
-  HCC_CUDA(cudaFuncSetAttribute(k_hook_seg_cas_sumd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                sumd_smem));
-  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_sumd, kHookSumdCta,
-                                                          sumd_smem));
-  c->occ_hook_sumd = std::max(occ, 1);
-  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_sum, kHookSumCta,
-                                                          kHookSmemMax));
-  c->occ_hook_sum = std::max(occ, 1);
-  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_sum_cas, kHookCasCta,
-                                                          kHookSmemMax));
-  c->occ_hook_sum_cas = std::max(occ, 1);
-  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_cas, kHookCasCta, 0));
-  c->occ_hook_cas = std::max(occ, 1);
-#if HCC_SMALL_CARVE >= 0
-  HCC_CUDA(cudaFuncSetAttribute(k_hook_small, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                HCC_SMALL_CARVE));
-#endif
-#if HCC_HOOK_CARVE >= 0
-  HCC_CUDA(cudaFuncSetAttribute(k_hook, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                HCC_HOOK_CARVE));
-  HCC_CUDA(cudaFuncSetAttribute(k_hook_cas, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                HCC_HOOK_CARVE));
-#endif
-#if HCC_COMP_CARVE >= 0
-  HCC_CUDA(cudaFuncSetAttribute(k_compress_s0b, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                HCC_COMP_CARVE));
-#endif
-  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_compress,
-                                                          kVertThreads, 0));
-  c->occ_vert = std::max(occ, 1);
-  *out = c;
-  return HCC_OK;
-  }
-  catch (const CudaFail& f) {
-    hcc_destroy(c);
-    return f.code;
-  }
-}
-
-static void peer_release(hcc_ctx* c);
-
-int hcc_destroy(hcc_ctx* c) {
-  if (!c) return HCC_OK;
-  peer_release(c);
-  for (size_t r = 0; r < c->merge.size(); ++r) {
-    MergeShard& ms = c->merge[r];
-    if (r < c->subs.size()) cudaSetDevice(c->subs[r]->dev);
-    if (ms.forest) hcc_forest_free(ms.forest);
-    cudaFree(ms.bits);
-    cudaFree(ms.pairs);
-    cudaFree(ms.cnt);
-    cudaFree(ms.tab);
-    for (cudaEvent_t ev : {ms.ev_exp, ms.ev_t0, ms.ev_m0, ms.ev_t1})
-      if (ev) cudaEventDestroy(ev);
-  }
-  for (hcc_ctx* sc : c->subs) hcc_destroy(sc);
-  cudaSetDevice(c->dev);
-  drop_exec(c);
-  if (c->stream) cudaStreamSynchronize(c->stream);
-  cudaFree(c->d_ctrl);
-  cudaFree(c->d_recs);
-  cudaFreeHost(c->h_ctrl);
-  cudaFreeHost(c->h_recs);
-  cudaFree(c->scratch_pi);
-  cudaFree(c->wl[0]);
-  cudaFree(c->wl[1]);
-  cudaFree(c->s0b_base);
-  cudaFree(c->s0f);
-  for (cudaEvent_t ev : c->seg_ev) cudaEventDestroy(ev);
-  if (c->ev0) cudaEventDestroy(c->ev0);
-  if (c->ev1) cudaEventDestroy(c->ev1);
-  if (c->stream) cudaStreamDestroy(c->stream);
-  if (c->copy_stream) {
-    cudaStreamSynchronize(c->copy_stream);
-    cudaStreamDestroy(c->copy_stream);
-  }
-  if (c->check_stream) {
-    cudaStreamSynchronize(c->check_stream);
-    cudaStreamDestroy(c->check_stream);
-  }
-  if (c->order_ev) cudaEventDestroy(c->order_ev);
-  for (cudaEvent_t ev : c->chunk_ev) cudaEventDestroy(ev);
-  delete c;
-  return HCC_OK;
-}
-
-int hcc_ctx_segments(hcc_ctx* c, hcc_segment_rec* out, uint64_t cap,
-                     uint64_t* count) {
-  if (!c) return fail(HCC_EINVAL, "null context");
-  u64 k = std::min<u64>(cap, c->last_recs.size());
-  if (out)
-    for (u64 i = 0; i < k; ++i) out[i] = c->last_recs[i];
-  if (count) *count = c->last_recs.size();
-  return HCC_OK;
-}
-
-int hcc_ctx_sm_count(hcc_ctx* c, int* out) {
-  if (!c || !out) return fail(HCC_EINVAL, "null argument");
-  *out = c->sms;
-  return HCC_OK;
-}
-
-// ---- graphs ----------------------------------------------------------------
-
-int hcc_graph_from_edges_u64(hcc_ctx* c, const uint64_t* uv, uint64_t m,
-                             uint64_t n, hcc_graph** out) {
-  if (!out) return fail(HCC_EINVAL, "null output");
-  *out = nullptr;
-  if (int r = ctx_enter(c)) return r;
-  if (n > kMaxN)
-    return fail(HCC_EINVAL, "vertex count >= 2^32 is not supported by the "
-                            "device forest (u32 ids)");
-  if (m > 0 && !uv) return fail(HCC_EINVAL, "null edge buffer");
-  if (!c->subs.empty()) return multi_from_edges(c, uv, true, m, n, out);
-  hcc_graph* g = new hcc_graph;
-  g->ctx = c;
-  g->n = n;
-  g->m = m;
-  u64* stage = nullptr;
-  u32* d_err = nullptr;
-  HCC_GUARD_BEGIN
-  HCC_CUDA(cudaMalloc(&g->d_edges, std::max<u64>(m, 2) * sizeof(uint2)));
-  HCC_CUDA(cudaMalloc(&d_err, sizeof(u32)));
-  HCC_CUDA(cudaMemsetAsync(d_err, 0, sizeof(u32), c->stream));
-  const u64 chunk = std::min<u64>(m, 1ull << 26);  // 1 GiB of u64 pairs
-  if (m > 0) HCC_CUDA(cudaMalloc(&stage, chunk * 2 * sizeof(u64)));
-  for (u64 off = 0; off < m; off += chunk) {
-    u64 k = std::min(chunk, m - off);
-    HCC_CUDA(cudaMemcpyAsync(stage, uv + 2 * off, k * 2 * sizeof(u64),
-                             cudaMemcpyHostToDevice, c->stream));
-    k_narrow_u64<<<grid_for(k, 256, 65536), 256, 0, c->stream>>>(
-        stage, g->d_edges + off, k, n, d_err);
-    HCC_CUDA(cudaGetLastError());
-  }
-  u32 err = 0;
-  HCC_CUDA(cudaMemcpyAsync(&err, d_err, sizeof(u32), cudaMemcpyDeviceToHost,
-                           c->stream));
-  HCC_CUDA(cudaStreamSynchronize(c->stream));
-  cudaFree(stage);
-  cudaFree(d_err);
-  stage = nullptr;
-  d_err = nullptr;
-  if (err) {
-    hcc_graph_free(g);
-    return fail(HCC_ERANGE, "edge endpoint out of range");
-  }
-  *out = g;
-  return HCC_OK;
-  }
-  catch (const CudaFail& f) {
-    cudaFree(stage);
-    cudaFree(d_err);
-    hcc_graph_free(g);
-    return f.code;
-  }
-}
-
-int hcc_graph_from_edges_u32(hcc_ctx* c, const uint32_t* uv, uint64_t m,
-                             uint64_t n, hcc_graph** out) {
-  if (!out) return fail(HCC_EINVAL, "null output");
-  *out = nullptr;
-  if (int r = ctx_enter(c)) return r;
-  if (n > kMaxN) return fail(HCC_EINVAL, "vertex count >= 2^32");
-  if (m > 0 && !uv) return fail(HCC_EINVAL, "null edge buffer");
-  if (!c->subs.empty()) return multi_from_edges(c, uv, false, m, n, out);
-  hcc_graph* g = new hcc_graph;
-  g->ctx = c;
-  g->n = n;
-  g->m = m;
-  u32* d_err = nullptr;
-  HCC_GUARD_BEGIN
-  HCC_CUDA(cudaMalloc(&g->d_edges, std::max<u64>(m, 2) * sizeof(uint2)));
-  HCC_CUDA(cudaMalloc(&d_err, sizeof(u32)));
-  HCC_CUDA(cudaMemsetAsync(d_err, 0, sizeof(u32), c->stream));
-  if (m > 0) {
-    HCC_CUDA(cudaMemcpyAsync(g->d_edges, uv, m * sizeof(uint2),
-                             cudaMemcpyHostToDevice, c->stream));
-    k_check_u32<<<grid_for(m, 256, 65536), 256, 0, c->stream>>>(g->d_edges, m,
-                                                                n, d_err);
-    HCC_CUDA(cudaGetLastError());
-  }
-  u32 err = 0;
-  HCC_CUDA(cudaMemcpyAsync(&err, d_err, sizeof(u32), cudaMemcpyDeviceToHost,
-                           c->stream));
-  HCC_CUDA(cudaStreamSynchronize(c->stream));
-  cudaFree(d_err);
-  d_err = nullptr;
-  if (err) {
-    hcc_graph_free(g);
-    return fail(HCC_ERANGE, "edge endpoint out of range");
-  }
-  *out = g;
-  return HCC_OK;
-  }
-  catch (const CudaFail& f) {
-    cudaFree(d_err);
-    hcc_graph_free(g);
-    return f.code;
-  }
-}
+namespace hcc {
+namespace host {
 
 // Wait for a graph's pending asynchronous upload and report its endpoint
 // check (check_endpoints, graph.hpp:89-94).  Every entry point that reads a
 // graph's edges calls this first.
-static int graph_ready(const hcc_graph* g) {
+int graph_ready(const hcc_graph* g) {
   if (g)
     for (const hcc_graph* sh : g->shards)
       if (int r = graph_ready(sh)) return r;
@@ -1338,351 +933,8 @@ static int graph_ready(const hcc_graph* g) {
   return HCC_OK;
 }
 
-int hcc_graph_upload_async(hcc_ctx* c, hcc_graph* g, const uint32_t* uv, uint64_t first,
-                           uint64_t count) {
-  if (!g || (count && !uv)) return fail(HCC_EINVAL, "null argument");
-  if (first > g->m || count > g->m - first)
-    return fail(HCC_EINVAL, "range out of bounds");
-  if (int r = ctx_enter(c)) return r;
-  if (!g->shards.empty()) return multi_range_io(c, g, const_cast<uint32_t*>(uv), first, count, 0);
-  if (int r = graph_ready(g)) return r;  // one upload in flight per graph
-  HCC_GUARD_BEGIN
-  if (!c->copy_stream) {
-    HCC_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-    HCC_CUDA(cudaStreamCreateWithFlags(&c->check_stream, cudaStreamNonBlocking));
-  }
-  if (!g->up_ev) {
-    HCC_CUDA(cudaEventCreateWithFlags(&g->up_ev, cudaEventDisableTiming));
-    HCC_CUDA(cudaMalloc(&g->d_err, sizeof(u32)));
-    HCC_CUDA(cudaMallocHost(&g->h_err, sizeof(u32)));
-  }
-  // the graph's previous readers ran on the context stream
-  if (!c->order_ev) HCC_CUDA(cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming));
-  HCC_CUDA(cudaEventRecord(c->order_ev, c->stream));
-  HCC_CUDA(cudaStreamWaitEvent(c->copy_stream, c->order_ev, 0));
-  HCC_CUDA(cudaMemsetAsync(g->d_err, 0, sizeof(u32), c->copy_stream));
-  // chunked copy; each chunk's endpoint check runs on the check stream while
-  // the next chunk copies, so only the last check follows the transfer
-  constexpr u64 kChunk = 16ull << 20;  // edges (128 MiB)
-  const u64 nch = (count + kChunk - 1) / kChunk;
-  while (c->chunk_ev.size() < nch) {
-    cudaEvent_t ev;
-    HCC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    c->chunk_ev.push_back(ev);
-  }
-  HCC_CUDA(cudaEventRecord(c->order_ev, c->copy_stream));
-  HCC_CUDA(cudaStreamWaitEvent(c->check_stream, c->order_ev, 0));
-  for (u64 k = 0; k < nch; ++k) {
-    const u64 b = first + k * kChunk, cnt = std::min<u64>(kChunk, count - k * kChunk);
-    HCC_CUDA(cudaMemcpyAsync(g->d_edges + b, uv + 2 * (b - first), cnt * sizeof(uint2),
-                             cudaMemcpyHostToDevice, c->copy_stream));
-    HCC_CUDA(cudaEventRecord(c->chunk_ev[k], c->copy_stream));
-    HCC_CUDA(cudaStreamWaitEvent(c->check_stream, c->chunk_ev[k], 0));
-    k_check_u32<<<grid_for(cnt, 256, 65536), 256, 0, c->check_stream>>>(g->d_edges + b, cnt,
-                                                                        g->n, g->d_err);
-    HCC_CUDA(cudaGetLastError());
-  }
-  HCC_CUDA(cudaMemcpyAsync(g->h_err, g->d_err, sizeof(u32), cudaMemcpyDeviceToHost,
-                           c->check_stream));
-  HCC_CUDA(cudaEventRecord(g->up_ev, c->check_stream));
-  g->pending = true;
-  g->has_stats = false;
-  return HCC_OK;
-  HCC_GUARD_END
-}
-
-int hcc_graph_assign_edges_u32(hcc_ctx* c, hcc_graph* g, const uint32_t* uv,
-                               uint64_t first, uint64_t count) {
-  // the chunked upload with overlapped endpoint checks, then wait for it
-  if (int r = hcc_graph_upload_async(c, g, uv, first, count)) return r;
-  return graph_ready(g);
-}
-
-int hcc_graph_from_csr(hcc_ctx* c, const uint64_t* row_ptr, const uint32_t* col,
-                       uint64_t n, hcc_graph** out) {
-  if (!out) return fail(HCC_EINVAL, "null output");
-  *out = nullptr;
-  if (int r = ctx_enter(c)) return r;
-  if (n > kMaxN) return fail(HCC_EINVAL, "vertex count >= 2^32");
-  if (!row_ptr) return fail(HCC_EINVAL, "null row_ptr");
-  if (row_ptr[0] != 0) return fail(HCC_EINVAL, "row_ptr[0] must be 0");
-  for (u64 i = 0; i < n; ++i)
-    if (row_ptr[i + 1] < row_ptr[i])
-      return fail(HCC_EINVAL, "row_ptr must be non-decreasing");
-  const u64 m = row_ptr[n];
-  if (m > 0 && !col) return fail(HCC_EINVAL, "null col");
-  if (!c->subs.empty()) {
-    // sharded: expand on the host (row order), then partition the edge list
-    std::vector<u32> uv;
-    try {
-      uv.resize(2 * m);
-    } catch (const std::bad_alloc&) {
-      return fail(HCC_ENOMEM, "host allocation failed");
-    }
-    for (u64 u = 0; u < n; ++u)
-      for (u64 j = row_ptr[u]; j < row_ptr[u + 1]; ++j) {
-        if (col[j] >= n) return fail(HCC_ERANGE, "column index out of range");
-        uv[2 * j] = (u32)u;
-        uv[2 * j + 1] = col[j];
-      }
-    return multi_from_edges(c, uv.data(), false, m, n, out);
-  }
-  hcc_graph* g = new hcc_graph;
-  g->ctx = c;
-  g->n = n;
-  g->m = m;
-  u64* d_rp = nullptr;
-  u32 *d_col = nullptr, *d_err = nullptr;
-  HCC_GUARD_BEGIN
-  HCC_CUDA(cudaMalloc(&g->d_edges, std::max<u64>(m, 2) * sizeof(uint2)));
-  HCC_CUDA(cudaMalloc(&d_err, sizeof(u32)));
-  HCC_CUDA(cudaMemsetAsync(d_err, 0, sizeof(u32), c->stream));
-  if (m > 0) {
-    HCC_CUDA(cudaMalloc(&d_rp, (n + 1) * sizeof(u64)));
-    HCC_CUDA(cudaMalloc(&d_col, m * sizeof(u32)));
-    HCC_CUDA(cudaMemcpyAsync(d_rp, row_ptr, (n + 1) * sizeof(u64),
-                             cudaMemcpyHostToDevice, c->stream));
-    HCC_CUDA(cudaMemcpyAsync(d_col, col, m * sizeof(u32),
-                             cudaMemcpyHostToDevice, c->stream));
-    k_csr_expand<<<grid_for(m, 256, 65536), 256, 0, c->stream>>>(
-        d_rp, d_col, n, g->d_edges, m, d_err);
-    HCC_CUDA(cudaGetLastError());
-  }
-  u32 err = 0;
-  HCC_CUDA(cudaMemcpyAsync(&err, d_err, sizeof(u32), cudaMemcpyDeviceToHost,
-                           c->stream));
-  HCC_CUDA(cudaStreamSynchronize(c->stream));
-  cudaFree(d_rp);
-  cudaFree(d_col);
-  cudaFree(d_err);
-  d_rp = nullptr;
-  d_col = nullptr;
-  d_err = nullptr;
-  if (err) {
-    hcc_graph_free(g);
-    return fail(HCC_ERANGE, "column index out of range");
-  }
-  *out = g;
-  return HCC_OK;
-  }
-  catch (const CudaFail& f) {
-    cudaFree(d_rp);
-    cudaFree(d_col);
-    cudaFree(d_err);
-    hcc_graph_free(g);
-    return f.code;
-  }
-}
-
-static int generate_impl(hcc_ctx* c, const char* spec_c, uint64_t default_seed,
-                         bool ranged, u64 first, u64 count, hcc_graph** out) {
-  if (!out || !spec_c) return fail(HCC_EINVAL, "null argument");
-  *out = nullptr;
-  if (int r = ctx_enter(c)) return r;
-  std::string spec(spec_c);
-  size_t colon = spec.find(':');
-  if (colon == std::string::npos)
-    return fail(HCC_EINVAL, "generator spec needs the form kind:params");
-  std::string kind = spec.substr(0, colon), params = spec.substr(colon + 1);
-  u64 n = 0, m = 0, rows = 0, cols = 0, seed = default_seed, scale = 0, ef = 0;
-  double a = 0.57, b = 0.19, cc = 0.19, d = 0.05;
-  std::string v;
-  if (kind == "grid") {
-    size_t x = params.find('x');
-    if (x == std::string::npos || !parse_u64(params.substr(0, x), &rows) ||
-        !parse_u64(params.substr(x + 1), &cols))
-      return fail(HCC_EINVAL, "grid spec needs RxC");
-    if (rows == 0 || cols == 0) return fail(HCC_EINVAL, "grid: zero vertices");
-    n = rows * cols;
-    m = rows * (cols - 1) + (rows - 1) * cols;
-  } else if (kind == "rmatx") {
-    if (!spec_get(params, "scale", &v) || !parse_u64(v, &scale) ||
-        !spec_get(params, "ef", &v) || !parse_u64(v, &ef))
-      return fail(HCC_EINVAL, "rmatx spec needs scale= and ef=");
-    if (scale > 32) return fail(HCC_EINVAL, "rmatx: scale > 32");
-    if (spec_get(params, "seed", &v) && !parse_u64(v, &seed))
-      return fail(HCC_EINVAL, "rmatx: bad seed");
-    if (spec_get(params, "a", &v)) a = atof(v.c_str());
-    if (spec_get(params, "b", &v)) b = atof(v.c_str());
-    if (spec_get(params, "c", &v)) cc = atof(v.c_str());
-    if (spec_get(params, "d", &v)) d = atof(v.c_str());
-    if (std::fabs(a + b + cc + d - 1.0) > 1e-9)
-      return fail(HCC_EINVAL, "rmat: quadrant probabilities must sum to 1");
-    n = 1ull << scale;
-    m = ef * n;
-  } else if (kind == "erx") {
-    if (!spec_get(params, "n", &v) || !parse_u64(v, &n) ||
-        !spec_get(params, "m", &v) || !parse_u64(v, &m))
-      return fail(HCC_EINVAL, "erx spec needs n= and m=");
-    if (spec_get(params, "seed", &v) && !parse_u64(v, &seed))
-      return fail(HCC_EINVAL, "erx: bad seed");
-    if (n == 0) return fail(HCC_EINVAL, "erdos_renyi: zero vertices");
-  } else {
-    return fail(HCC_EINVAL, "unknown device generator kind `" + kind + "`");
-  }
-  if (n > kMaxN + 1 || (kind != "rmatx" && n > kMaxN))
-    return fail(HCC_EINVAL, "vertex count >= 2^32");
-  if (kind == "rmatx" && n > kMaxN)
-    return fail(HCC_EINVAL, "rmatx: scale 32 needs 2^32 vertices (> u32)");
-  if (ranged) {
-    if (first > m || count > m - first)
-      return fail(HCC_EINVAL, "generator range out of bounds");
-  } else {
-    first = 0;
-    count = m;
-  }
-  if (!c->subs.empty()) return multi_generate(c, spec_c, default_seed, n, first, count, out);
-  hcc_graph* g = new hcc_graph;
-  g->ctx = c;
-  g->n = n;
-  g->m = count;
-  g->first = first;
-  HCC_GUARD_BEGIN
-  HCC_CUDA(cudaMalloc(&g->d_edges, std::max<u64>(count, 2) * sizeof(uint2)));
-  if (count > 0) {
-    unsigned grid = grid_for(count, 256, (u64)c->sms * 32);
-    if (kind == "grid") {
-      k_gen_grid<<<grid, 256, 0, c->stream>>>(g->d_edges, rows, cols, first, count);
-    } else if (kind == "rmatx") {
-      k_gen_rmatx<<<grid, 256, 0, c->stream>>>(
-          g->d_edges, first, count, (u32)scale, seed, prob_threshold(a),
-          prob_threshold(a + b), prob_threshold(a + b + cc));
-    } else {
-      k_gen_erx<<<grid, 256, 0, c->stream>>>(g->d_edges, first, count, n, seed);
-    }
-    HCC_CUDA(cudaGetLastError());
-  }
-  HCC_CUDA(cudaStreamSynchronize(c->stream));
-  *out = g;
-  return HCC_OK;
-  }
-  catch (const CudaFail& f) {
-    hcc_graph_free(g);
-    return f.code;
-  }
-}
-
-int hcc_graph_generate(hcc_ctx* c, const char* spec, uint64_t default_seed,
-                       hcc_graph** out) {
-  return generate_impl(c, spec, default_seed, false, 0, 0, out);
-}
-
-int hcc_graph_generate_range(hcc_ctx* c, const char* spec, uint64_t default_seed,
-                             uint64_t first, uint64_t count, hcc_graph** out) {
-  return generate_impl(c, spec, default_seed, true, first, count, out);
-}
-
-int hcc_graph_info(const hcc_graph* g, uint64_t* n, uint64_t* m) {
-  if (!g) return fail(HCC_EINVAL, "null graph");
-  if (n) *n = g->n;
-  if (m) *m = g->m;
-  return HCC_OK;
-}
-
-int hcc_graph_download_u32(hcc_ctx* c, const hcc_graph* g, uint32_t* uv,
-                           uint64_t first, uint64_t count) {
-  if (int r = graph_ready(g)) return r;
-  if (!g || (count && !uv)) return fail(HCC_EINVAL, "null argument");
-  if (first > g->m || count > g->m - first)
-    return fail(HCC_EINVAL, "range out of bounds");
-  if (int r = ctx_enter(c)) return r;
-  if (!g->shards.empty())
-    return multi_range_io(c, const_cast<hcc_graph*>(g), uv, first, count, 2);
-  HCC_GUARD_BEGIN
-  if (count)
-    HCC_CUDA(cudaMemcpy(uv, g->d_edges + first, count * sizeof(uint2),
-                        cudaMemcpyDeviceToHost));
-  return HCC_OK;
-  HCC_GUARD_END
-}
-
-int hcc_graph_checksum(hcc_ctx* c, const hcc_graph* g, uint64_t* out) {
-  if (int r = graph_ready(g)) return r;
-  if (!g || !out) return fail(HCC_EINVAL, "null argument");
-  if (int r = ctx_enter(c)) return r;
-  if (!g->shards.empty()) {  // position-keyed terms: the shard sums add up
-    u64 sum = 0;
-    for (size_t r = 0; r < g->shards.size(); ++r) {
-      uint64_t x = 0;
-      if (int e = hcc_graph_checksum(c->subs[r], g->shards[r], &x)) return e;
-      sum += x;
-    }
-    *out = sum;
-    return HCC_OK;
-  }
-  u64* d = nullptr;
-  HCC_GUARD_BEGIN
-  HCC_CUDA(cudaMalloc(&d, sizeof(u64)));
-  HCC_CUDA(cudaMemsetAsync(d, 0, sizeof(u64), c->stream));
-  if (g->m)
-    k_checksum<<<grid_for(g->m, 256, (u64)c->sms * 16), 256, 0, c->stream>>>(
-        g->d_edges, g->m, g->first, d);
-  HCC_CUDA(cudaGetLastError());
-  HCC_CUDA(cudaMemcpyAsync(out, d, sizeof(u64), cudaMemcpyDeviceToHost,
-                           c->stream));
-  HCC_CUDA(cudaStreamSynchronize(c->stream));
-  cudaFree(d);
-  return HCC_OK;
-  }
-  catch (const CudaFail& f) {
-    cudaFree(d);
-    return f.code;
-  }
-}
-
-int hcc_graph_compute_stats(hcc_ctx* c, const hcc_graph* g_c,
-                            hcc_graph_stats* out) {
-  if (int r = graph_ready(g_c)) return r;
-  if (!g_c || !out) return fail(HCC_EINVAL, "null argument");
-  if (int r = ctx_enter(c)) return r;
-  hcc_graph* g = const_cast<hcc_graph*>(g_c);
-  if (!g->shards.empty() && !g->has_stats) {
-    if (int r = multi_stats(c, g, &g->stats)) return r;
-    g->has_stats = true;
-  }
-  HCC_GUARD_BEGIN
-  if (!g->has_stats)
-    if (int r = compute_stats_dev(c, g)) return r;
-  *out = g->stats;
-  return HCC_OK;
-  HCC_GUARD_END
-}
-
-int hcc_graph_free(hcc_graph* g) {
-  if (!g) return HCC_OK;
-  if (!g->shards.empty()) {
-    for (hcc_graph* sh : g->shards) hcc_graph_free(sh);
-    delete g;
-    return HCC_OK;
-  }
-  if (g->ctx) {
-    cudaSetDevice(g->ctx->dev);
-    // the cached executable graph may reference these edges
-    if (g->ctx->key.edges == g->d_edges || g->ctx->alt_key.edges == g->d_edges)
-      drop_exec(g->ctx);
-    if (g->pending) cudaEventSynchronize(g->up_ev);
-  }
-  if (g->up_ev) cudaEventDestroy(g->up_ev);
-  cudaFree(g->d_err);
-  cudaFreeHost(g->h_err);
-  cudaFree(g->d_edges);
-  delete g;
-  return HCC_OK;
-}
-
-uint64_t hcc_choose_segment_count(const hcc_graph_stats* st) {
-  // engines.hpp:35-41
-  if (!st || st->n == 0) return 1;
-  u64 s = (u64)std::floor(st->avg_degree + 0.5);
-  if (s < 1) s = 1;
-  if (st->m_stored > 0 && s > st->m_stored) s = st->m_stored;
-  return s;
-}
-
-// ---- the CC engine -----------------------------------------------------------
-
 // partition_edges(m, s) boundaries (engines.hpp:43-58).
-static std::vector<u64> uniform_bounds(u64 m, u64 s) {
+std::vector<u64> uniform_bounds(u64 m, u64 s) {
   std::vector<u64> b(s + 1, 0);
   const u64 q = m / s, r = m % s;
   for (u64 i = 0; i < s; ++i) b[i + 1] = b[i] + q + (i < r ? 1 : 0);
@@ -1695,7 +947,7 @@ static std::vector<u64> uniform_bounds(u64 m, u64 s) {
 // edges streams in the cheap regime where both endpoints already share a
 // star.  Every segment costs one compress over n, so few segments are used.
 // HCC_PLAN="geo:<k>:<growth>" overrides (first boundary m / 2^k).
-static std::vector<u64> geometric_bounds(u64 m) {
+std::vector<u64> geometric_bounds(u64 m) {
   int k = 7, growth = 8;
   if (const char* e = std::getenv("HCC_PLAN")) {
     int kk = 0, gg = 0;
@@ -1719,11 +971,11 @@ static std::vector<u64> geometric_bounds(u64 m) {
 // run_cc's internal "worklist overflowed, repeat" code (never returned).
 constexpr int kRerun = -1;
 
-static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
+int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
                   hcc_forest* f, hcc_metrics* mx);
 
 // run_cc, repeated once with m-sized worklists after an overflow.
-static int run_cc_sized(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o, hcc_forest* f,
+int run_cc_sized(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o, hcc_forest* f,
                         hcc_metrics* mx) {
   int r = run_cc(c, g, o, f, mx);
   if (r == kRerun) {
@@ -1734,7 +986,7 @@ static int run_cc_sized(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o, hcc_f
   return r;
 }
 
-static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
+int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
                   hcc_forest* f, hcc_metrics* mx) {
   if (int r = graph_ready(g)) return r;
   if (!g->shards.empty())
@@ -2218,6 +1470,607 @@ static int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   HCC_GUARD_END
 }
 
+}  // namespace host
+}  // namespace hcc
+
+// ===========================================================================
+// C-ABI
+
+extern "C" {
+
+int hcc_abi_version(void) { return HCC_ABI_VERSION; }
+
+const char* hcc_last_error(void) { return g_err.c_str(); }
+
+int hcc_device_count(void) { return usable_devices(); }
+
+int hcc_create(int device, hcc_ctx** out) {
+  if (!out) return fail(HCC_EINVAL, "null output");
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(HCC_ENODEV, "no CUDA device visible (libhookcc_cuda has no "
+                            "CPU fallback)");
+  }
+  if (device < 0 || device >= count)
+    return fail(HCC_EINVAL, "device index out of range");
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess)
+    return fail(HCC_ECUDA, "cudaGetDeviceProperties failed");
+  if (prop.major != 10)
+    return fail(HCC_ENODEV, std::string("device ") + prop.name +
+                                " is not sm_100 (this build targets sm_100a)");
+  hcc_ctx* c = new hcc_ctx;
+  HCC_GUARD_BEGIN
+  c->dev = device;
+  HCC_CUDA(cudaSetDevice(device));
+  c->sms = prop.multiProcessorCount;
+  HCC_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  HCC_CUDA(cudaMalloc(&c->d_ctrl, sizeof(DevCtrl)));
+  HCC_CUDA(cudaMalloc(&c->d_recs, sizeof(DevRec) * kMaxRecs));
+  HCC_CUDA(cudaMallocHost(&c->h_ctrl, sizeof(DevCtrl)));
+  HCC_CUDA(cudaMallocHost(&c->h_recs, sizeof(DevRec) * kMaxRecs));
+  HCC_CUDA(cudaMemset(c->d_ctrl, 0, sizeof(DevCtrl)));
+  HCC_CUDA(cudaEventCreate(&c->ev0));
+  HCC_CUDA(cudaEventCreate(&c->ev1));
+  int occ = 0;
+  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook, kHookCta, 0));
+  c->occ_hook = std::max(occ, 1);
+  // the summary hook stages the star-0 summary and its slow-path queues
+  HCC_CUDA(cudaFuncSetAttribute(k_hook_sum, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kHookSmemMax));
+  HCC_CUDA(cudaFuncSetAttribute(k_hook_sum_cas, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kHookSmemMax));
+  const int sumd_smem = (int)sum_region_words(kS0fMaxBytes / 4) * 4;
+  HCC_CUDA(cudaFuncSetAttribute(k_hook_sumd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                sumd_smem));
+  HCC_CUDA(cudaFuncSetAttribute(k_hook_sumd_dyn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                sumd_smem));
+  HCC_CUDA(cudaFuncSetAttribute(k_hook_sumd_pfx, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                sumd_smem));
+  HCC_CUDA(cudaFuncSetAttribute(k_hook_seg_cas_sumd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                sumd_smem));
+  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_sumd, kHookSumdCta,
+                                                          sumd_smem));
+  c->occ_hook_sumd = std::max(occ, 1);
+  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_sum, kHookSumCta,
+                                                          kHookSmemMax));
+  c->occ_hook_sum = std::max(occ, 1);
+  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_sum_cas, kHookCasCta,
+                                                          kHookSmemMax));
+  c->occ_hook_sum_cas = std::max(occ, 1);
+  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_cas, kHookCasCta, 0));
+  c->occ_hook_cas = std::max(occ, 1);
+#if HCC_SMALL_CARVE >= 0
+  HCC_CUDA(cudaFuncSetAttribute(k_hook_small, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                HCC_SMALL_CARVE));
+#endif
+#if HCC_HOOK_CARVE >= 0
+  HCC_CUDA(cudaFuncSetAttribute(k_hook, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                HCC_HOOK_CARVE));
+  HCC_CUDA(cudaFuncSetAttribute(k_hook_cas, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                HCC_HOOK_CARVE));
+#endif
+#if HCC_COMP_CARVE >= 0
+  HCC_CUDA(cudaFuncSetAttribute(k_compress_s0b, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                HCC_COMP_CARVE));
+#endif
+  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_compress,
+                                                          kVertThreads, 0));
+  c->occ_vert = std::max(occ, 1);
+  *out = c;
+  return HCC_OK;
+  }
+  catch (const CudaFail& f) {
+    hcc_destroy(c);
+    return f.code;
+  }
+}
+
+int hcc_destroy(hcc_ctx* c) {
+  if (!c) return HCC_OK;
+  peer_release(c);
+  for (size_t r = 0; r < c->merge.size(); ++r) {
+    MergeShard& ms = c->merge[r];
+    if (r < c->subs.size()) cudaSetDevice(c->subs[r]->dev);
+    if (ms.forest) hcc_forest_free(ms.forest);
+    cudaFree(ms.bits);
+    cudaFree(ms.pairs);
+    cudaFree(ms.cnt);
+    cudaFree(ms.tab);
+    for (cudaEvent_t ev : {ms.ev_exp, ms.ev_t0, ms.ev_m0, ms.ev_t1})
+      if (ev) cudaEventDestroy(ev);
+  }
+  for (hcc_ctx* sc : c->subs) hcc_destroy(sc);
+  cudaSetDevice(c->dev);
+  drop_exec(c);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  cudaFree(c->d_ctrl);
+  cudaFree(c->d_recs);
+  cudaFreeHost(c->h_ctrl);
+  cudaFreeHost(c->h_recs);
+  cudaFree(c->scratch_pi);
+  cudaFree(c->wl[0]);
+  cudaFree(c->wl[1]);
+  cudaFree(c->s0b_base);
+  cudaFree(c->s0f);
+  for (cudaEvent_t ev : c->seg_ev) cudaEventDestroy(ev);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->copy_stream) {
+    cudaStreamSynchronize(c->copy_stream);
+    cudaStreamDestroy(c->copy_stream);
+  }
+  if (c->check_stream) {
+    cudaStreamSynchronize(c->check_stream);
+    cudaStreamDestroy(c->check_stream);
+  }
+  if (c->order_ev) cudaEventDestroy(c->order_ev);
+  for (cudaEvent_t ev : c->chunk_ev) cudaEventDestroy(ev);
+  delete c;
+  return HCC_OK;
+}
+
+int hcc_ctx_segments(hcc_ctx* c, hcc_segment_rec* out, uint64_t cap,
+                     uint64_t* count) {
+  if (!c) return fail(HCC_EINVAL, "null context");
+  u64 k = std::min<u64>(cap, c->last_recs.size());
+  if (out)
+    for (u64 i = 0; i < k; ++i) out[i] = c->last_recs[i];
+  if (count) *count = c->last_recs.size();
+  return HCC_OK;
+}
+
+int hcc_ctx_sm_count(hcc_ctx* c, int* out) {
+  if (!c || !out) return fail(HCC_EINVAL, "null argument");
+  *out = c->sms;
+  return HCC_OK;
+}
+
+// ---- graphs ----------------------------------------------------------------
+
+int hcc_graph_from_edges_u64(hcc_ctx* c, const uint64_t* uv, uint64_t m,
+                             uint64_t n, hcc_graph** out) {
+  if (!out) return fail(HCC_EINVAL, "null output");
+  *out = nullptr;
+  if (int r = ctx_enter(c)) return r;
+  if (n > kMaxN)
+    return fail(HCC_EINVAL, "vertex count >= 2^32 is not supported by the "
+                            "device forest (u32 ids)");
+  if (m > 0 && !uv) return fail(HCC_EINVAL, "null edge buffer");
+  if (!c->subs.empty()) return multi_from_edges(c, uv, true, m, n, out);
+  hcc_graph* g = new hcc_graph;
+  g->ctx = c;
+  g->n = n;
+  g->m = m;
+  u64* stage = nullptr;
+  u32* d_err = nullptr;
+  HCC_GUARD_BEGIN
+  HCC_CUDA(cudaMalloc(&g->d_edges, std::max<u64>(m, 2) * sizeof(uint2)));
+  HCC_CUDA(cudaMalloc(&d_err, sizeof(u32)));
+  HCC_CUDA(cudaMemsetAsync(d_err, 0, sizeof(u32), c->stream));
+  const u64 chunk = std::min<u64>(m, 1ull << 26);  // 1 GiB of u64 pairs
+  if (m > 0) HCC_CUDA(cudaMalloc(&stage, chunk * 2 * sizeof(u64)));
+  for (u64 off = 0; off < m; off += chunk) {
+    u64 k = std::min(chunk, m - off);
+    HCC_CUDA(cudaMemcpyAsync(stage, uv + 2 * off, k * 2 * sizeof(u64),
+                             cudaMemcpyHostToDevice, c->stream));
+    k_narrow_u64<<<grid_for(k, 256, 65536), 256, 0, c->stream>>>(
+        stage, g->d_edges + off, k, n, d_err);
+    HCC_CUDA(cudaGetLastError());
+  }
+  u32 err = 0;
+  HCC_CUDA(cudaMemcpyAsync(&err, d_err, sizeof(u32), cudaMemcpyDeviceToHost,
+                           c->stream));
+  HCC_CUDA(cudaStreamSynchronize(c->stream));
+  cudaFree(stage);
+  cudaFree(d_err);
+  stage = nullptr;
+  d_err = nullptr;
+  if (err) {
+    hcc_graph_free(g);
+    return fail(HCC_ERANGE, "edge endpoint out of range");
+  }
+  *out = g;
+  return HCC_OK;
+  }
+  catch (const CudaFail& f) {
+    cudaFree(stage);
+    cudaFree(d_err);
+    hcc_graph_free(g);
+    return f.code;
+  }
+}
+
+int hcc_graph_from_edges_u32(hcc_ctx* c, const uint32_t* uv, uint64_t m,
+                             uint64_t n, hcc_graph** out) {
+  if (!out) return fail(HCC_EINVAL, "null output");
+  *out = nullptr;
+  if (int r = ctx_enter(c)) return r;
+  if (n > kMaxN) return fail(HCC_EINVAL, "vertex count >= 2^32");
+  if (m > 0 && !uv) return fail(HCC_EINVAL, "null edge buffer");
+  if (!c->subs.empty()) return multi_from_edges(c, uv, false, m, n, out);
+  hcc_graph* g = new hcc_graph;
+  g->ctx = c;
+  g->n = n;
+  g->m = m;
+  u32* d_err = nullptr;
+  HCC_GUARD_BEGIN
+  HCC_CUDA(cudaMalloc(&g->d_edges, std::max<u64>(m, 2) * sizeof(uint2)));
+  HCC_CUDA(cudaMalloc(&d_err, sizeof(u32)));
+  HCC_CUDA(cudaMemsetAsync(d_err, 0, sizeof(u32), c->stream));
+  if (m > 0) {
+    HCC_CUDA(cudaMemcpyAsync(g->d_edges, uv, m * sizeof(uint2),
+                             cudaMemcpyHostToDevice, c->stream));
+    k_check_u32<<<grid_for(m, 256, 65536), 256, 0, c->stream>>>(g->d_edges, m,
+                                                                n, d_err);
+    HCC_CUDA(cudaGetLastError());
+  }
+  u32 err = 0;
+  HCC_CUDA(cudaMemcpyAsync(&err, d_err, sizeof(u32), cudaMemcpyDeviceToHost,
+                           c->stream));
+  HCC_CUDA(cudaStreamSynchronize(c->stream));
+  cudaFree(d_err);
+  d_err = nullptr;
+  if (err) {
+    hcc_graph_free(g);
+    return fail(HCC_ERANGE, "edge endpoint out of range");
+  }
+  *out = g;
+  return HCC_OK;
+  }
+  catch (const CudaFail& f) {
+    cudaFree(d_err);
+    hcc_graph_free(g);
+    return f.code;
+  }
+}
+
+int hcc_graph_upload_async(hcc_ctx* c, hcc_graph* g, const uint32_t* uv, uint64_t first,
+                           uint64_t count) {
+  if (!g || (count && !uv)) return fail(HCC_EINVAL, "null argument");
+  if (first > g->m || count > g->m - first)
+    return fail(HCC_EINVAL, "range out of bounds");
+  if (int r = ctx_enter(c)) return r;
+  if (!g->shards.empty()) return multi_range_io(c, g, const_cast<uint32_t*>(uv), first, count, 0);
+  if (int r = graph_ready(g)) return r;  // one upload in flight per graph
+  HCC_GUARD_BEGIN
+  if (!c->copy_stream) {
+    HCC_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    HCC_CUDA(cudaStreamCreateWithFlags(&c->check_stream, cudaStreamNonBlocking));
+  }
+  if (!g->up_ev) {
+    HCC_CUDA(cudaEventCreateWithFlags(&g->up_ev, cudaEventDisableTiming));
+    HCC_CUDA(cudaMalloc(&g->d_err, sizeof(u32)));
+    HCC_CUDA(cudaMallocHost(&g->h_err, sizeof(u32)));
+  }
+  // the graph's previous readers ran on the context stream
+  if (!c->order_ev) HCC_CUDA(cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming));
+  HCC_CUDA(cudaEventRecord(c->order_ev, c->stream));
+  HCC_CUDA(cudaStreamWaitEvent(c->copy_stream, c->order_ev, 0));
+  HCC_CUDA(cudaMemsetAsync(g->d_err, 0, sizeof(u32), c->copy_stream));
+  // chunked copy; each chunk's endpoint check runs on the check stream while
+  // the next chunk copies, so only the last check follows the transfer
+  constexpr u64 kChunk = 16ull << 20;  // edges (128 MiB)
+  const u64 nch = (count + kChunk - 1) / kChunk;
+  while (c->chunk_ev.size() < nch) {
+    cudaEvent_t ev;
+    HCC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    c->chunk_ev.push_back(ev);
+  }
+  HCC_CUDA(cudaEventRecord(c->order_ev, c->copy_stream));
+  HCC_CUDA(cudaStreamWaitEvent(c->check_stream, c->order_ev, 0));
+  for (u64 k = 0; k < nch; ++k) {
+    const u64 b = first + k * kChunk, cnt = std::min<u64>(kChunk, count - k * kChunk);
+    HCC_CUDA(cudaMemcpyAsync(g->d_edges + b, uv + 2 * (b - first), cnt * sizeof(uint2),
+                             cudaMemcpyHostToDevice, c->copy_stream));
+    HCC_CUDA(cudaEventRecord(c->chunk_ev[k], c->copy_stream));
+    HCC_CUDA(cudaStreamWaitEvent(c->check_stream, c->chunk_ev[k], 0));
+    k_check_u32<<<grid_for(cnt, 256, 65536), 256, 0, c->check_stream>>>(g->d_edges + b, cnt,
+                                                                        g->n, g->d_err);
+    HCC_CUDA(cudaGetLastError());
+  }
+  HCC_CUDA(cudaMemcpyAsync(g->h_err, g->d_err, sizeof(u32), cudaMemcpyDeviceToHost,
+                           c->check_stream));
+  HCC_CUDA(cudaEventRecord(g->up_ev, c->check_stream));
+  g->pending = true;
+  g->has_stats = false;
+  return HCC_OK;
+  HCC_GUARD_END
+}
+
+int hcc_graph_assign_edges_u32(hcc_ctx* c, hcc_graph* g, const uint32_t* uv,
+                               uint64_t first, uint64_t count) {
+  // the chunked upload with overlapped endpoint checks, then wait for it
+  if (int r = hcc_graph_upload_async(c, g, uv, first, count)) return r;
+  return graph_ready(g);
+}
+
+int hcc_graph_from_csr(hcc_ctx* c, const uint64_t* row_ptr, const uint32_t* col,
+                       uint64_t n, hcc_graph** out) {
+  if (!out) return fail(HCC_EINVAL, "null output");
+  *out = nullptr;
+  if (int r = ctx_enter(c)) return r;
+  if (n > kMaxN) return fail(HCC_EINVAL, "vertex count >= 2^32");
+  if (!row_ptr) return fail(HCC_EINVAL, "null row_ptr");
+  if (row_ptr[0] != 0) return fail(HCC_EINVAL, "row_ptr[0] must be 0");
+  for (u64 i = 0; i < n; ++i)
+    if (row_ptr[i + 1] < row_ptr[i])
+      return fail(HCC_EINVAL, "row_ptr must be non-decreasing");
+  const u64 m = row_ptr[n];
+  if (m > 0 && !col) return fail(HCC_EINVAL, "null col");
+  if (!c->subs.empty()) {
+    // sharded: expand on the host (row order), then partition the edge list
+    std::vector<u32> uv;
+    try {
+      uv.resize(2 * m);
+    } catch (const std::bad_alloc&) {
+      return fail(HCC_ENOMEM, "host allocation failed");
+    }
+    for (u64 u = 0; u < n; ++u)
+      for (u64 j = row_ptr[u]; j < row_ptr[u + 1]; ++j) {
+        if (col[j] >= n) return fail(HCC_ERANGE, "column index out of range");
+        uv[2 * j] = (u32)u;
+        uv[2 * j + 1] = col[j];
+      }
+    return multi_from_edges(c, uv.data(), false, m, n, out);
+  }
+  hcc_graph* g = new hcc_graph;
+  g->ctx = c;
+  g->n = n;
+  g->m = m;
+  u64* d_rp = nullptr;
+  u32 *d_col = nullptr, *d_err = nullptr;
+  HCC_GUARD_BEGIN
+  HCC_CUDA(cudaMalloc(&g->d_edges, std::max<u64>(m, 2) * sizeof(uint2)));
+  HCC_CUDA(cudaMalloc(&d_err, sizeof(u32)));
+  HCC_CUDA(cudaMemsetAsync(d_err, 0, sizeof(u32), c->stream));
+  if (m > 0) {
+    HCC_CUDA(cudaMalloc(&d_rp, (n + 1) * sizeof(u64)));
+    HCC_CUDA(cudaMalloc(&d_col, m * sizeof(u32)));
+    HCC_CUDA(cudaMemcpyAsync(d_rp, row_ptr, (n + 1) * sizeof(u64),
+                             cudaMemcpyHostToDevice, c->stream));
+    HCC_CUDA(cudaMemcpyAsync(d_col, col, m * sizeof(u32),
+                             cudaMemcpyHostToDevice, c->stream));
+    k_csr_expand<<<grid_for(m, 256, 65536), 256, 0, c->stream>>>(
+        d_rp, d_col, n, g->d_edges, m, d_err);
+    HCC_CUDA(cudaGetLastError());
+  }
+  u32 err = 0;
+  HCC_CUDA(cudaMemcpyAsync(&err, d_err, sizeof(u32), cudaMemcpyDeviceToHost,
+                           c->stream));
+  HCC_CUDA(cudaStreamSynchronize(c->stream));
+  cudaFree(d_rp);
+  cudaFree(d_col);
+  cudaFree(d_err);
+  d_rp = nullptr;
+  d_col = nullptr;
+  d_err = nullptr;
+  if (err) {
+    hcc_graph_free(g);
+    return fail(HCC_ERANGE, "column index out of range");
+  }
+  *out = g;
+  return HCC_OK;
+  }
+  catch (const CudaFail& f) {
+    cudaFree(d_rp);
+    cudaFree(d_col);
+    cudaFree(d_err);
+    hcc_graph_free(g);
+    return f.code;
+  }
+}
+
+static int generate_impl(hcc_ctx* c, const char* spec_c, uint64_t default_seed,
+                         bool ranged, u64 first, u64 count, hcc_graph** out) {
+  if (!out || !spec_c) return fail(HCC_EINVAL, "null argument");
+  *out = nullptr;
+  if (int r = ctx_enter(c)) return r;
+  std::string spec(spec_c);
+  size_t colon = spec.find(':');
+  if (colon == std::string::npos)
+    return fail(HCC_EINVAL, "generator spec needs the form kind:params");
+  std::string kind = spec.substr(0, colon), params = spec.substr(colon + 1);
+  u64 n = 0, m = 0, rows = 0, cols = 0, seed = default_seed, scale = 0, ef = 0;
+  double a = 0.57, b = 0.19, cc = 0.19, d = 0.05;
+  std::string v;
+  if (kind == "grid") {
+    size_t x = params.find('x');
+    if (x == std::string::npos || !parse_u64(params.substr(0, x), &rows) ||
+        !parse_u64(params.substr(x + 1), &cols))
+      return fail(HCC_EINVAL, "grid spec needs RxC");
+    if (rows == 0 || cols == 0) return fail(HCC_EINVAL, "grid: zero vertices");
+    n = rows * cols;
+    m = rows * (cols - 1) + (rows - 1) * cols;
+  } else if (kind == "rmatx") {
+    if (!spec_get(params, "scale", &v) || !parse_u64(v, &scale) ||
+        !spec_get(params, "ef", &v) || !parse_u64(v, &ef))
+      return fail(HCC_EINVAL, "rmatx spec needs scale= and ef=");
+    if (scale > 32) return fail(HCC_EINVAL, "rmatx: scale > 32");
+    if (spec_get(params, "seed", &v) && !parse_u64(v, &seed))
+      return fail(HCC_EINVAL, "rmatx: bad seed");
+    if (spec_get(params, "a", &v)) a = atof(v.c_str());
+    if (spec_get(params, "b", &v)) b = atof(v.c_str());
+    if (spec_get(params, "c", &v)) cc = atof(v.c_str());
+    if (spec_get(params, "d", &v)) d = atof(v.c_str());
+    if (std::fabs(a + b + cc + d - 1.0) > 1e-9)
+      return fail(HCC_EINVAL, "rmat: quadrant probabilities must sum to 1");
+    n = 1ull << scale;
+    m = ef * n;
+  } else if (kind == "erx") {
+    if (!spec_get(params, "n", &v) || !parse_u64(v, &n) ||
+        !spec_get(params, "m", &v) || !parse_u64(v, &m))
+      return fail(HCC_EINVAL, "erx spec needs n= and m=");
+    if (spec_get(params, "seed", &v) && !parse_u64(v, &seed))
+      return fail(HCC_EINVAL, "erx: bad seed");
+    if (n == 0) return fail(HCC_EINVAL, "erdos_renyi: zero vertices");
+  } else {
+    return fail(HCC_EINVAL, "unknown device generator kind `" + kind + "`");
+  }
+  if (n > kMaxN + 1 || (kind != "rmatx" && n > kMaxN))
+    return fail(HCC_EINVAL, "vertex count >= 2^32");
+  if (kind == "rmatx" && n > kMaxN)
+    return fail(HCC_EINVAL, "rmatx: scale 32 needs 2^32 vertices (> u32)");
+  if (ranged) {
+    if (first > m || count > m - first)
+      return fail(HCC_EINVAL, "generator range out of bounds");
+  } else {
+    first = 0;
+    count = m;
+  }
+  if (!c->subs.empty()) return multi_generate(c, spec_c, default_seed, n, first, count, out);
+  hcc_graph* g = new hcc_graph;
+  g->ctx = c;
+  g->n = n;
+  g->m = count;
+  g->first = first;
+  HCC_GUARD_BEGIN
+  HCC_CUDA(cudaMalloc(&g->d_edges, std::max<u64>(count, 2) * sizeof(uint2)));
+  if (count > 0) {
+    unsigned grid = grid_for(count, 256, (u64)c->sms * 32);
+    if (kind == "grid") {
+      k_gen_grid<<<grid, 256, 0, c->stream>>>(g->d_edges, rows, cols, first, count);
+    } else if (kind == "rmatx") {
+      k_gen_rmatx<<<grid, 256, 0, c->stream>>>(
+          g->d_edges, first, count, (u32)scale, seed, prob_threshold(a),
+          prob_threshold(a + b), prob_threshold(a + b + cc));
+    } else {
+      k_gen_erx<<<grid, 256, 0, c->stream>>>(g->d_edges, first, count, n, seed);
+    }
+    HCC_CUDA(cudaGetLastError());
+  }
+  HCC_CUDA(cudaStreamSynchronize(c->stream));
+  *out = g;
+  return HCC_OK;
+  }
+  catch (const CudaFail& f) {
+    hcc_graph_free(g);
+    return f.code;
+  }
+}
+
+int hcc_graph_generate(hcc_ctx* c, const char* spec, uint64_t default_seed,
+                       hcc_graph** out) {
+  return generate_impl(c, spec, default_seed, false, 0, 0, out);
+}
+
+int hcc_graph_generate_range(hcc_ctx* c, const char* spec, uint64_t default_seed,
+                             uint64_t first, uint64_t count, hcc_graph** out) {
+  return generate_impl(c, spec, default_seed, true, first, count, out);
+}
+
+int hcc_graph_info(const hcc_graph* g, uint64_t* n, uint64_t* m) {
+  if (!g) return fail(HCC_EINVAL, "null graph");
+  if (n) *n = g->n;
+  if (m) *m = g->m;
+  return HCC_OK;
+}
+
+int hcc_graph_download_u32(hcc_ctx* c, const hcc_graph* g, uint32_t* uv,
+                           uint64_t first, uint64_t count) {
+  if (int r = graph_ready(g)) return r;
+  if (!g || (count && !uv)) return fail(HCC_EINVAL, "null argument");
+  if (first > g->m || count > g->m - first)
+    return fail(HCC_EINVAL, "range out of bounds");
+  if (int r = ctx_enter(c)) return r;
+  if (!g->shards.empty())
+    return multi_range_io(c, const_cast<hcc_graph*>(g), uv, first, count, 2);
+  HCC_GUARD_BEGIN
+  if (count)
+    HCC_CUDA(cudaMemcpy(uv, g->d_edges + first, count * sizeof(uint2),
+                        cudaMemcpyDeviceToHost));
+  return HCC_OK;
+  HCC_GUARD_END
+}
+
+int hcc_graph_checksum(hcc_ctx* c, const hcc_graph* g, uint64_t* out) {
+  if (int r = graph_ready(g)) return r;
+  if (!g || !out) return fail(HCC_EINVAL, "null argument");
+  if (int r = ctx_enter(c)) return r;
+  if (!g->shards.empty()) {  // position-keyed terms: the shard sums add up
+    u64 sum = 0;
+    for (size_t r = 0; r < g->shards.size(); ++r) {
+      uint64_t x = 0;
+      if (int e = hcc_graph_checksum(c->subs[r], g->shards[r], &x)) return e;
+      sum += x;
+    }
+    *out = sum;
+    return HCC_OK;
+  }
+  u64* d = nullptr;
+  HCC_GUARD_BEGIN
+  HCC_CUDA(cudaMalloc(&d, sizeof(u64)));
+  HCC_CUDA(cudaMemsetAsync(d, 0, sizeof(u64), c->stream));
+  if (g->m)
+    k_checksum<<<grid_for(g->m, 256, (u64)c->sms * 16), 256, 0, c->stream>>>(
+        g->d_edges, g->m, g->first, d);
+  HCC_CUDA(cudaGetLastError());
+  HCC_CUDA(cudaMemcpyAsync(out, d, sizeof(u64), cudaMemcpyDeviceToHost,
+                           c->stream));
+  HCC_CUDA(cudaStreamSynchronize(c->stream));
+  cudaFree(d);
+  return HCC_OK;
+  }
+  catch (const CudaFail& f) {
+    cudaFree(d);
+    return f.code;
+  }
+}
+
+int hcc_graph_compute_stats(hcc_ctx* c, const hcc_graph* g_c,
+                            hcc_graph_stats* out) {
+  if (int r = graph_ready(g_c)) return r;
+  if (!g_c || !out) return fail(HCC_EINVAL, "null argument");
+  if (int r = ctx_enter(c)) return r;
+  hcc_graph* g = const_cast<hcc_graph*>(g_c);
+  if (!g->shards.empty() && !g->has_stats) {
+    if (int r = multi_stats(c, g, &g->stats)) return r;
+    g->has_stats = true;
+  }
+  HCC_GUARD_BEGIN
+  if (!g->has_stats)
+    if (int r = compute_stats_dev(c, g)) return r;
+  *out = g->stats;
+  return HCC_OK;
+  HCC_GUARD_END
+}
+
+int hcc_graph_free(hcc_graph* g) {
+  if (!g) return HCC_OK;
+  if (!g->shards.empty()) {
+    for (hcc_graph* sh : g->shards) hcc_graph_free(sh);
+    delete g;
+    return HCC_OK;
+  }
+  if (g->ctx) {
+    cudaSetDevice(g->ctx->dev);
+    // the cached executable graph may reference these edges
+    if (g->ctx->key.edges == g->d_edges || g->ctx->alt_key.edges == g->d_edges)
+      drop_exec(g->ctx);
+    if (g->pending) cudaEventSynchronize(g->up_ev);
+  }
+  if (g->up_ev) cudaEventDestroy(g->up_ev);
+  cudaFree(g->d_err);
+  cudaFreeHost(g->h_err);
+  cudaFree(g->d_edges);
+  delete g;
+  return HCC_OK;
+}
+
+uint64_t hcc_choose_segment_count(const hcc_graph_stats* st) {
+  // engines.hpp:35-41
+  if (!st || st->n == 0) return 1;
+  u64 s = (u64)std::floor(st->avg_degree + 0.5);
+  if (s < 1) s = 1;
+  if (st->m_stored > 0 && s > st->m_stored) s = st->m_stored;
+  return s;
+}
+
+// ---- the CC engine -----------------------------------------------------------
+
 int hcc_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o, hcc_forest* f,
            uint32_t* labels_out, hcc_metrics* mx) {
   if (!g) return fail(HCC_EINVAL, "null graph");
@@ -2660,741 +2513,6 @@ int hcc_rehook_rows(hcc_ctx* c, hcc_forest* f, const uint32_t* dev_bit_rows, uin
   if (mx) *mx = out;
   return HCC_OK;
   HCC_GUARD_END
-}
-
-}  // extern "C"
-
-// ===========================================================================
-// Multi-device contexts: edge-partitioned CC in one process (north-star (5),
-// SURVEY.md §8e).  hcc_create_multi(devices, ndev) builds one sub-context
-// per shard (a device may appear several times: several shards share it).
-// Graphs created on such a context are split by partition_edges(m, ndev)
-// (engines.hpp:43-58), shard r on subs[r].  hcc_cc on it:
-//   1. local CC    every shard runs the single-GPU engine (its own stream,
-//                  one host thread per shard) into a full-size local forest,
-//                  then exports it (k_export: bitmap of pi(v) == 0 plus
-//                  sparse (v, pi(v)) pairs) into its merge buffers;
-//   2. merge       every shard waits on the others' export events (device
-//                  waits, cross-device) and runs k_merge_gather, which reads
-//                  the peers' export buffers straight over NVLink (P2P) and
-//                  appends the relations its own forest lacks to its
-//                  worklist; the worklist engine re-hooks them;
-//   3. labels      every shard now holds the global min-canonical forest;
-//                  shard 0's is returned.
-// A pair list that overflowed its buffer (the count is read on the device,
-// the host checks it after the round) grows the buffer and repeats steps
-// 1b-2: the relations already merged are true ones, so a repeat is exact.
-
-#include <condition_variable>
-#include <thread>
-
-namespace {
-
-// fn(r) on one host thread per shard; the first failure's message is moved
-// to the calling thread (g_err is thread-local).
-// HCC_MULTI_SERIAL=1 runs the shards one after another on one thread: on a
-// single GPU hosting every shard, each shard's phases then run alone, which
-// is the per-rank cost an N-GPU run would see (tools/scale_model.py).
-int for_shards(int G, const std::function<int(int)>& fn) {
-  std::vector<int> rc(G, 0);
-  std::vector<std::string> msg(G);
-  std::vector<std::thread> th;
-  th.reserve(G);
-  static const bool serial = std::getenv("HCC_MULTI_SERIAL") && std::atoi(std::getenv("HCC_MULTI_SERIAL"));
-  for (int r = 0; r < G; ++r) {
-    th.emplace_back([&, r] {
-      try {
-        rc[r] = fn(r);
-      } catch (const CudaFail& f) {
-        rc[r] = f.code;
-      } catch (const std::bad_alloc&) {
-        rc[r] = fail(HCC_ENOMEM, "host allocation failed");
-      } catch (const std::exception& e) {
-        rc[r] = fail(HCC_ECUDA, e.what());
-      }
-      if (rc[r]) msg[r] = g_err;
-    });
-    if (serial) th.back().join();
-  }
-  for (std::thread& t : th)
-    if (t.joinable()) t.join();
-  for (int r = 0; r < G; ++r)
-    if (rc[r]) {
-      g_err = msg[r];
-      return rc[r];
-    }
-  return HCC_OK;
-}
-
-// Merge buffers of every shard for n vertices and pair capacity >= cap.
-void ensure_merge(hcc_ctx* c, u64 n, u64 cap) {
-  const int G = (int)c->subs.size();
-  if ((int)c->merge.size() != G) c->merge.resize(G);
-  const u64 nwords = (n + 31) / 32;
-  bool dirty = false;
-  for (int r = 0; r < G; ++r) {
-    MergeShard& ms = c->merge[r];
-    hcc_ctx* sc = c->subs[r];
-    HCC_CUDA(cudaSetDevice(sc->dev));
-    if (!ms.cnt) {
-      HCC_CUDA(cudaMalloc(&ms.cnt, sizeof(u64)));
-      HCC_CUDA(cudaMalloc(&ms.tab, sizeof(PeerTab)));
-      HCC_CUDA(cudaEventCreateWithFlags(&ms.ev_exp, cudaEventDisableTiming));
-      HCC_CUDA(cudaEventCreate(&ms.ev_t0));
-      HCC_CUDA(cudaEventCreate(&ms.ev_m0));
-      HCC_CUDA(cudaEventCreate(&ms.ev_t1));
-      dirty = true;
-    }
-    if (ms.bits_words < nwords) {
-      cudaFree(ms.bits);
-      ms.bits = nullptr;
-      HCC_CUDA(cudaMalloc(&ms.bits, std::max<u64>(nwords, 1) * sizeof(u32)));
-      ms.bits_words = nwords;
-      dirty = true;
-    }
-    if (ms.cap < cap) {
-      cudaFree(ms.pairs);
-      ms.pairs = nullptr;
-      ms.cap = 0;
-      HCC_CUDA(cudaMalloc(&ms.pairs, cap * sizeof(uint2)));
-      ms.cap = cap;
-      dirty = true;
-    }
-  }
-  if (!dirty) return;
-  PeerTab t{};
-  t.npeers = (u32)G;
-  for (int r = 0; r < G; ++r) {
-    t.bits[r] = c->merge[r].bits;
-    t.pairs[r] = c->merge[r].pairs;
-    t.count[r] = c->merge[r].cnt;
-    t.cap[r] = c->merge[r].cap;
-  }
-  for (int r = 0; r < G; ++r) {
-    HCC_CUDA(cudaSetDevice(c->subs[r]->dev));
-    HCC_CUDA(cudaMemcpy(c->merge[r].tab, &t, sizeof(PeerTab), cudaMemcpyHostToDevice));
-  }
-  HCC_CUDA(cudaSetDevice(c->dev));
-}
-
-// Shard r: export its forest into its merge buffers (stream-ordered after
-// its local CC) and record the export event the peers wait on.
-void enqueue_export(hcc_ctx* sc, MergeShard& ms, const hcc_forest* f) {
-  HCC_CUDA(cudaMemsetAsync(ms.cnt, 0, sizeof(u64), sc->stream));
-  const u64 nwords = (f->n + 31) / 32;
-  if (f->n)
-    k_export<<<grid_for(nwords * 32, 256, (u64)sc->sms * 32), 256, 0, sc->stream>>>(
-        f->d_pi, f->n, ms.bits, ms.pairs, ms.cap, ms.cnt);
-  HCC_CUDA(cudaGetLastError());
-  HCC_CUDA(cudaEventRecord(ms.ev_exp, sc->stream));
-}
-
-// Shard r: wait for every peer's export, gather the remote relations over
-// NVLink into the worklist, re-hook until convergence.
-void merge_shard(hcc_ctx* c, int r, hcc_forest* f, u64 records_cap) {
-  hcc_ctx* sc = c->subs[r];
-  MergeShard& ms = c->merge[r];
-  const int G = (int)c->subs.size();
-  const u64 n = f->n;
-  for (int s = 0; s < G; ++s)
-    if (s != r) HCC_CUDA(cudaStreamWaitEvent(sc->stream, c->merge[s].ev_exp, 0));
-  ensure_wl(sc, records_cap);
-  const Plan P = rehook_plan(sc, f->d_pi, n);
-  HCC_CUDA(cudaEventRecord(ms.ev_m0, sc->stream));
-  k_begin<<<1, 1, 0, sc->stream>>>(sc->d_ctrl, sc->d_recs, 1);
-  k_merge_gather<<<std::max<unsigned>(1u, (unsigned)sc->sms * 8u), 256, 0, sc->stream>>>(
-      ms.tab, (u32)r, f->d_pi, n, sc->wl[0], &sc->d_ctrl->wl_count[0], sc->wl_cap,
-      &sc->d_ctrl->err, &sc->d_ctrl->dirty, &sc->d_ctrl->merged_links);
-  HCC_CUDA(cudaGetLastError());
-  rehook_loop(sc, P);
-  HCC_CUDA(cudaEventRecord(ms.ev_t1, sc->stream));
-  // components (metrics only, after the timed region)
-  if (r == 0)
-    k_count_roots<<<grid_for(n, 256, (u64)sc->sms * 16), 256, 0, sc->stream>>>(f->d_pi, n,
-                                                                              sc->d_ctrl);
-  HCC_CUDA(cudaGetLastError());
-  HCC_CUDA(cudaMemcpyAsync(sc->h_ctrl, sc->d_ctrl, sizeof(DevCtrl), cudaMemcpyDeviceToHost,
-                           sc->stream));
-  HCC_CUDA(cudaMemcpyAsync(sc->h_recs, sc->d_recs, sizeof(DevRec), cudaMemcpyDeviceToHost,
-                           sc->stream));
-  HCC_CUDA(cudaStreamSynchronize(sc->stream));
-  if (sc->h_ctrl->err & 4u) throw CudaFail{fail(HCC_ECUDA, "merge worklist overflow")};
-  float ms_merge = 0.f, ms_total = 0.f;
-  HCC_CUDA(cudaEventElapsedTime(&ms_merge, ms.ev_m0, ms.ev_t1));
-  HCC_CUDA(cudaEventElapsedTime(&ms_total, ms.ev_t0, ms.ev_t1));
-  ms.merge_ms += ms_merge;
-  ms.total_ms = ms_total;
-  ms.passes += sc->h_ctrl->passes;
-  ms.records += sc->h_recs[0].edges_in;
-  ms.linked += sc->h_ctrl->merged_links;
-}
-
-}  // namespace
-
-static int multi_from_edges(hcc_ctx* c, const void* uv, bool wide, u64 m, u64 n,
-                            hcc_graph** out) {
-  const int G = (int)c->subs.size();
-  hcc_graph* g = new hcc_graph;
-  g->ctx = c;
-  g->n = n;
-  g->m = m;
-  g->bounds = uniform_bounds(m, (u64)G);
-  g->shards.assign(G, nullptr);
-  const int rc = for_shards(G, [&](int r) -> int {
-    const u64 b = g->bounds[r], k = g->bounds[r + 1] - b;
-    const int st = wide ? hcc_graph_from_edges_u64(c->subs[r], static_cast<const uint64_t*>(uv) + 2 * b,
-                                                   k, n, &g->shards[r])
-                        : hcc_graph_from_edges_u32(c->subs[r], static_cast<const uint32_t*>(uv) + 2 * b,
-                                                   k, n, &g->shards[r]);
-    if (!st) g->shards[r]->first = b;
-    return st;
-  });
-  if (rc) {
-    for (hcc_graph*& sh : g->shards)
-      if (!sh) sh = new hcc_graph;  // placeholders so free() sees a sharded graph
-    hcc_graph_free(g);
-    return rc;
-  }
-  *out = g;
-  return HCC_OK;
-}
-
-static int multi_generate(hcc_ctx* c, const char* spec, u64 seed, u64 n, u64 first, u64 count,
-                          hcc_graph** out) {
-  const int G = (int)c->subs.size();
-  hcc_graph* g = new hcc_graph;
-  g->ctx = c;
-  g->n = n;
-  g->m = count;
-  g->first = first;
-  g->bounds = uniform_bounds(count, (u64)G);
-  g->shards.assign(G, nullptr);
-  const int rc = for_shards(G, [&](int r) -> int {
-    const u64 b = g->bounds[r], k = g->bounds[r + 1] - b;
-    return hcc_graph_generate_range(c->subs[r], spec, seed, first + b, k, &g->shards[r]);
-  });
-  if (rc) {
-    for (hcc_graph*& sh : g->shards)
-      if (!sh) sh = new hcc_graph;
-    hcc_graph_free(g);
-    return rc;
-  }
-  *out = g;
-  return HCC_OK;
-}
-
-// op 0: asynchronous upload, 1: synchronous assign, 2: download.  The range
-// [first, first+count) is split at the shard boundaries.
-static int multi_range_io(hcc_ctx* c, hcc_graph* g, uint32_t* uv, u64 first, u64 count, int op) {
-  for (size_t r = 0; r < g->shards.size(); ++r) {
-    const u64 b = std::max(first, g->bounds[r]);
-    const u64 e = std::min(first + count, g->bounds[r + 1]);
-    if (b >= e) continue;
-    uint32_t* src = uv + 2 * (b - first);
-    const u64 lo = b - g->bounds[r];
-    int st;
-    if (op == 2)
-      st = hcc_graph_download_u32(c->subs[r], g->shards[r], src, lo, e - b);
-    else
-      st = hcc_graph_upload_async(c->subs[r], g->shards[r], src, lo, e - b);
-    if (st) return st;
-  }
-  g->has_stats = false;
-  if (op == 1) return graph_ready(g);
-  return HCC_OK;
-}
-
-// compute_stats of a sharded graph: the shards are copied (peer copies)
-// into one temporary graph on the first device.  Off the hot path.
-static int multi_stats(hcc_ctx* c, const hcc_graph* g, hcc_graph_stats* out) {
-  if (int r = graph_ready(g)) return r;
-  hcc_graph tmp;
-  tmp.ctx = c;
-  tmp.n = g->n;
-  tmp.m = g->m;
-  int rc = HCC_OK;
-  try {
-    HCC_CUDA(cudaSetDevice(c->dev));
-    HCC_CUDA(cudaMalloc(&tmp.d_edges, std::max<u64>(g->m, 2) * sizeof(uint2)));
-    for (size_t r = 0; r < g->shards.size(); ++r)
-      if (g->shards[r]->m)
-        HCC_CUDA(cudaMemcpyPeer(tmp.d_edges + g->bounds[r], c->dev, g->shards[r]->d_edges,
-                                c->subs[r]->dev, g->shards[r]->m * sizeof(uint2)));
-    rc = compute_stats_dev(c, &tmp);
-    if (!rc) *out = tmp.stats;
-  } catch (const CudaFail& f) {
-    rc = f.code;
-  }
-  cudaFree(tmp.d_edges);
-  tmp.d_edges = nullptr;
-  return rc;
-}
-
-static int multi_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o_in, hcc_forest* f,
-                    uint32_t* lab32, uint64_t* lab64, hcc_metrics* mx) {
-  const int G = (int)c->subs.size();
-  if ((int)g->shards.size() != G || g->ctx != c)
-    return fail(HCC_EINVAL, "graph was not created on this multi-device context");
-  if (int r = graph_ready(g)) return r;
-  hcc_opts o = {HCC_ALGO_BASELINE_MJ, 0, 0, 0, 0, nullptr, nullptr};
-  if (o_in) o = *o_in;
-  if (o.algo < HCC_ALGO_BASELINE || o.algo > HCC_ALGO_ADAPTIVE)
-    return fail(HCC_EINVAL, "unknown algorithm");
-  if (o.observer)
-    return fail(HCC_EINVAL, "phase observers need a single-device context");
-  const u64 n = g->n;
-  if (f && f->n != n) return fail(HCC_EINVAL, "forest size does not match the graph");
-  if (f && f->dev != c->subs[0]->dev)
-    return fail(HCC_EINVAL, "the forest must live on the first device of the context");
-  hcc_metrics out{};
-  out.n = n;
-  out.m = g->m;
-  if (o.algo == HCC_ALGO_ADAPTIVE && o.segments == 0) {
-    // s from the WHOLE graph's stats (engines.hpp:245-247), not per shard
-    hcc_graph_stats st;
-    if (int r = hcc_graph_compute_stats(c, g, &st)) return r;
-    o.segments = hcc_choose_segment_count(&st);
-  }
-  if (n == 0) {
-    if (mx) *mx = out;
-    return HCC_OK;
-  }
-  u64 cap = 0;
-  try {
-    cap = c->merge.empty() ? 0 : c->merge[0].cap;
-    if (cap == 0) cap = std::max<u64>(1ull << 16, n / 64);
-    ensure_merge(c, n, cap);
-    for (int r = 0; r < G; ++r) {
-      MergeShard& ms = c->merge[r];
-      if (!(r == 0 && f) && (!ms.forest || ms.forest->n != n)) {
-        if (ms.forest) hcc_forest_free(ms.forest);
-        ms.forest = nullptr;
-        if (int st = hcc_forest_create(c->subs[r], n, &ms.forest)) return st;
-      }
-      ms.local_ms = ms.merge_ms = ms.total_ms = 0;
-      ms.passes = ms.records = ms.exported = ms.linked = 0;
-    }
-  } catch (const CudaFail& fl) {
-    return fl.code;
-  }
-  auto forest_of = [&](int r) { return (r == 0 && f) ? f : c->merge[r].forest; };
-  std::vector<hcc_metrics> lm(G);
-  // 1. local CC + export
-  int rc = for_shards(G, [&](int r) -> int {
-    hcc_ctx* sc = c->subs[r];
-    MergeShard& ms = c->merge[r];
-    HCC_CUDA(cudaSetDevice(sc->dev));
-    HCC_CUDA(cudaEventRecord(ms.ev_t0, sc->stream));
-    if (int st = run_cc_sized(sc, g->shards[r], &o, forest_of(r), &lm[r])) return st;
-    ms.local_ms = lm[r].total_ms;
-    enqueue_export(sc, ms, forest_of(r));
-    return HCC_OK;
-  });
-  // 2. merge; repeated (export + merge) while some pair list overflowed
-  for (int attempt = 0; !rc; ++attempt) {
-    u64 pairs_total = 0;
-    for (int r = 0; r < G; ++r) pairs_total += c->merge[r].cap;
-    rc = for_shards(G, [&](int r) -> int {
-      HCC_CUDA(cudaSetDevice(c->subs[r]->dev));
-      merge_shard(c, r, forest_of(r), n + pairs_total + 1);
-      return HCC_OK;
-    });
-    if (rc) break;
-    u64 need = 0, total = 0;
-    try {
-      for (int r = 0; r < G; ++r) {
-        HCC_CUDA(cudaSetDevice(c->subs[r]->dev));
-        u64 k = 0;
-        HCC_CUDA(cudaMemcpy(&k, c->merge[r].cnt, sizeof(u64), cudaMemcpyDeviceToHost));
-        c->merge[r].exported = k;
-        need = std::max(need, k);
-        total += k;
-      }
-      if (need <= c->merge[0].cap) break;
-      if (attempt >= 3) {
-        rc = fail(HCC_ECUDA, "merge pair buffers kept overflowing");
-        break;
-      }
-      // the repeat exports forests that already absorbed part of the remote
-      // relations: a rank's new list is bounded by the union of all lists
-      // (usually; the third repeat takes n, which always suffices)
-      ensure_merge(c, n, attempt >= 2 ? std::max<u64>(n, 1)
-                                      : std::min<u64>(std::max<u64>(n, 1), total + total / 8 + 1));
-    } catch (const CudaFail& fl) {
-      rc = fl.code;
-      break;
-    }
-    rc = for_shards(G, [&](int r) -> int {
-      HCC_CUDA(cudaSetDevice(c->subs[r]->dev));
-      HCC_CUDA(cudaEventRecord(c->merge[r].ev_t0, c->subs[r]->stream));
-      enqueue_export(c->subs[r], c->merge[r], forest_of(r));
-      return HCC_OK;
-    });
-  }
-  cudaSetDevice(c->dev);
-  if (rc) return rc;
-  // metrics: device time of the slowest shard (max over shards)
-  for (int r = 0; r < G; ++r) {
-    const hcc_metrics& l = lm[r];
-    const MergeShard& ms = c->merge[r];
-    out.total_ms = std::max(out.total_ms, ms.local_ms + ms.merge_ms);
-    out.hook_ms = std::max(out.hook_ms, l.hook_ms);
-    out.compress_ms = std::max(out.compress_ms, l.compress_ms);
-    out.outer_iterations = std::max(out.outer_iterations, l.outer_iterations);
-    out.counters.hook_traversal_steps += l.counters.hook_traversal_steps;
-    out.counters.cas_failures += l.counters.cas_failures;
-    out.counters.jump_steps += l.counters.jump_steps;
-    out.passes += l.passes + ms.passes;
-    out.edges_processed += l.edges_processed + ms.records;
-    out.kernels += l.kernels + 3 + 3 * ms.passes;
-    out.wl_reruns |= l.wl_reruns;
-  }
-  out.s = lm[0].s;
-  out.segments_clamped = lm[0].segments_clamped;
-  out.used_device_loop = lm[0].used_device_loop;
-  out.star0_bitmap = lm[0].star0_bitmap;
-  out.wl_capacity = lm[0].wl_capacity;
-  out.components = c->subs[0]->h_ctrl->components;
-  out.records = G;
-  if (mx) *mx = out;
-  if (lab32 || lab64) {
-    const hcc_forest* f0 = forest_of(0);
-    HCC_GUARD_BEGIN
-    HCC_CUDA(cudaSetDevice(c->subs[0]->dev));
-    if (lab32) {
-      HCC_CUDA(cudaMemcpy(lab32, f0->d_pi, n * sizeof(u32), cudaMemcpyDeviceToHost));
-    } else {
-      uint32_t* tmp = reinterpret_cast<uint32_t*>(lab64) + n;
-      HCC_CUDA(cudaMemcpy(tmp, f0->d_pi, n * sizeof(u32), cudaMemcpyDeviceToHost));
-      for (u64 i = 0; i < n; ++i) lab64[i] = tmp[i];
-    }
-    HCC_CUDA(cudaSetDevice(c->dev));
-    return HCC_OK;
-    HCC_GUARD_END
-  }
-  return HCC_OK;
-}
-
-extern "C" {
-
-int hcc_create_multi(const int* devices, int ndev, hcc_ctx** out) {
-  if (!out || !devices) return fail(HCC_EINVAL, "null argument");
-  *out = nullptr;
-  if (ndev < 1 || ndev > (int)kMaxShards)
-    return fail(HCC_EINVAL, "shard count must be in [1, 64]");
-  hcc_ctx* c = nullptr;
-  if (int r = hcc_create(devices[0], &c)) return r;
-  for (int i = 0; i < ndev; ++i) {
-    hcc_ctx* sc = nullptr;
-    if (int r = hcc_create(devices[i], &sc)) {
-      hcc_destroy(c);
-      return r;
-    }
-    c->subs.push_back(sc);
-  }
-  // P2P between every pair of distinct devices: the merge kernel reads the
-  // peers' export buffers in place over NVLink
-  c->peer_access = 1;
-  for (int i = 0; i < ndev; ++i)
-    for (int j = 0; j < ndev; ++j) {
-      const int a = devices[i], b = devices[j];
-      if (a == b) continue;
-      int can = 0;
-      if (cudaDeviceCanAccessPeer(&can, a, b) != cudaSuccess || !can) {
-        cudaGetLastError();
-        hcc_destroy(c);
-        return fail(HCC_ENCCL, "no peer access from device " + std::to_string(a) + " to " +
-                                   std::to_string(b) + " (the merge reads peer memory)");
-      }
-      cudaSetDevice(a);
-      const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
-      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
-        cudaGetLastError();
-        hcc_destroy(c);
-        return fail(HCC_ENCCL, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
-      }
-      cudaGetLastError();
-    }
-  cudaSetDevice(devices[0]);
-  *out = c;
-  return HCC_OK;
-}
-
-int hcc_ctx_shards(hcc_ctx* c, int* count) {
-  if (!c || !count) return fail(HCC_EINVAL, "null argument");
-  *count = c->subs.empty() ? 1 : (int)c->subs.size();
-  return HCC_OK;
-}
-
-int hcc_ctx_shard_metrics(hcc_ctx* c, hcc_shard_metrics* out, uint64_t cap, uint64_t* count) {
-  if (!c) return fail(HCC_EINVAL, "null context");
-  const u64 G = c->merge.size();
-  if (count) *count = G;
-  for (u64 r = 0; r < std::min<u64>(cap, G); ++r) {
-    const MergeShard& ms = c->merge[r];
-    hcc_shard_metrics x{};
-    x.total_ms = ms.local_ms + ms.merge_ms;
-    x.local_ms = ms.local_ms;
-    x.merge_ms = ms.merge_ms;
-    x.span_ms = ms.total_ms;
-    x.pairs_exported = ms.exported;
-    x.records_merged = ms.records;
-    x.rehook_passes = ms.passes;
-    x.bitmap_bytes = ms.bits_words * 4;
-    x.roots_linked = ms.linked;
-    x.device = c->subs[r]->dev;
-    x.peer_access = c->peer_access;
-    out[r] = x;
-  }
-  return HCC_OK;
-}
-
-}  // extern "C"
-
-// ===========================================================================
-// Multi-process merge over CUDA IPC (one process per GPU, e.g. torchrun;
-// paper_1612_01178_b200/distributed.py).  Each rank allocates its export
-// buffers in one arena and an interprocess event, and publishes both as a
-// handle blob; after the blobs are exchanged (any transport: the Python
-// binding all-gathers them over torch.distributed once), every rank maps its
-// peers' arenas (cudaIpcOpenMemHandle, lazy peer access) and the same
-// k_merge_gather kernel reads them in place over NVLink.  Per run: local CC,
-// hcc_peer_export (k_export + event record), a host barrier (so every
-// record precedes every wait), hcc_peer_merge (device waits on the peers'
-// events, gather, re-hook).
-
-struct PeerBlob {
-  cudaIpcMemHandle_t mem;
-  cudaIpcEventHandle_t ev;
-  u64 bits_off, pairs_off, cap, nwords, n;
-  int32_t rank, world, dev, pad_;
-};
-static_assert(sizeof(PeerBlob) <= HCC_PEER_HANDLE_BYTES, "peer handle blob too large");
-
-struct hcc_peer_state {
-  int rank = 0, world = 1;
-  u64 n = 0, cap = 0, nwords = 0;
-  char* arena = nullptr;
-  u64* cnt = nullptr;
-  u32* bits = nullptr;
-  uint2* pairs = nullptr;
-  cudaEvent_t ev = nullptr;                 // this rank's export event
-  std::vector<char*> mapped;                // peers' arenas (nullptr = self)
-  std::vector<cudaEvent_t> peer_ev;         // peers' export events
-  std::vector<PeerBlob> blobs;
-  PeerTab* d_tab = nullptr;
-  cudaEvent_t ev_m0 = nullptr, ev_m1 = nullptr;
-  bool connected = false;
-};
-
-static void peer_release(hcc_ctx* c) {
-  hcc_peer_state* p = c->peer;
-  if (!p) return;
-  cudaSetDevice(c->dev);
-  cudaStreamSynchronize(c->stream);
-  for (char* a : p->mapped)
-    if (a) cudaIpcCloseMemHandle(a);
-  for (size_t r = 0; r < p->peer_ev.size(); ++r)
-    if (p->peer_ev[r]) cudaEventDestroy(p->peer_ev[r]);
-  if (p->ev) cudaEventDestroy(p->ev);
-  if (p->ev_m0) cudaEventDestroy(p->ev_m0);
-  if (p->ev_m1) cudaEventDestroy(p->ev_m1);
-  cudaFree(p->arena);
-  cudaFree(p->d_tab);
-  cudaGetLastError();
-  delete p;
-  c->peer = nullptr;
-}
-
-extern "C" {
-
-int hcc_peer_open(hcc_ctx* c, uint64_t n, uint64_t cap, int rank, int world, void* handle_out) {
-  if (!handle_out || world < 1 || rank < 0 || rank >= world || world > (int)kMaxShards)
-    return fail(HCC_EINVAL, "bad peer arguments (rank/world/handle)");
-  if (n > kMaxN) return fail(HCC_EINVAL, "vertex count >= 2^32");
-  if (int r = ctx_enter(c)) return r;
-  if (!c->subs.empty()) return fail(HCC_EINVAL, "peer merge needs a single-device context");
-  peer_release(c);
-  hcc_peer_state* p = new hcc_peer_state;
-  c->peer = p;
-  HCC_GUARD_BEGIN
-  p->rank = rank;
-  p->world = world;
-  p->n = n;
-  p->cap = std::max<u64>(cap, 1);
-  p->nwords = (n + 31) / 32;
-  const u64 bits_off = 256, pairs_off = (bits_off + p->nwords * 4 + 255) & ~255ull;
-  HCC_CUDA(cudaMalloc(&p->arena, pairs_off + p->cap * sizeof(uint2)));
-  p->cnt = reinterpret_cast<u64*>(p->arena);
-  p->bits = reinterpret_cast<u32*>(p->arena + bits_off);
-  p->pairs = reinterpret_cast<uint2*>(p->arena + pairs_off);
-  HCC_CUDA(cudaMemset(p->cnt, 0, sizeof(u64)));
-  HCC_CUDA(cudaEventCreateWithFlags(&p->ev, cudaEventDisableTiming | cudaEventInterprocess));
-  HCC_CUDA(cudaEventCreate(&p->ev_m0));
-  HCC_CUDA(cudaEventCreate(&p->ev_m1));
-  HCC_CUDA(cudaMalloc(&p->d_tab, sizeof(PeerTab)));
-  PeerBlob b{};
-  HCC_CUDA(cudaIpcGetMemHandle(&b.mem, p->arena));
-  HCC_CUDA(cudaIpcGetEventHandle(&b.ev, p->ev));
-  b.bits_off = bits_off;
-  b.pairs_off = pairs_off;
-  b.cap = p->cap;
-  b.nwords = p->nwords;
-  b.n = n;
-  b.rank = rank;
-  b.world = world;
-  b.dev = c->dev;
-  std::memset(handle_out, 0, HCC_PEER_HANDLE_BYTES);
-  std::memcpy(handle_out, &b, sizeof(b));
-  return HCC_OK;
-  }
-  catch (const CudaFail& f) {
-    peer_release(c);
-    return f.code;
-  }
-}
-
-int hcc_peer_connect(hcc_ctx* c, const void* handles) {
-  if (!handles) return fail(HCC_EINVAL, "null handles");
-  if (int r = ctx_enter(c)) return r;
-  hcc_peer_state* p = c->peer;
-  if (!p) return fail(HCC_EINVAL, "hcc_peer_open first");
-  const int W = p->world;
-  p->blobs.resize(W);
-  for (int r = 0; r < W; ++r) {
-    std::memcpy(&p->blobs[r], static_cast<const char*>(handles) + (size_t)r * HCC_PEER_HANDLE_BYTES,
-                sizeof(PeerBlob));
-    const PeerBlob& b = p->blobs[r];
-    if (b.rank != r || b.world != W || b.n != p->n)
-      return fail(HCC_EINVAL, "peer handles disagree (rank order, world or n)");
-  }
-  HCC_GUARD_BEGIN
-  p->mapped.assign(W, nullptr);
-  p->peer_ev.assign(W, nullptr);
-  PeerTab t{};
-  t.npeers = (u32)W;
-  for (int r = 0; r < W; ++r) {
-    const PeerBlob& b = p->blobs[r];
-    char* base = p->arena;
-    if (r != p->rank) {
-      void* m = nullptr;
-      const cudaError_t e = cudaIpcOpenMemHandle(&m, b.mem, cudaIpcMemLazyEnablePeerAccess);
-      if (e != cudaSuccess) {
-        cudaGetLastError();
-        return fail(HCC_ENCCL, std::string("cudaIpcOpenMemHandle (rank ") + std::to_string(r) +
-                                   "): " + cudaGetErrorString(e));
-      }
-      p->mapped[r] = base = static_cast<char*>(m);
-      HCC_CUDA(cudaIpcOpenEventHandle(&p->peer_ev[r], b.ev));
-    }
-    t.bits[r] = reinterpret_cast<const u32*>(base + b.bits_off);
-    t.pairs[r] = reinterpret_cast<const uint2*>(base + b.pairs_off);
-    t.count[r] = reinterpret_cast<const u64*>(base);
-    t.cap[r] = b.cap;
-  }
-  HCC_CUDA(cudaMemcpy(p->d_tab, &t, sizeof(PeerTab), cudaMemcpyHostToDevice));
-  p->connected = true;
-  return HCC_OK;
-  HCC_GUARD_END
-}
-
-int hcc_peer_export(hcc_ctx* c, hcc_forest* f) {
-  if (!f) return fail(HCC_EINVAL, "null forest");
-  if (int r = ctx_enter(c)) return r;
-  hcc_peer_state* p = c->peer;
-  if (!p || !p->connected) return fail(HCC_EINVAL, "peer merge not connected");
-  if (f->n != p->n || f->dev != c->dev) return fail(HCC_EINVAL, "forest does not match the peer setup");
-  HCC_GUARD_BEGIN
-  HCC_CUDA(cudaEventRecord(p->ev_m0, c->stream));
-  HCC_CUDA(cudaMemsetAsync(p->cnt, 0, sizeof(u64), c->stream));
-  if (f->n)
-    k_export<<<grid_for(p->nwords * 32, 256, (u64)c->sms * 32), 256, 0, c->stream>>>(
-        f->d_pi, f->n, p->bits, p->pairs, p->cap, p->cnt);
-  HCC_CUDA(cudaGetLastError());
-  HCC_CUDA(cudaEventRecord(p->ev, c->stream));
-  return HCC_OK;
-  HCC_GUARD_END
-}
-
-int hcc_peer_merge(hcc_ctx* c, hcc_forest* f, hcc_metrics* mx, int* overflow) {
-  if (!f || !overflow) return fail(HCC_EINVAL, "null argument");
-  if (int r = ctx_enter(c)) return r;
-  hcc_peer_state* p = c->peer;
-  if (!p || !p->connected) return fail(HCC_EINVAL, "peer merge not connected");
-  if (f->n != p->n || f->dev != c->dev) return fail(HCC_EINVAL, "forest does not match the peer setup");
-  hcc_metrics out{};
-  out.n = f->n;
-  HCC_GUARD_BEGIN
-  const u64 n = f->n;
-  for (int r = 0; r < p->world; ++r)
-    if (r != p->rank) HCC_CUDA(cudaStreamWaitEvent(c->stream, p->peer_ev[r], 0));
-  u64 pairs_total = 0;
-  for (const PeerBlob& b : p->blobs) pairs_total += b.cap;
-  ensure_wl(c, n + pairs_total + 1);
-  const Plan P = rehook_plan(c, f->d_pi, n);
-  k_begin<<<1, 1, 0, c->stream>>>(c->d_ctrl, c->d_recs, 1);
-  k_merge_gather<<<std::max<unsigned>(1u, (unsigned)c->sms * 8u), 256, 0, c->stream>>>(
-      p->d_tab, (u32)p->rank, f->d_pi, n, c->wl[0], &c->d_ctrl->wl_count[0], c->wl_cap,
-      &c->d_ctrl->err, &c->d_ctrl->dirty, &c->d_ctrl->merged_links);
-  HCC_CUDA(cudaGetLastError());
-  rehook_loop(c, P);
-  HCC_CUDA(cudaEventRecord(p->ev_m1, c->stream));
-  // components (metrics only, after the timed region)
-  k_count_roots<<<grid_for(n, 256, (u64)c->sms * 16), 256, 0, c->stream>>>(f->d_pi, n,
-                                                                         c->d_ctrl);
-  HCC_CUDA(cudaGetLastError());
-  HCC_CUDA(cudaMemcpyAsync(c->h_ctrl, c->d_ctrl, sizeof(DevCtrl), cudaMemcpyDeviceToHost,
-                           c->stream));
-  HCC_CUDA(cudaMemcpyAsync(c->h_recs, c->d_recs, sizeof(DevRec), cudaMemcpyDeviceToHost,
-                           c->stream));
-  HCC_CUDA(cudaStreamSynchronize(c->stream));
-  // the peers' pair counts (read from their arenas, after the waits)
-  int ovf = 0;
-  for (int r = 0; r < p->world; ++r) {
-    u64 k = 0;
-    const char* base = r == p->rank ? p->arena : p->mapped[r];
-    HCC_CUDA(cudaMemcpy(&k, base, sizeof(u64), cudaMemcpyDeviceToHost));
-    if (k > p->blobs[r].cap) ovf = 1;
-    if (r == p->rank) out.m = k;  // pairs this rank exported
-  }
-  *overflow = ovf;
-  if (c->h_ctrl->err & 4u) return fail(HCC_ECUDA, "merge worklist overflow");
-  float ms = 0.f;
-  HCC_CUDA(cudaEventElapsedTime(&ms, p->ev_m0, p->ev_m1));
-  out.total_ms = ms;  // export through re-hook, incl. waiting for the peers
-  out.passes = c->h_ctrl->passes;
-  out.outer_iterations = c->h_ctrl->passes;
-  out.edges_processed = c->h_recs[0].edges_in;  // remote relations re-hooked
-  out.components = c->h_ctrl->components;
-  out.kernels = 4 + 3 * c->h_ctrl->passes;
-  if (mx) *mx = out;
-  return HCC_OK;
-  HCC_GUARD_END
-}
-
-int hcc_peer_disconnect(hcc_ctx* c) {
-  if (!c) return fail(HCC_EINVAL, "null context");
-  hcc_peer_state* p = c->peer;
-  if (!p) return HCC_OK;
-  cudaSetDevice(c->dev);
-  cudaStreamSynchronize(c->stream);
-  for (char*& a : p->mapped) {
-    if (a) cudaIpcCloseMemHandle(a);
-    a = nullptr;
-  }
-  for (cudaEvent_t& ev : p->peer_ev) {
-    if (ev) cudaEventDestroy(ev);
-    ev = nullptr;
-  }
-  cudaGetLastError();
-  p->connected = false;
-  return HCC_OK;
-}
-
-int hcc_peer_close(hcc_ctx* c) {
-  if (!c) return fail(HCC_EINVAL, "null context");
-  peer_release(c);
-  return HCC_OK;
 }
 
 }  // extern "C"
