@@ -94,7 +94,7 @@ def main() -> None:
     # the streaming topology hook's launches (k_hook / k_hook_sum that did
     # work: a gated-out launch exits in a few microseconds), as the bench's
     # roofline: k_hook_small (slot 0) and the worklist kernels are others
-    hooks = [e for e in rs if e["kernel"].split("::")[-1] in ("k_hook", "k_hook_sum")
+    hooks = [e for e in rs if e["kernel"].split("::")[-1] in ("k_hook", "k_hook_sum", "k_hook_sumd")
              and e[KEYS[0]] > 20e-6]
     topo = hooks
     traffic = [e[KEYS[1]] + e[KEYS[2]] for e in topo]
