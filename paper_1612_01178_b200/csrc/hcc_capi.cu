@@ -318,7 +318,6 @@ struct Plan {
   // after the first, measured slower).
   int sumd = 1;
   bool sum_vote = false;
-  bool sum_prefix = false;     // truncated prefix summary (HCC_S0F_PREFIX)
 };
 
 HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
@@ -419,15 +418,11 @@ void launch_hook(const Plan& P, cudaStream_t s, const HookArgs& a) {
 }
 
 // Summary-predicated streaming hook (the summary in shared memory, no
-// queues); the dynamic-schedule build for large forests.
+// queues).
 void launch_hook_sumd(hcc_ctx* c, const Plan& P, cudaStream_t s, const HookArgs& a) {
-  const size_t smem = (size_t)sum_region_words(a.s0f_words) * 4;
-  if (P.sum_prefix)
-    k_hook_sumd_pfx<<<c->sms * c->occ_hook_sumd, kHookSumdCta, smem, s>>>(a);
-  else if (P.dyn && P.n >= (1ull << 26))
-    k_hook_sumd_dyn<<<c->sms * c->occ_hook_sumd, kHookSumdCta, smem, s>>>(a);
-  else
-    k_hook_sumd<<<c->sms * c->occ_hook_sumd, kHookSumdCta, smem, s>>>(a);
+  (void)P;
+  k_hook_sumd<<<c->sms * c->occ_hook_sumd, kHookSumdCta,
+                (size_t)sum_region_words(a.s0f_words) * 4, s>>>(a);
 }
 
 // Segment hook of the adaptive / atomic engines (no appends).  HCC_SEG_CAS=0
@@ -465,11 +460,13 @@ bool sum_slot(const Plan& P, u64 sgi) {
 // Unrolled adaptive-plan slot whose hook is chosen on the device between the
 // summary-predicated k_hook_sumd (the slot that takes every remaining edge)
 // and the plain k_hook (forming slots).
-// Only with a one-bit-per-word summary (n <= 2^24): a coarser one covers
-// little of RMAT's lookups, and its 64 KB of shared memory then only costs
-// L1 (RMAT-28's steady slot 27.4 -> 32.4 ms, RMAT-26 7.3 -> 8.5 ms).
+// (The step before the slot also checks the summary's coverage of a sample
+// of the slot's endpoints, k_step_adapt: a coarse summary covers little of
+// RMAT's lookups at n > 2^24, and the kernel's 64 KB of shared memory then
+// only costs L1 -- RMAT-28's steady slot 27.4 -> 32.4 ms unconditionally --
+// while it pays for ER at n = 2^26: 17.3 -> 14.5 ms.)
 bool remainder_slot(const Plan& P, u64 sgi) {
-  return P.sumd == 1 && !P.sum_vote && P.sum && P.sum_shift == 0 && !P.sum_prefix && P.adapt &&
+  return P.sumd == 1 && !P.sum_vote && P.sum && P.adapt &&
          P.chunked && sgi >= 1 && !slot_small(P, sgi) && !(P.cas_mode >= 2 && sgi + 1 == P.nseg);
 }
 
@@ -572,14 +569,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
               ha.gate = kGateIfSum;
               hp.gate = kGateIfPlain;
               launch_hook_sum(c, q.s(), ha);
-              if (P.sumd) {
-                // the plain choice with summary-predicated lookups
-                HookArgs hd = ha;
-                hd.gate = kGateIfPlain;
-                launch_hook_sumd(c, P, q.s(), hd);
-              } else {
-                launch_hook(P, q.s(), hp);
-              }
+              launch_hook(P, q.s(), hp);
             } else if (P.sumd >= 2 && P.sum && sgi >= 1 && !ha.cas) {
               HookArgs hd = ha;
               hd.gate = kGateAlways;
@@ -608,14 +598,15 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
             // worklist passes reuse the last one: coverage only grows)
             // and so does the bitmap-use decision (a 2048-endpoint sample)
             const bool vote = sgi + 1 < P.nseg && sum_slot(P, sgi + 1) && P.sum_vote;
-            const int rvote = sgi + 1 < P.nseg && remainder_slot(P, sgi + 1) ? 1 : 0;
+            const bool rvote = sgi + 1 < P.nseg && remainder_slot(P, sgi + 1);
             if (P.s0b)
               k_step_adapt<<<1, 1024, 0, q.s()>>>(ctrl, recs, P.m, P.forming_pct,
                                                  vote ? c->s0f : nullptr, P.sum_words,
-                                                 P.edges, c->s0b, rvote);
+                                                 P.edges, c->s0b, rvote ? c->s0f : nullptr,
+                                                 P.sum_shift);
             else
               k_step_adapt<<<1, 1, 0, q.s()>>>(ctrl, recs, P.m, P.forming_pct, nullptr, 0,
-                                              nullptr, nullptr, 0);
+                                              nullptr, nullptr, nullptr, 0);
           } else
             k_step_segment<<<1, 1, 0, q.s()>>>(ctrl, recs, 0, 0);
         }
@@ -1143,16 +1134,6 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
     while (((nwords + (1ull << sh) - 1) >> sh) > (u64)kS0fMaxBytes * 8) ++sh;
     bool sum_ok = sh <= 6;
     if (const char* e = std::getenv("HCC_S0F")) sum_ok = sum_ok && std::atoi(e) != 0;
-    // HCC_S0F_PREFIX=1 (experiment): for n > 2^24, one bit per word over the
-    // first 2^19 words (vertices < 2^24, RMAT's hot prefix) instead of one
-    // bit per 2^shift words over all of them
-    const bool prefix = sh > 0 && std::getenv("HCC_S0F_PREFIX") &&
-                        std::atoi(std::getenv("HCC_S0F_PREFIX")) != 0;
-    if (prefix) {
-      sh = 0;
-      sum_ok = true;
-      P.sum_prefix = true;
-    }
     if (sum_ok) {
       P.sum = true;
       P.sum_shift = sh;
@@ -1161,10 +1142,9 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
       ensure_s0f(c, P.sum_words);
     }
   }
-  // with a coarse summary (shift > 0: n > 2^24) the summary hook still
-  // pays where the giant fills whole words (ER with n = 2^24 + 1: 3.0 ms on
-  // the plain hook), so the device vote between it and the plain hook stays
-  P.sum_vote = P.sum && P.sum_shift > 0;
+  // (HCC_SUM_VOTE=1: round 1's device vote between k_hook_sum and the
+  // plain hook on word coverage, instead of the k_hook_sumd choice)
+  P.sum_vote = false;
   if (const char* e = std::getenv("HCC_SUM_VOTE")) P.sum_vote = std::atoi(e) != 0;
   {
     const char* w = std::getenv("HCC_WALK");
@@ -1524,10 +1504,6 @@ int hcc_create(int device, hcc_ctx** out) {
                                 (int)kHookSmemMax));
   const int sumd_smem = (int)sum_region_words(kS0fMaxBytes / 4) * 4;
   HCC_CUDA(cudaFuncSetAttribute(k_hook_sumd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                sumd_smem));
-  HCC_CUDA(cudaFuncSetAttribute(k_hook_sumd_dyn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                sumd_smem));
-  HCC_CUDA(cudaFuncSetAttribute(k_hook_sumd_pfx, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 sumd_smem));
   HCC_CUDA(cudaFuncSetAttribute(k_hook_seg_cas_sumd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 sumd_smem));

@@ -56,9 +56,9 @@ constexpr int kHookCasCta = HCC_HOOK_CAS_CTA;
 #endif
 constexpr int kHookSumdCta = HCC_HOOK_SUMD_CTA;
 constexpr u32 kS0fMaxBytes = HCC_S0F_MAX_BYTES;
-// Shared-memory words the staged summary of `w` words occupies: whole
-// 32-word rows (the swizzle permutes within a row) plus the zero sentinel's.
-__host__ __device__ constexpr u32 sum_region_words(u32 w) { return ((w >> 5) + 1) << 5; }
+// Shared-memory words the staged summary of `w` words occupies (whole
+// 32-word rows: the swizzle permutes within a row).
+__host__ __device__ constexpr u32 sum_region_words(u32 w) { return ((w + 31) >> 5) << 5; }
 constexpr int kHookSlow = 4;
 // HookArgs.gate: k_hook_sum and k_hook are launched back to back for a
 // voted slot and the one not chosen (DevCtrl.use_sum) exits at entry.
@@ -210,8 +210,6 @@ __global__ void k_hook_sum_cas(HookArgs a);
 __global__ void k_hook_seg_cas(HookArgs a);
 __global__ void k_hook_sumd(HookArgs a);
 __global__ void k_hook_seg_cas_sumd(HookArgs a);
-__global__ void k_hook_sumd_dyn(HookArgs a);
-__global__ void k_hook_sumd_pfx(HookArgs a);
 __global__ void k_star_pick(const u32* pi, u64 n, DevCtrl* ctrl);
 __global__ void k_cas_hook(HookArgs a);
 __global__ void k_compress(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
@@ -231,7 +229,7 @@ __global__ void k_step_segment(DevCtrl* ctrl, DevRec* recs,
                                cudaGraphConditionalHandle h, int use_cond);
 __global__ void k_step_adapt(DevCtrl* ctrl, DevRec* recs, u64 m, u32 forming_pct,
                              const u32* sum, u32 sum_words, const uint2* edges,
-                             const u32* bits, int remainder_vote);
+                             const u32* bits, const u32* rsum, u32 rshift);
 __global__ void k_step_outer(DevCtrl* ctrl, DevRec* recs,
                              cudaGraphConditionalHandle h, int use_cond);
 __global__ void k_step_jump(DevCtrl* ctrl, cudaGraphConditionalHandle h,

@@ -123,14 +123,9 @@ __device__ __forceinline__ u32 sum_swz(u32 i) {
 }
 
 // Vertex x's group is all in star 0 (summary bit of bitmap word x >> 5).
-// PFX: a truncated table (HCC_S0F_PREFIX) covering only the first
-// words * 32 groups; later groups read the zero sentinel word past its end.
-// (Bounding every lookup made the default kernels spill, so it is a
-// separate instantiation.)
-template <bool PFX = false>
-__device__ __forceinline__ bool sum_covered(const u32* s_sum, u32 x, u32 shift, u32 words) {
+__device__ __forceinline__ bool sum_covered(const u32* s_sum, u32 x, u32 shift) {
   const u32 g = x >> (5u + shift);
-  return (s_sum[sum_swz(PFX ? min(g >> 5, words) : g >> 5)] >> (g & 31u)) & 1u;
+  return (s_sum[sum_swz(g >> 5)] >> (g & 31u)) & 1u;
 }
 
 // Control words a kernel reads at entry (dirty, star, use_sum) are written
@@ -386,7 +381,7 @@ __global__ void k_init_pi(u32* pi, u64 n, u32* bits) {
 // Lookups, root walk and stores for S edges of one thread (the body of a
 // hook tile).  Returns the mask of edges whose (h, l) pair in (pu, pv)
 // must be appended to the worklist (stored links and deferred walks).
-template <int S, bool SUM, bool BOTH = false, bool CAS = false, bool PFX = false>
+template <int S, bool SUM, bool BOTH = false, bool CAS = false>
 __device__ __forceinline__ u32 resolve_edges(const HookArgs& a, u32& links, u32& tries,
                                              const u32* bits,
                                              const u32* s_sum, u32 star,
@@ -401,8 +396,8 @@ __device__ __forceinline__ u32 resolve_edges(const HookArgs& a, u32& links, u32&
     for (int k = 0; k < S; ++k) {
       const u32 xu = ed[k].x >> 5, xv = ed[k].y >> 5;
       if (SUM) {
-        wu[k] = sum_covered<PFX>(s_sum, ed[k].x, a.s0f_shift, a.s0f_words) ? ~0u : ld_bits(bits + xu);
-        wv[k] = sum_covered<PFX>(s_sum, ed[k].y, a.s0f_shift, a.s0f_words) ? ~0u : ld_bits(bits + xv);
+        wu[k] = sum_covered(s_sum, ed[k].x, a.s0f_shift) ? ~0u : ld_bits(bits + xu);
+        wv[k] = sum_covered(s_sum, ed[k].y, a.s0f_shift) ? ~0u : ld_bits(bits + xv);
       } else {
         wu[k] = ld_bits(bits + xu);
         wv[k] = ld_bits(bits + xv);
@@ -522,7 +517,6 @@ __device__ __forceinline__ u32 resolve_edges(const HookArgs& a, u32& links, u32&
 // Copy the star-0 summary into shared memory (swizzled rows).
 __device__ __forceinline__ void load_summary(const HookArgs& a, u32* s_sum) {
   for (u32 i = threadIdx.x; i < a.s0f_words; i += blockDim.x) s_sum[sum_swz(i)] = a.s0f[i];
-  if (threadIdx.x == 0) s_sum[sum_swz(a.s0f_words)] = 0u;  // sentinel (sum_covered)
   __syncthreads();
 }
 
@@ -784,7 +778,7 @@ __device__ __forceinline__ void emit(const HookArgs& a, WarpOut& w, uint2* wl_ou
 // size for the bitmap's hot words; e.g. RMAT, whose isolated vertices break
 // most words) every edge takes the bitmap / gather path directly.
 template <int EPT, bool SUM, bool CAS = false, bool APPEND = true, bool SUMD = false,
-          bool DYNOK = true, bool PFX = false>
+          bool DYNOK = true>
 __device__ __forceinline__ void hook_stream(const HookArgs& a) {
   constexpr int S = kHookSlow;
   const uint2* src;
@@ -904,7 +898,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
 #else
       u32 h[EPT], l[EPT];
       const u32 act =
-          resolve_edges<EPT, true, false, CAS, PFX>(a, links, tries, bits, s_sum, star, ed, h, l);
+          resolve_edges<EPT, true, false, CAS>(a, links, tries, bits, s_sum, star, ed, h, l);
       emit<EPT, APPEND>(a, wo, wl_out, cnt_out, lane, act, h, l);
 #endif
       continue;
@@ -920,8 +914,8 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
       const bool done = ed[k].x == ed[k].y ||
-                        (sum_covered(s_sum, ed[k].x, a.s0f_shift, a.s0f_words) &&
-                         sum_covered(s_sum, ed[k].y, a.s0f_shift, a.s0f_words));
+                        (sum_covered(s_sum, ed[k].x, a.s0f_shift) &&
+                         sum_covered(s_sum, ed[k].y, a.s0f_shift));
       need |= done ? 0u : 1u << k;
     }
     const u32 nneed = __popc(need);
@@ -1020,34 +1014,26 @@ __global__ void __launch_bounds__(kHookCta, 1) k_hook_seg_cas_sumd(HookArgs a) {
 
 // Streaming hook with summary-predicated lookups (the summary in shared
 // memory, no slow-path queues: 64 KB instead of 128 KB of shared memory).
-// Static schedule: the dynamic one's state made it spill 40 B (measured on
-// RMAT-24's steady slot: the static schedule is as fast there).
+// Static schedule: the dynamic one's state made it spill 40 B, and the
+// kernel only serves n <= 2^24, where the static schedule is as fast.
 __global__ void __launch_bounds__(kHookSumdCta, 1) k_hook_sumd(HookArgs a) {
   if (a.gate == kGateIfPlain && __ldg(&a.ctrl->use_sum)) return;
   if (a.gate == kGateIfSum && !__ldg(&a.ctrl->use_sum)) return;
   hook_stream<kHookEPT, false, false, true, true, false>(a);
 }
 
-// Dynamic schedule (large forests, n >= 2^26: placement-dependent
-// stragglers, §3.2); spills 40 B.
-__global__ void __launch_bounds__(kHookSumdCta, 1) k_hook_sumd_dyn(HookArgs a) {
-  if (a.gate == kGateIfPlain && __ldg(&a.ctrl->use_sum)) return;
-  if (a.gate == kGateIfSum && !__ldg(&a.ctrl->use_sum)) return;
-  hook_stream<kHookEPT, false, false, true, true, true>(a);
-}
 
-// The large-forest build over a truncated (prefix) summary.
-__global__ void __launch_bounds__(kHookSumdCta, 1) k_hook_sumd_pfx(HookArgs a) {
-  if (a.gate == kGateIfPlain && __ldg(&a.ctrl->use_sum)) return;
-  if (a.gate == kGateIfSum && !__ldg(&a.ctrl->use_sum)) return;
-  hook_stream<kHookEPT, false, false, true, true, true, true>(a);
-}
 
 // Streaming hook with the star-0 summary in shared memory (full warps,
 // chunked appends, s0f set).
+// Static schedule (HCC_SUM_DYN=1: dynamic, which spilled 12 B and measured
+// the same: ER n = 2^24 + 1 2.34 vs 2.32 ms, n = 2^26 16.15 vs 16.14 ms).
+#ifndef HCC_SUM_DYN
+#define HCC_SUM_DYN 0
+#endif
 __global__ void __launch_bounds__(kHookSumCta, 1) k_hook_sum(HookArgs a) {
   if (a.gate == kGateIfSum && !__ldg(&a.ctrl->use_sum)) return;
-  hook_stream<kHookEPT, true>(a);
+  hook_stream<kHookEPT, true, false, true, false, HCC_SUM_DYN != 0>(a);
 }
 
 // Small segments (the forming regime): kSmallEPT (2) edges per thread, one
@@ -1512,7 +1498,7 @@ __global__ void k_step_segment(DevCtrl* c, DevRec* recs,
 // store ratio (records are per segment).
 __global__ void k_step_adapt(DevCtrl* c, DevRec* recs, u64 m, u32 forming_pct,
                              const u32* sum, u32 sum_words, const uint2* edges,
-                             const u32* bits, int remainder_vote) {
+                             const u32* bits, const u32* rsum, u32 rshift) {
   // Every thread derives the next range from the pass-start control words
   // (same addresses: broadcast reads), so the sample loads below issue
   // without waiting for thread 0's bookkeeping; thread 0 writes after the
@@ -1545,10 +1531,7 @@ __global__ void k_step_adapt(DevCtrl* c, DevRec* recs, u64 m, u32 forming_pct,
     c->seg_b = s_b;
     c->seg_e = s_e;
     c->seg = seg + 1;
-    // the summary-predicated hook streams the slot that takes every
-    // remaining edge (the steady regime: the forming slots' summaries cover
-    // little); the plain hook the others
-    if (remainder_vote) c->use_sum = (s_e == m && s_e > s_b) ? 1u : 0u;
+    if (rsum) c->use_sum = 0u;  // set below for the remainder slot
     c->passes += (len > 0);
     c->dirty = 0;
     next_rec(c, recs);
@@ -1558,6 +1541,18 @@ __global__ void k_step_adapt(DevCtrl* c, DevRec* recs, u64 m, u32 forming_pct,
     const u32 hits = ((bits[ed.x >> 5] >> (ed.x & 31u)) & 1u) + ((bits[ed.y >> 5] >> (ed.y & 31u)) & 1u);
     const int n_hit = __syncthreads_count(hits == 2) * 2 + __syncthreads_count(hits == 1);
     if (threadIdx.x == 0) c->use_bits = (u32)n_hit * 2 >= 2 * blockDim.x ? 1u : 0u;
+    // The slot that takes every remaining edge (the steady regime) streams
+    // with summary-predicated lookups (k_hook_sumd) when the summary
+    // answers at least a quarter of its sampled endpoints (RMAT-24: 63%;
+    // RMAT-28 with one bit per 16 words: little, and the kernel's 64 KB of
+    // shared memory would only cost L1); otherwise the plain hook.
+    if (rsum) {
+      const u32 gx = ed.x >> (5u + rshift), gy = ed.y >> (5u + rshift);
+      const u32 cov = ((rsum[gx >> 5] >> (gx & 31u)) & 1u) + ((rsum[gy >> 5] >> (gy & 31u)) & 1u);
+      const int n_cov = __syncthreads_count(cov == 2) * 2 + __syncthreads_count(cov == 1);
+      if (threadIdx.x == 0 && s_e == m)
+        c->use_sum = (u32)n_cov * 4 >= 2 * blockDim.x ? 1u : 0u;
+    }
   }
   // Star summary vote for the next hook launch: the summary path pays off
   // when at least half of the groups are covered.

@@ -289,3 +289,31 @@ def test_gpu_ipc_merge_multiprocess(oracle, tmp_path, world, cap):
         assert res["components"] == int(np.sum(want == np.arange(1 << 16, dtype=np.uint32)))
         if cap:
             assert res["reopens"] >= 1
+
+
+@pytest.mark.gpu
+def test_bench_multi_rank_path_on_one_gpu(tmp_path):
+    """bench.py's N > 1 code path (torchrun, 2 ranks; --share-gpus puts both
+    on the one GPU of the test box and uses gloo for the host collectives):
+    edge-partitioned RMAT-24, local CC + CUDA-IPC merge, e2e leg, the
+    reference-arm rule (rank 0 alone).  Checks the JSON line's schema and
+    that both ranks hold the same, correct labels."""
+    import json
+    import subprocess
+    import sys
+    root = Path(__file__).resolve().parents[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(root / "bench.py"),
+           "--gpus", "2", "--share-gpus", "--workload", "rmat24", "--steps", "2",
+           "--warmup", "3", "--e2e-steps", "1", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["labels_consistent_across_ranks"] and d["components"] == 7908545
+    assert d["config"]["edges_per_gpu"] == (1 << 27)
+    for k in ("roofline", "e2e", "clocks", "merge", "timing"):
+        assert k in d
+    assert d["e2e"]["value"] > 0 and d["merge"]["reopens"] == 0
