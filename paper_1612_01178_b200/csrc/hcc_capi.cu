@@ -318,6 +318,7 @@ struct Plan {
   // after the first, measured slower).
   int sumd = 1;
   bool sum_vote = false;
+  bool wl_sumd = true;         // worklist passes follow the steady slot's choice (HCC_WL_SUMD)
 };
 
 HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
@@ -631,7 +632,17 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
         wa.cas = P.cas_mode >= 1 && P.chunked ? 1 : 0;
         c->wl_kernel = wa.cas ? HCC_HOOK_KERNEL_CAS
                               : (P.chunked ? HCC_HOOK_KERNEL_STREAM : HCC_HOOK_KERNEL_LEGACY);
-        if (wa.s0f && P.adapt && P.sum_vote) {
+        if (wa.s0f && P.adapt && !P.sum_vote && P.sumd == 1 && wa.cas && P.wl_sumd) {
+          // after a steady slot that streamed with summary-predicated
+          // lookups (use_sum still set), the worklist passes do too
+          HookArgs wp = wa;
+          wa.gate = kGateIfSum;
+          wp.gate = kGateIfPlain;
+          wp.s0f = nullptr;
+          k_hook_cas_sumd<<<c->sms * c->occ_hook_cas_sumd, kHookCasCta,
+                            (size_t)sum_region_words(wa.s0f_words) * 4, q.s()>>>(wa);
+          launch_hook(P, q.s(), wp);
+        } else if (wa.s0f && P.adapt && P.sum_vote) {
           HookArgs wp = wa;
           wa.gate = kGateIfSum;
           wp.gate = kGateIfPlain;
@@ -1146,6 +1157,7 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   // plain hook on word coverage, instead of the k_hook_sumd choice)
   P.sum_vote = false;
   if (const char* e = std::getenv("HCC_SUM_VOTE")) P.sum_vote = std::atoi(e) != 0;
+  if (const char* e = std::getenv("HCC_WL_SUMD")) P.wl_sumd = std::atoi(e) != 0;
   {
     const char* w = std::getenv("HCC_WALK");
     P.walk = w ? std::atoi(w) : kDefaultWalk;
@@ -1263,6 +1275,7 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   key.plan = key.plan * 3 + (P.wide_compress ? 1 : 0);
   key.plan = key.plan * 3 + (u64)P.sumd;
   key.plan = key.plan * 3 + (P.sum_vote ? 1 : 0);
+  key.plan = key.plan * 3 + (P.wl_sumd ? 1 : 0);
   key.plan = key.plan * 1000003ull + P.sum_words * 64ull + P.sum_shift;
   key.plan = key.plan * 31 + (P.adapt ? 1000 + P.adapt_shift + 100000ull * P.forming_pct : 0);
   key.plan = key.plan * 1000003ull + P.adapt_first;
@@ -1507,6 +1520,11 @@ int hcc_create(int device, hcc_ctx** out) {
                                 sumd_smem));
   HCC_CUDA(cudaFuncSetAttribute(k_hook_seg_cas_sumd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 sumd_smem));
+  HCC_CUDA(cudaFuncSetAttribute(k_hook_cas_sumd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                sumd_smem));
+  HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_cas_sumd, kHookCasCta,
+                                                          sumd_smem));
+  c->occ_hook_cas_sumd = std::max(occ, 1);
   HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_sumd, kHookSumdCta,
                                                           sumd_smem));
   c->occ_hook_sumd = std::max(occ, 1);

@@ -117,7 +117,7 @@ struct hcc_ctx {
   u64 wl_cap = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int occ_hook = 1, occ_vert = 1, occ_hook_sum = 1, occ_hook_cas = 1, occ_hook_sum_cas = 1,
-      occ_hook_sumd = 1;
+      occ_hook_sumd = 1, occ_hook_cas_sumd = 1;
   // cached executable graph for repeated calls with identical arguments,
   // plus the previous one (two graphs used alternately, e.g. a pipelined
   // upload into one while the other runs, keep both instantiated)

@@ -1007,6 +1007,12 @@ __global__ void __launch_bounds__(kHookCta, HCC_HOOK_MINB) k_hook_seg_cas(HookAr
 #ifndef HCC_SUMD_HALVES
 #define HCC_SUMD_HALVES 0
 #endif
+// Worklist pass (CAS stores) with summary-predicated lookups.
+__global__ void __launch_bounds__(kHookCasCta, 1) k_hook_cas_sumd(HookArgs a) {
+  if (a.gate == kGateIfSum && !__ldg(&a.ctrl->use_sum)) return;
+  hook_stream<kHookEPT, false, true, true, true, false>(a);
+}
+
 // Adaptive / atomic segment hook with summary-predicated lookups.
 __global__ void __launch_bounds__(kHookCta, 1) k_hook_seg_cas_sumd(HookArgs a) {
   hook_stream<kHookEPT, false, true, false, true, false>(a);

@@ -719,14 +719,16 @@ def test_wide_compress_blocks(ctx, oracle, spec):
 @pytest.mark.parametrize("spec", ["rmatx:scale=20,ef=16,seed=7", "erx:n=16777217,m=67108864,seed=2",
                                   "grid:1100x1000", "erx:n=1048579,m=8000000,seed=5"])
 def test_steady_hook_variants(ctx, oracle, spec):
-    """The steady slot's hook choices give identical labels: k_hook_sumd
-    (default), the k_hook_sum / k_hook device vote (HCC_SUM_VOTE=1), the plain
-    hook (HCC_SUMD=0), sumd in every streaming slot (HCC_SUMD=2)."""
+    """The steady slot's hook choices give identical labels: k_hook_sumd by
+    sampled summary coverage (default; the worklist passes follow with
+    k_hook_cas_sumd), the k_hook_sum / k_hook device vote (HCC_SUM_VOTE=1),
+    the plain hook (HCC_SUMD=0), sumd in every streaming slot (HCC_SUMD=2),
+    plain worklist passes (HCC_WL_SUMD=0)."""
     import os
     g = ctx.generate(spec)
     want = oracle.cc(g.n, g.edges())
     for env in ({}, {"HCC_SUM_VOTE": "1"}, {"HCC_SUMD": "0"}, {"HCC_SUMD": "2"},
-                {"HCC_SUMD": "1", "HCC_DYN": "0"}):
+                {"HCC_SUMD": "1", "HCC_DYN": "0"}, {"HCC_WL_SUMD": "0"}):
         os.environ.update(env)
         try:
             lab, _ = ctx.cc(g, "baseline-mj")
