@@ -319,6 +319,7 @@ struct Plan {
   int sumd = 1;
   bool sum_vote = false;
   bool wl_sumd = true;         // worklist passes follow the steady slot's choice (HCC_WL_SUMD)
+X
 };
 
 HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
@@ -530,6 +531,13 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           ha.b = P.bounds[sgi];
           ha.e = P.bounds[sgi + 1];
           if (P.s0b && sgi >= 1) use_s0b(c, P, ha);
+          // star of the next bitmap (the giant need not contain vertex 0),
+          // not after the last slot (only the worklist passes would see
+          // it): the streaming hooks' last block runs the pick (no
+          // k_star_pick node), the small forming-slot hook gets the kernel
+          const bool pick = P.s0b && P.adapt && sgi >= 1 && sgi + 1 < P.nseg;
+          const bool pick_in_hook = pick && !slot_small(P, sgi) && P.fold_pick;
+          ha.pick = pick_in_hook ? 1 : 0;
           if (P.hook_events) q.record(c->seg_ev[2 * sgi]);
           c->slot_kernel.push_back(slot_small(P, sgi)       ? HCC_HOOK_KERNEL_SMALL
                                    : remainder_slot(P, sgi) ? HCC_HOOK_KERNEL_SUMD
@@ -581,10 +589,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           }
           if (P.hook_events) q.record(c->seg_ev[2 * sgi + 1]);
           q.phase_done(HCC_PHASE_HOOK);
-          // star of the next bitmap (the giant need not contain vertex 0)
-          // (not after the last slot: only the worklist passes would see it)
-          if (P.s0b && P.adapt && sgi >= 1 && sgi + 1 < P.nseg)
-            k_star_pick<<<1, 32, 0, q.s()>>>(P.pi, P.n, ctrl);
+          if (pick && !pick_in_hook) k_star_pick<<<1, 32, 0, q.s()>>>(P.pi, P.n, ctrl);
           // compress (+ star-0 bitmap, initialised by k_start)
           if (P.s0b)
             launch_compress_s0b(c, P, q.s());
@@ -1158,6 +1163,7 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   P.sum_vote = false;
   if (const char* e = std::getenv("HCC_SUM_VOTE")) P.sum_vote = std::atoi(e) != 0;
   if (const char* e = std::getenv("HCC_WL_SUMD")) P.wl_sumd = std::atoi(e) != 0;
+  if (const char* e = std::getenv("HCC_FOLD_PICK")) P.fold_pick = std::atoi(e) != 0;
   {
     const char* w = std::getenv("HCC_WALK");
     P.walk = w ? std::atoi(w) : kDefaultWalk;
@@ -1276,6 +1282,7 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   key.plan = key.plan * 3 + (u64)P.sumd;
   key.plan = key.plan * 3 + (P.sum_vote ? 1 : 0);
   key.plan = key.plan * 3 + (P.wl_sumd ? 1 : 0);
+  key.plan = key.plan * 3 + (P.fold_pick ? 1 : 0);
   key.plan = key.plan * 1000003ull + P.sum_words * 64ull + P.sum_shift;
   key.plan = key.plan * 31 + (P.adapt ? 1000 + P.adapt_shift + 100000ull * P.forming_pct : 0);
   key.plan = key.plan * 1000003ull + P.adapt_first;
@@ -1429,12 +1436,15 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
     if (o->algo == HCC_ALGO_BASELINE_MJ && !P.full_passes && !P.bounds.empty()) {
       const u64 wl = nrec > nseg ? nrec - nseg : 0;
       k += 3 * nseg + 3 * wl;  // hook+compress+step per slot and per wl pass
-      if (P.s0b && P.adapt && nseg >= 3) k += nseg - 2;  // k_star_pick, slots 1..nseg-2
-      if (P.sum && P.adapt && nseg <= kMaxUnrolledSegments) {
-        // voted launches: summary and plain hook back to back
-        for (u64 sgi = 1; sgi < nseg; ++sgi) k += sum_slot(P, sgi) ? 1 : 0;
-        k += wl;
+      for (u64 sgi = 1; sgi < nseg && nseg <= kMaxUnrolledSegments; ++sgi) {
+        const bool pick = P.s0b && P.adapt && sgi + 1 < nseg;
+        k += pick && !(P.fold_pick && !slot_small(P, sgi)) ? 1 : 0;  // k_star_pick
+        // gated pairs (two launches, one exits at entry)
+        k += remainder_slot(P, sgi) || (P.sum && P.adapt && P.sum_vote && sum_slot(P, sgi)) ? 1 : 0;
       }
+      // gated worklist pairs
+      if (P.sum && P.adapt && ((P.sum_vote) || (P.sumd == 1 && P.wl_sumd && P.cas_mode >= 1)))
+        k += wl;
     } else {
       k += (chain ? 2 : P.cas_stream ? 4 : 3) * iters;  // hook/(pick)/compress(or jump)/step
     }
