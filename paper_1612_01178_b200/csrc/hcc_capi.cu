@@ -319,7 +319,11 @@ struct Plan {
   int sumd = 1;
   bool sum_vote = false;
   bool wl_sumd = true;         // worklist passes follow the steady slot's choice (HCC_WL_SUMD)
-X
+  // star pick in the streaming hook's last block instead of a k_star_pick
+  // node (HCC_FOLD_PICK=1): measured no gain for the worklist engine
+  // (RMAT-24 1.474 vs 1.477 ms, ER and grid slightly slower: the pick's
+  // dependent chases then extend the hook's tail instead of a node)
+  bool fold_pick = false;
 };
 
 HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
