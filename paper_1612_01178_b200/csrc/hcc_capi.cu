@@ -472,8 +472,10 @@ bool sum_slot(const Plan& P, u64 sgi) {
 // only costs L1 -- RMAT-28's steady slot 27.4 -> 32.4 ms unconditionally --
 // while it pays for ER at n = 2^26: 17.3 -> 14.5 ms.)
 bool remainder_slot(const Plan& P, u64 sgi) {
+  // (slot 1 would be the remainder only if the first m/128 edges left the
+  // graph out of the forming regime: no gated pair there)
   return P.sumd == 1 && !P.sum_vote && P.sum && P.adapt &&
-         P.chunked && sgi >= 1 && !slot_small(P, sgi) && !(P.cas_mode >= 2 && sgi + 1 == P.nseg);
+         P.chunked && sgi >= 2 && !slot_small(P, sgi) && !(P.cas_mode >= 2 && sgi + 1 == P.nseg);
 }
 
 // Enqueue one full CC run (pi init through convergence) on seq.

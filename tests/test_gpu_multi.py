@@ -145,7 +145,7 @@ def _digest(lab: np.ndarray) -> str:
     return hashlib.sha256(np.ascontiguousarray(lab, dtype="<u4").tobytes()).hexdigest()
 
 
-@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("G", [2, 4, 8])
 def test_rmat28_edge_partitioned_exact(capi, G):
     """BASELINE configs[4]: RMAT scale-28 (2^32 edges) edge-partitioned over G
     shards, bit-exact against the streaming oracle's digest."""
