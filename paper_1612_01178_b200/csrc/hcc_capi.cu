@@ -426,9 +426,11 @@ void launch_hook(const Plan& P, cudaStream_t s, const HookArgs& a) {
 // Summary-predicated streaming hook (the summary in shared memory, no
 // queues).
 void launch_hook_sumd(hcc_ctx* c, const Plan& P, cudaStream_t s, const HookArgs& a) {
-  (void)P;
-  k_hook_sumd<<<c->sms * c->occ_hook_sumd, kHookSumdCta,
-                (size_t)sum_region_words(a.s0f_words) * 4, s>>>(a);
+  const size_t smem = (size_t)sum_region_words(a.s0f_words) * 4;
+  if (P.sum_shift == 0)
+    k_hook_sumd<<<c->sms * c->occ_hook_sumd, kHookSumdCta, smem, s>>>(a);
+  else
+    k_hook_sumd_sh<<<c->sms * c->occ_hook_sumd, kHookSumdCta, smem, s>>>(a);
 }
 
 // Segment hook of the adaptive / atomic engines (no appends).  HCC_SEG_CAS=0
@@ -650,8 +652,12 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           wa.gate = kGateIfSum;
           wp.gate = kGateIfPlain;
           wp.s0f = nullptr;
-          k_hook_cas_sumd<<<c->sms * c->occ_hook_cas_sumd, kHookCasCta,
-                            (size_t)sum_region_words(wa.s0f_words) * 4, q.s()>>>(wa);
+          if (P.sum_shift == 0)
+            k_hook_cas_sumd<<<c->sms * c->occ_hook_cas_sumd, kHookCasCta,
+                              (size_t)sum_region_words(wa.s0f_words) * 4, q.s()>>>(wa);
+          else
+            k_hook_cas_sumd_sh<<<c->sms * c->occ_hook_cas_sumd, kHookCasCta,
+                                 (size_t)sum_region_words(wa.s0f_words) * 4, q.s()>>>(wa);
           launch_hook(P, q.s(), wp);
         } else if (wa.s0f && P.adapt && P.sum_vote) {
           HookArgs wp = wa;
@@ -1537,6 +1543,10 @@ int hcc_create(int device, hcc_ctx** out) {
   HCC_CUDA(cudaFuncSetAttribute(k_hook_seg_cas_sumd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 sumd_smem));
   HCC_CUDA(cudaFuncSetAttribute(k_hook_cas_sumd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                sumd_smem));
+  HCC_CUDA(cudaFuncSetAttribute(k_hook_cas_sumd_sh, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                sumd_smem));
+  HCC_CUDA(cudaFuncSetAttribute(k_hook_sumd_sh, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 sumd_smem));
   HCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hook_cas_sumd, kHookCasCta,
                                                           sumd_smem));

@@ -209,6 +209,8 @@ __global__ void k_hook_cas(HookArgs a);
 __global__ void k_hook_sum_cas(HookArgs a);
 __global__ void k_hook_seg_cas(HookArgs a);
 __global__ void k_hook_sumd(HookArgs a);
+__global__ void k_hook_sumd_sh(HookArgs a);
+__global__ void k_hook_cas_sumd_sh(HookArgs a);
 __global__ void k_hook_seg_cas_sumd(HookArgs a);
 __global__ void k_hook_cas_sumd(HookArgs a);
 __global__ void k_star_pick(const u32* pi, u64 n, DevCtrl* ctrl);

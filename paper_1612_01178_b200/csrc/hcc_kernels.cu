@@ -118,8 +118,16 @@ __device__ __forceinline__ u32 ld_pi_gather(const u32* p) {
 // a hash of its row index.  Skewed graphs hit summary words whose indices
 // have few one bits (RMAT hubs: 0, 32, 64, 1024, ...), which would all sit
 // in bank 0 unswizzled.
+#ifndef HCC_SWZ
+#define HCC_SWZ 0
+#endif
+
 __device__ __forceinline__ u32 sum_swz(u32 i) {
+#if HCC_SWZ == 1
+  return i ^ ((i >> 5) & 31u);
+#else
   return i ^ (((i >> 5) ^ (i >> 10)) & 31u);
+#endif
 }
 
 // Vertex x's group is all in star 0 (summary bit of bitmap word x >> 5).
@@ -381,7 +389,7 @@ __global__ void k_init_pi(u32* pi, u64 n, u32* bits) {
 // Lookups, root walk and stores for S edges of one thread (the body of a
 // hook tile).  Returns the mask of edges whose (h, l) pair in (pu, pv)
 // must be appended to the worklist (stored links and deferred walks).
-template <int S, bool SUM, bool BOTH = false, bool CAS = false>
+template <int S, bool SUM, bool BOTH = false, bool CAS = false, bool SH0 = false>
 __device__ __forceinline__ u32 resolve_edges(const HookArgs& a, u32& links, u32& tries,
                                              const u32* bits,
                                              const u32* s_sum, u32 star,
@@ -396,8 +404,12 @@ __device__ __forceinline__ u32 resolve_edges(const HookArgs& a, u32& links, u32&
     for (int k = 0; k < S; ++k) {
       const u32 xu = ed[k].x >> 5, xv = ed[k].y >> 5;
       if (SUM) {
-        wu[k] = sum_covered(s_sum, ed[k].x, a.s0f_shift) ? ~0u : ld_bits(bits + xu);
-        wv[k] = sum_covered(s_sum, ed[k].y, a.s0f_shift) ? ~0u : ld_bits(bits + xv);
+        // (SH0: the one-bit-per-word table of n <= 2^24 as a compile-time
+        // shift: the steady slot 0.825 -> 0.790 ms on RMAT-24, though
+        // ptxas then spills 8 B in k_hook_sumd)
+        const u32 sh = SH0 ? 0u : a.s0f_shift;
+        wu[k] = sum_covered(s_sum, ed[k].x, sh) ? ~0u : ld_bits(bits + xu);
+        wv[k] = sum_covered(s_sum, ed[k].y, sh) ? ~0u : ld_bits(bits + xv);
       } else {
         wu[k] = ld_bits(bits + xu);
         wv[k] = ld_bits(bits + xv);
@@ -778,7 +790,7 @@ __device__ __forceinline__ void emit(const HookArgs& a, WarpOut& w, uint2* wl_ou
 // size for the bitmap's hot words; e.g. RMAT, whose isolated vertices break
 // most words) every edge takes the bitmap / gather path directly.
 template <int EPT, bool SUM, bool CAS = false, bool APPEND = true, bool SUMD = false,
-          bool DYNOK = true>
+          bool DYNOK = true, bool SH0 = false>
 __device__ __forceinline__ void hook_stream(const HookArgs& a) {
   constexpr int S = kHookSlow;
   const uint2* src;
@@ -898,7 +910,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
 #else
       u32 h[EPT], l[EPT];
       const u32 act =
-          resolve_edges<EPT, true, false, CAS>(a, links, tries, bits, s_sum, star, ed, h, l);
+          resolve_edges<EPT, true, false, CAS, SH0>(a, links, tries, bits, s_sum, star, ed, h, l);
       emit<EPT, APPEND>(a, wo, wl_out, cnt_out, lane, act, h, l);
 #endif
       continue;
@@ -1010,12 +1022,17 @@ __global__ void __launch_bounds__(kHookCta, HCC_HOOK_MINB) k_hook_seg_cas(HookAr
 // Worklist pass (CAS stores) with summary-predicated lookups.
 __global__ void __launch_bounds__(kHookCasCta, 1) k_hook_cas_sumd(HookArgs a) {
   if (a.gate == kGateIfSum && !__ldg(&a.ctrl->use_sum)) return;
+  hook_stream<kHookEPT, false, true, true, true, false, true>(a);
+}
+
+__global__ void __launch_bounds__(kHookCasCta, 1) k_hook_cas_sumd_sh(HookArgs a) {
+  if (a.gate == kGateIfSum && !__ldg(&a.ctrl->use_sum)) return;
   hook_stream<kHookEPT, false, true, true, true, false>(a);
 }
 
 // Adaptive / atomic segment hook with summary-predicated lookups.
 __global__ void __launch_bounds__(kHookCta, 1) k_hook_seg_cas_sumd(HookArgs a) {
-  hook_stream<kHookEPT, false, true, false, true, false>(a);
+  hook_stream<kHookEPT, false, true, false, true, false, true>(a);
 }
 
 // Streaming hook with summary-predicated lookups (the summary in shared
@@ -1023,6 +1040,13 @@ __global__ void __launch_bounds__(kHookCta, 1) k_hook_seg_cas_sumd(HookArgs a) {
 // Static schedule: the dynamic one's state made it spill 40 B, and the
 // kernel only serves n <= 2^24, where the static schedule is as fast.
 __global__ void __launch_bounds__(kHookSumdCta, 1) k_hook_sumd(HookArgs a) {
+  if (a.gate == kGateIfPlain && __ldg(&a.ctrl->use_sum)) return;
+  if (a.gate == kGateIfSum && !__ldg(&a.ctrl->use_sum)) return;
+  hook_stream<kHookEPT, false, false, true, true, false, true>(a);
+}
+
+// A coarser summary (n > 2^24: one bit per 2^shift words).
+__global__ void __launch_bounds__(kHookSumdCta, 1) k_hook_sumd_sh(HookArgs a) {
   if (a.gate == kGateIfPlain && __ldg(&a.ctrl->use_sum)) return;
   if (a.gate == kGateIfSum && !__ldg(&a.ctrl->use_sum)) return;
   hook_stream<kHookEPT, false, false, true, true, false>(a);
