@@ -56,9 +56,9 @@ constexpr int kHookCasCta = HCC_HOOK_CAS_CTA;
 #endif
 constexpr int kHookSumdCta = HCC_HOOK_SUMD_CTA;
 constexpr u32 kS0fMaxBytes = HCC_S0F_MAX_BYTES;
-// Shared-memory words the staged summary of `w` words occupies (whole
-// 32-word rows: the swizzle permutes within a row).
-__host__ __device__ constexpr u32 sum_region_words(u32 w) { return ((w + 31) >> 5) << 5; }
+// Shared-memory words the staged summary of `w` words occupies (32-word rows
+// padded to 33 words, sum_swz).
+__host__ __device__ constexpr u32 sum_region_words(u32 w) { return ((w + 31) >> 5) * 33; }
 constexpr int kHookSlow = 4;
 // HookArgs.gate: k_hook_sum and k_hook are launched back to back for a
 // voted slot and the one not chosen (DevCtrl.use_sum) exits at entry.

@@ -114,23 +114,14 @@ __device__ __forceinline__ u32 ld_pi_gather(const u32* p) {
 #endif
 }
 
-// Shared-memory slot of summary word i: each 32-word row is XOR-permuted by
-// a hash of its row index.  Skewed graphs hit summary words whose indices
-// have few one bits (RMAT hubs: 0, 32, 64, 1024, ...), which would all sit
-// in bank 0 unswizzled.
-#ifndef HCC_SWZ
-#define HCC_SWZ 0
-#endif
+// Shared-memory slot of summary word i: 32-word rows padded to 33 words, so
+// consecutive rows start in consecutive banks.  Skewed graphs hit summary
+// words whose indices have few one bits (RMAT hubs: 0, 32, 64, ...), which
+// would all sit in bank 0 unpadded.  (Round 1 XOR-permuted each row by a
+// hash of its index, 5 instructions a lookup against 2: RMAT-24 1.431 ->
+// 1.414 ms, ER 2^24 2.00 -> 1.90 ms with the padding.)
+__device__ __forceinline__ u32 sum_swz(u32 i) { return i + (i >> 5); }
 
-__device__ __forceinline__ u32 sum_swz(u32 i) {
-#if HCC_SWZ == 1
-  return i ^ ((i >> 5) & 31u);
-#else
-  return i ^ (((i >> 5) ^ (i >> 10)) & 31u);
-#endif
-}
-
-// Vertex x's group is all in star 0 (summary bit of bitmap word x >> 5).
 __device__ __forceinline__ bool sum_covered(const u32* s_sum, u32 x, u32 shift) {
   const u32 g = x >> (5u + shift);
   return (s_sum[sum_swz(g >> 5)] >> (g & 31u)) & 1u;
