@@ -373,7 +373,7 @@ size_t hook_smem(const HookArgs& a, unsigned block) {
   return (size_t)sum_region_words(a.s0f_words) * 4 + (size_t)((block + 31) / 32) * 32 * kHookEPT * 8;
 }
 constexpr size_t kHookSmemMax =
-    (size_t)sum_region_words(kS0fMaxBytes / 4) * 4 + (size_t)kHookSumCta * kHookEPT * 8;
+    (size_t)sum_region_words(kSumTableMaxBytes / 4) * 4 + (size_t)kHookSumCta * kHookEPT * 8;
 
 // Unrolled topology slot that runs the small-segment hook (forming regime).
 bool slot_small(const Plan& P, u64 sgi) {
@@ -427,7 +427,7 @@ void launch_hook(const Plan& P, cudaStream_t s, const HookArgs& a) {
 // queues).
 void launch_hook_sumd(hcc_ctx* c, const Plan& P, cudaStream_t s, const HookArgs& a) {
   const size_t smem = (size_t)sum_region_words(a.s0f_words) * 4;
-  if (P.sum_shift == 0)
+  if (P.sum_shift == kSumShiftFixed)
     k_hook_sumd<<<c->sms * c->occ_hook_sumd, kHookSumdCta, smem, s>>>(a);
   else
     k_hook_sumd_sh<<<c->sms * c->occ_hook_sumd, kHookSumdCta, smem, s>>>(a);
@@ -440,8 +440,11 @@ void launch_hook_sumd(hcc_ctx* c, const Plan& P, cudaStream_t s, const HookArgs&
 void launch_seg_cas(const Plan& P, cudaStream_t s, const HookArgs& a) {
   static const int v = std::getenv("HCC_SEG_CAS") ? std::atoi(std::getenv("HCC_SEG_CAS")) : 1;
   static const int sd = std::getenv("HCC_SEG_SUMD") ? std::atoi(std::getenv("HCC_SEG_SUMD")) : 1;
-  if (v && sd && P.sum && P.sum_shift == 0 && a.s0f) {
+  if (v && sd && P.sum && P.sum_shift == kSumShiftFixed && a.s0f) {
     k_hook_seg_cas_sumd<<<P.grid_hook, kHookCta, (size_t)sum_region_words(a.s0f_words) * 4, s>>>(a);
+  } else if (v && sd && P.sum && P.sum_shift == 0 && a.s0f) {
+    k_hook_seg_cas_sumd_sh<<<P.grid_hook, kHookCta, (size_t)sum_region_words(a.s0f_words) * 4,
+                             s>>>(a);
   } else if (v) {
     k_hook_seg_cas<<<P.grid_hook, kHookCta, 0, s>>>(a);
   } else {
@@ -652,7 +655,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
           wa.gate = kGateIfSum;
           wp.gate = kGateIfPlain;
           wp.s0f = nullptr;
-          if (P.sum_shift == 0)
+          if (P.sum_shift == kSumShiftFixed)
             k_hook_cas_sumd<<<c->sms * c->occ_hook_cas_sumd, kHookCasCta,
                               (size_t)sum_region_words(wa.s0f_words) * 4, q.s()>>>(wa);
           else
@@ -1162,11 +1165,17 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
     while (((nwords + (1ull << sh) - 1) >> sh) > (u64)kS0fMaxBytes * 8) ++sh;
     bool sum_ok = sh <= 6;
     if (const char* e = std::getenv("HCC_S0F")) sum_ok = sum_ok && std::atoi(e) != 0;
+    // one bit per 16 vertices while that table fits (HCC_SUM_HALF=0: per word)
+    // (not for the adaptive engine's 31 short segment hooks, whose L1 the
+    // 132 KB table costs more: RMAT-24 2.81 vs 2.66 ms)
+    bool half = HCC_SUM_HALF && (n + 15) / 16 <= (u64)kSumHalfMaxBytes * 8 && !cas_stream;
+    if (const char* e = std::getenv("HCC_SUM_HALF")) half = half && std::atoi(e) != 0;
     if (sum_ok) {
       P.sum = true;
-      P.sum_shift = sh;
-      P.sum_words = (u32)std::min<u64>((((nwords + (1ull << sh) - 1) >> sh) + 31) / 32,
-                                       kS0fMaxBytes / 4);
+      P.sum_shift = half ? kSumHalfShift : sh;
+      P.sum_words = half ? (u32)(((n + 15) / 16 + 31) / 32)
+                         : (u32)std::min<u64>((((nwords + (1ull << sh) - 1) >> sh) + 31) / 32,
+                                              kS0fMaxBytes / 4);
       ensure_s0f(c, P.sum_words);
     }
   }
@@ -1537,7 +1546,7 @@ int hcc_create(int device, hcc_ctx** out) {
                                 (int)kHookSmemMax));
   HCC_CUDA(cudaFuncSetAttribute(k_hook_sum_cas, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kHookSmemMax));
-  const int sumd_smem = (int)sum_region_words(kS0fMaxBytes / 4) * 4;
+  const int sumd_smem = (int)sum_region_words(kSumTableMaxBytes / 4) * 4;
   HCC_CUDA(cudaFuncSetAttribute(k_hook_sumd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 sumd_smem));
   HCC_CUDA(cudaFuncSetAttribute(k_hook_seg_cas_sumd, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1545,6 +1554,8 @@ int hcc_create(int device, hcc_ctx** out) {
   HCC_CUDA(cudaFuncSetAttribute(k_hook_cas_sumd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 sumd_smem));
   HCC_CUDA(cudaFuncSetAttribute(k_hook_cas_sumd_sh, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                sumd_smem));
+  HCC_CUDA(cudaFuncSetAttribute(k_hook_seg_cas_sumd_sh, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 sumd_smem));
   HCC_CUDA(cudaFuncSetAttribute(k_hook_sumd_sh, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 sumd_smem));

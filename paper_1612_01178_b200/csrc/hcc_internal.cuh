@@ -56,6 +56,20 @@ constexpr int kHookCasCta = HCC_HOOK_CAS_CTA;
 #endif
 constexpr int kHookSumdCta = HCC_HOOK_SUMD_CTA;
 constexpr u32 kS0fMaxBytes = HCC_S0F_MAX_BYTES;
+// Half-word summary (one bit per 16 vertices: RMAT-24's lookups are 76%
+// covered instead of 63% at one bit per 32), used while its table fits
+// kSumHalfMaxBytes (n <= 2^24).  Its shift is ~0u: consumers index bit
+// x >> (5 + shift), and 5 + ~0u wraps to 4.
+#ifndef HCC_SUM_HALF
+#define HCC_SUM_HALF 1
+#endif
+constexpr u32 kSumHalfShift = ~0u;
+constexpr u32 kSumHalfMaxBytes = 128u * 1024u;
+// Largest staged table (shared-memory budgets of the summary hooks).
+constexpr u32 kSumTableMaxBytes = kSumHalfMaxBytes > kS0fMaxBytes ? kSumHalfMaxBytes : kS0fMaxBytes;
+// The shift the summary-predicated kernels compile in (their _sh builds take
+// it at run time).
+constexpr u32 kSumShiftFixed = HCC_SUM_HALF ? kSumHalfShift : 0u;
 // Shared-memory words the staged summary of `w` words occupies (32-word rows
 // padded to 33 words, sum_swz).
 __host__ __device__ constexpr u32 sum_region_words(u32 w) { return ((w + 31) >> 5) * 33; }
@@ -212,6 +226,7 @@ __global__ void k_hook_sumd(HookArgs a);
 __global__ void k_hook_sumd_sh(HookArgs a);
 __global__ void k_hook_cas_sumd_sh(HookArgs a);
 __global__ void k_hook_seg_cas_sumd(HookArgs a);
+__global__ void k_hook_seg_cas_sumd_sh(HookArgs a);
 __global__ void k_hook_cas_sumd(HookArgs a);
 __global__ void k_star_pick(const u32* pi, u64 n, DevCtrl* ctrl);
 __global__ void k_cas_hook(HookArgs a);

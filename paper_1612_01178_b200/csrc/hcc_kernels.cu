@@ -395,10 +395,9 @@ __device__ __forceinline__ u32 resolve_edges(const HookArgs& a, u32& links, u32&
     for (int k = 0; k < S; ++k) {
       const u32 xu = ed[k].x >> 5, xv = ed[k].y >> 5;
       if (SUM) {
-        // (SH0: the one-bit-per-word table of n <= 2^24 as a compile-time
-        // shift: the steady slot 0.825 -> 0.790 ms on RMAT-24, though
-        // ptxas then spills 8 B in k_hook_sumd)
-        const u32 sh = SH0 ? 0u : a.s0f_shift;
+        // (SH0: the table of n <= 2^24 with a compile-time shift: the
+        // steady slot 0.825 -> 0.790 ms on RMAT-24 at one bit per word)
+        const u32 sh = SH0 ? kSumShiftFixed : a.s0f_shift;
         wu[k] = sum_covered(s_sum, ed[k].x, sh) ? ~0u : ld_bits(bits + xu);
         wv[k] = sum_covered(s_sum, ed[k].y, sh) ? ~0u : ld_bits(bits + xv);
       } else {
@@ -1026,6 +1025,10 @@ __global__ void __launch_bounds__(kHookCta, 1) k_hook_seg_cas_sumd(HookArgs a) {
   hook_stream<kHookEPT, false, true, false, true, false, true>(a);
 }
 
+__global__ void __launch_bounds__(kHookCta, 1) k_hook_seg_cas_sumd_sh(HookArgs a) {
+  hook_stream<kHookEPT, false, true, false, true, false>(a);
+}
+
 // Streaming hook with summary-predicated lookups (the summary in shared
 // memory, no slow-path queues: 64 KB instead of 128 KB of shared memory).
 // Static schedule: the dynamic one's state made it spill 40 B, and the
@@ -1335,6 +1338,21 @@ __device__ __forceinline__ void emit_bits(u64 chunk, u64 n, u64 v0, u32 byte, u3
   w |= __shfl_xor_sync(0xffffffffu, w, 2);
   if ((lane & 3u) == 0 && v0 < n) bits[v0 >> 5] = w;
   if (!sum) return;
+  if (sum_shift == kSumHalfShift) {
+    // one bit per 16 vertices: word j of the warp (lanes 4j..4j+3) gives
+    // bits 2j (low half all in the star) and 2j + 1 (high half); a warp's
+    // 8 words are one 16-bit summary halfword
+    const u32 h2 = ((lane & 3u) == 0 && v0 < n)
+                       ? (((w & 0xffffu) == 0xffffu) ? 1u : 0u) | ((w >> 16) == 0xffffu ? 2u : 0u)
+                       : 0u;
+    u32 b16 = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) b16 |= __shfl_sync(0xffffffffu, h2, 4 * j) << (2 * j);
+    const u64 hw_idx = (chunk * blockDim.x + threadIdx.x) >> 5;
+    if (lane == 0 && hw_idx < (u64)sum_words * 2)
+      reinterpret_cast<unsigned short*>(sum)[hw_idx] = (unsigned short)b16;
+    return;
+  }
   // Star-0 summary: this chunk's 64 words -> 64 >> sum_shift bits (bit =
   // every word of its group is all ones).  Groups shared with other chunks
   // are merged with atomics (clear, then set), whole summary words stored.
