@@ -440,9 +440,9 @@ void launch_hook_sumd(hcc_ctx* c, const Plan& P, cudaStream_t s, const HookArgs&
 void launch_seg_cas(const Plan& P, cudaStream_t s, const HookArgs& a) {
   static const int v = std::getenv("HCC_SEG_CAS") ? std::atoi(std::getenv("HCC_SEG_CAS")) : 1;
   static const int sd = std::getenv("HCC_SEG_SUMD") ? std::atoi(std::getenv("HCC_SEG_SUMD")) : 1;
-  if (v && sd && P.sum && P.sum_shift == kSumShiftFixed && a.s0f) {
+  if (v && sd && P.sum && P.sum_shift == 0 && a.s0f) {
     k_hook_seg_cas_sumd<<<P.grid_hook, kHookCta, (size_t)sum_region_words(a.s0f_words) * 4, s>>>(a);
-  } else if (v && sd && P.sum && P.sum_shift == 0 && a.s0f) {
+  } else if (v && sd && P.sum && a.s0f) {
     k_hook_seg_cas_sumd_sh<<<P.grid_hook, kHookCta, (size_t)sum_region_words(a.s0f_words) * 4,
                              s>>>(a);
   } else if (v) {

@@ -114,6 +114,9 @@ __device__ __forceinline__ u32 ld_pi_gather(const u32* p) {
 #endif
 }
 
+// Template shift of the summary-predicated kernels (kSumShiftFixed).
+constexpr int kSumFixSh = HCC_SUM_HALF ? -2 : 0;
+
 // Shared-memory slot of summary word i: 32-word rows padded to 33 words, so
 // consecutive rows start in consecutive banks.  Skewed graphs hit summary
 // words whose indices have few one bits (RMAT hubs: 0, 32, 64, ...), which
@@ -380,7 +383,9 @@ __global__ void k_init_pi(u32* pi, u64 n, u32* bits) {
 // Lookups, root walk and stores for S edges of one thread (the body of a
 // hook tile).  Returns the mask of edges whose (h, l) pair in (pu, pv)
 // must be appended to the worklist (stored links and deferred walks).
-template <int S, bool SUM, bool BOTH = false, bool CAS = false, bool SH0 = false>
+// FIXSH: the summary's shift as a compile-time constant (>= 0, or -2 for
+// the half-word table's ~0u), -1 = the run-time a.s0f_shift.
+template <int S, bool SUM, bool BOTH = false, bool CAS = false, int FIXSH = -1>
 __device__ __forceinline__ u32 resolve_edges(const HookArgs& a, u32& links, u32& tries,
                                              const u32* bits,
                                              const u32* s_sum, u32 star,
@@ -395,9 +400,9 @@ __device__ __forceinline__ u32 resolve_edges(const HookArgs& a, u32& links, u32&
     for (int k = 0; k < S; ++k) {
       const u32 xu = ed[k].x >> 5, xv = ed[k].y >> 5;
       if (SUM) {
-        // (SH0: the table of n <= 2^24 with a compile-time shift: the
-        // steady slot 0.825 -> 0.790 ms on RMAT-24 at one bit per word)
-        const u32 sh = SH0 ? kSumShiftFixed : a.s0f_shift;
+        // (a compile-time shift: the steady slot 0.825 -> 0.790 ms on
+        // RMAT-24 at one bit per word)
+        const u32 sh = FIXSH == -2 ? kSumHalfShift : FIXSH >= 0 ? (u32)FIXSH : a.s0f_shift;
         wu[k] = sum_covered(s_sum, ed[k].x, sh) ? ~0u : ld_bits(bits + xu);
         wv[k] = sum_covered(s_sum, ed[k].y, sh) ? ~0u : ld_bits(bits + xv);
       } else {
@@ -780,7 +785,7 @@ __device__ __forceinline__ void emit(const HookArgs& a, WarpOut& w, uint2* wl_ou
 // size for the bitmap's hot words; e.g. RMAT, whose isolated vertices break
 // most words) every edge takes the bitmap / gather path directly.
 template <int EPT, bool SUM, bool CAS = false, bool APPEND = true, bool SUMD = false,
-          bool DYNOK = true, bool SH0 = false>
+          bool DYNOK = true, int FIXSH = -1>
 __device__ __forceinline__ void hook_stream(const HookArgs& a) {
   constexpr int S = kHookSlow;
   const uint2* src;
@@ -900,7 +905,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
 #else
       u32 h[EPT], l[EPT];
       const u32 act =
-          resolve_edges<EPT, true, false, CAS, SH0>(a, links, tries, bits, s_sum, star, ed, h, l);
+          resolve_edges<EPT, true, false, CAS, FIXSH>(a, links, tries, bits, s_sum, star, ed, h, l);
       emit<EPT, APPEND>(a, wo, wl_out, cnt_out, lane, act, h, l);
 #endif
       continue;
@@ -1012,7 +1017,7 @@ __global__ void __launch_bounds__(kHookCta, HCC_HOOK_MINB) k_hook_seg_cas(HookAr
 // Worklist pass (CAS stores) with summary-predicated lookups.
 __global__ void __launch_bounds__(kHookCasCta, 1) k_hook_cas_sumd(HookArgs a) {
   if (a.gate == kGateIfSum && !__ldg(&a.ctrl->use_sum)) return;
-  hook_stream<kHookEPT, false, true, true, true, false, true>(a);
+  hook_stream<kHookEPT, false, true, true, true, false, kSumFixSh>(a);
 }
 
 __global__ void __launch_bounds__(kHookCasCta, 1) k_hook_cas_sumd_sh(HookArgs a) {
@@ -1022,7 +1027,7 @@ __global__ void __launch_bounds__(kHookCasCta, 1) k_hook_cas_sumd_sh(HookArgs a)
 
 // Adaptive / atomic segment hook with summary-predicated lookups.
 __global__ void __launch_bounds__(kHookCta, 1) k_hook_seg_cas_sumd(HookArgs a) {
-  hook_stream<kHookEPT, false, true, false, true, false, true>(a);
+  hook_stream<kHookEPT, false, true, false, true, false, 0>(a);
 }
 
 __global__ void __launch_bounds__(kHookCta, 1) k_hook_seg_cas_sumd_sh(HookArgs a) {
@@ -1036,7 +1041,7 @@ __global__ void __launch_bounds__(kHookCta, 1) k_hook_seg_cas_sumd_sh(HookArgs a
 __global__ void __launch_bounds__(kHookSumdCta, 1) k_hook_sumd(HookArgs a) {
   if (a.gate == kGateIfPlain && __ldg(&a.ctrl->use_sum)) return;
   if (a.gate == kGateIfSum && !__ldg(&a.ctrl->use_sum)) return;
-  hook_stream<kHookEPT, false, false, true, true, false, true>(a);
+  hook_stream<kHookEPT, false, false, true, true, false, kSumFixSh>(a);
 }
 
 // A coarser summary (n > 2^24: one bit per 2^shift words).
