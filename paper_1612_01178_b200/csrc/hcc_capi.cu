@@ -324,6 +324,9 @@ struct Plan {
   // (RMAT-24 1.474 vs 1.477 ms, ER and grid slightly slower: the pick's
   // dependent chases then extend the hook's tail instead of a node)
   bool fold_pick = false;
+  // HCC_SUMD_ANY=1: any streaming slot >= 2 (not only the one taking the
+  // remaining edges) runs k_hook_sumd when the summary covers its sample
+  bool sumd_any = false;
 };
 
 HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
@@ -620,10 +623,10 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
               k_step_adapt<<<1, 1024, 0, q.s()>>>(ctrl, recs, P.m, P.forming_pct,
                                                  vote ? c->s0f : nullptr, P.sum_words,
                                                  P.edges, c->s0b, rvote ? c->s0f : nullptr,
-                                                 P.sum_shift);
+                                                 P.sum_shift, P.sumd_any ? 1 : 0);
             else
               k_step_adapt<<<1, 1, 0, q.s()>>>(ctrl, recs, P.m, P.forming_pct, nullptr, 0,
-                                              nullptr, nullptr, nullptr, 0);
+                                              nullptr, nullptr, nullptr, 0, 0);
           } else
             k_step_segment<<<1, 1, 0, q.s()>>>(ctrl, recs, 0, 0);
         }
@@ -1185,6 +1188,7 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   if (const char* e = std::getenv("HCC_SUM_VOTE")) P.sum_vote = std::atoi(e) != 0;
   if (const char* e = std::getenv("HCC_WL_SUMD")) P.wl_sumd = std::atoi(e) != 0;
   if (const char* e = std::getenv("HCC_FOLD_PICK")) P.fold_pick = std::atoi(e) != 0;
+  if (const char* e = std::getenv("HCC_SUMD_ANY")) P.sumd_any = std::atoi(e) != 0;
   {
     const char* w = std::getenv("HCC_WALK");
     P.walk = w ? std::atoi(w) : kDefaultWalk;
@@ -1304,6 +1308,7 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   key.plan = key.plan * 3 + (P.sum_vote ? 1 : 0);
   key.plan = key.plan * 3 + (P.wl_sumd ? 1 : 0);
   key.plan = key.plan * 3 + (P.fold_pick ? 1 : 0);
+  key.plan = key.plan * 3 + (P.sumd_any ? 1 : 0);
   key.plan = key.plan * 1000003ull + P.sum_words * 64ull + P.sum_shift;
   key.plan = key.plan * 31 + (P.adapt ? 1000 + P.adapt_shift + 100000ull * P.forming_pct : 0);
   key.plan = key.plan * 1000003ull + P.adapt_first;

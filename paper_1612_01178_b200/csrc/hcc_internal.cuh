@@ -247,7 +247,7 @@ __global__ void k_step_segment(DevCtrl* ctrl, DevRec* recs,
                                cudaGraphConditionalHandle h, int use_cond);
 __global__ void k_step_adapt(DevCtrl* ctrl, DevRec* recs, u64 m, u32 forming_pct,
                              const u32* sum, u32 sum_words, const uint2* edges,
-                             const u32* bits, const u32* rsum, u32 rshift);
+                             const u32* bits, const u32* rsum, u32 rshift, int rany);
 __global__ void k_step_outer(DevCtrl* ctrl, DevRec* recs,
                              cudaGraphConditionalHandle h, int use_cond);
 __global__ void k_step_jump(DevCtrl* ctrl, cudaGraphConditionalHandle h,

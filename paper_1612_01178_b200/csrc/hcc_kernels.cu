@@ -1542,7 +1542,7 @@ __global__ void k_step_segment(DevCtrl* c, DevRec* recs,
 // store ratio (records are per segment).
 __global__ void k_step_adapt(DevCtrl* c, DevRec* recs, u64 m, u32 forming_pct,
                              const u32* sum, u32 sum_words, const uint2* edges,
-                             const u32* bits, const u32* rsum, u32 rshift) {
+                             const u32* bits, const u32* rsum, u32 rshift, int rany) {
   // Every thread derives the next range from the pass-start control words
   // (same addresses: broadcast reads), so the sample loads below issue
   // without waiting for thread 0's bookkeeping; thread 0 writes after the
@@ -1594,7 +1594,7 @@ __global__ void k_step_adapt(DevCtrl* c, DevRec* recs, u64 m, u32 forming_pct,
       const u32 gx = ed.x >> (5u + rshift), gy = ed.y >> (5u + rshift);
       const u32 cov = ((rsum[gx >> 5] >> (gx & 31u)) & 1u) + ((rsum[gy >> 5] >> (gy & 31u)) & 1u);
       const int n_cov = __syncthreads_count(cov == 2) * 2 + __syncthreads_count(cov == 1);
-      if (threadIdx.x == 0 && s_e == m)
+      if (threadIdx.x == 0 && (s_e == m || rany))
         c->use_sum = (u32)n_cov * 4 >= 2 * blockDim.x ? 1u : 0u;
     }
   }
