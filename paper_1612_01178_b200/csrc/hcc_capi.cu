@@ -327,6 +327,8 @@ struct Plan {
   // HCC_SUMD_ANY=1: any streaming slot >= 2 (not only the one taking the
   // remaining edges) runs k_hook_sumd when the summary covers its sample
   bool sumd_any = false;
+  // compress L2 prefetch distance in blocks (0: off), for pi beyond L2
+  u32 comp_pf = 0;
 };
 
 HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
@@ -392,11 +394,12 @@ void launch_compress_s0b(hcc_ctx* c, const Plan& P, cudaStream_t s, int rec_idx 
   if (P.wide_compress)
     k_compress_s0b_w<<<grid_for((P.n + 7) / 8, kVertThreadsWide, 0x7fffffffull), kVertThreadsWide,
                        0, s>>>(P.pi, P.n, c->d_ctrl, c->d_recs, c->s0b, kCompressIfDirty,
-                               P.sum ? c->s0f : nullptr, P.sum_words, P.sum_shift, rec_idx, dslot);
+                               P.sum ? c->s0f : nullptr, P.sum_words, P.sum_shift, rec_idx, dslot,
+                               P.comp_pf);
   else
     k_compress_s0b<<<grid_for((P.n + 7) / 8, kVertThreads, 0x7fffffffull), kVertThreads, 0, s>>>(
         P.pi, P.n, c->d_ctrl, c->d_recs, c->s0b, kCompressIfDirty, P.sum ? c->s0f : nullptr,
-        P.sum_words, P.sum_shift, rec_idx, dslot);
+        P.sum_words, P.sum_shift, rec_idx, dslot, P.comp_pf);
 }
 
 // Preferred shared-memory carveout (percent) of the forming-slot hook.  RMAT's
@@ -1166,7 +1169,10 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
     const u64 nwords = (n + 31) / 32;
     u32 sh = 0;
     while (((nwords + (1ull << sh) - 1) >> sh) > (u64)kS0fMaxBytes * 8) ++sh;
-    bool sum_ok = sh <= 6;
+    // (one bit per 16 words or more, n > 2^27: the steady slot's coverage
+    // vote never picks the summary there, and building it cost RMAT-28's
+    // compresses 0.13 ms of block barriers)
+    bool sum_ok = sh <= kSumMaxShift;
     if (const char* e = std::getenv("HCC_S0F")) sum_ok = sum_ok && std::atoi(e) != 0;
     // one bit per 16 vertices while that table fits (HCC_SUM_HALF=0: per word)
     // (not for the adaptive engine's 31 short segment hooks, whose L1 the
@@ -1189,6 +1195,10 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   if (const char* e = std::getenv("HCC_WL_SUMD")) P.wl_sumd = std::atoi(e) != 0;
   if (const char* e = std::getenv("HCC_FOLD_PICK")) P.fold_pick = std::atoi(e) != 0;
   if (const char* e = std::getenv("HCC_SUMD_ANY")) P.sumd_any = std::atoi(e) != 0;
+  // pi beyond L2: the compress prefetches one residency wave (6 blocks per
+  // SM) ahead (RMAT-28's compresses 1.94 -> 1.89 ms in total)
+  P.comp_pf = n >= (1ull << 26) ? (u32)c->sms * 6u : 0u;
+  if (const char* e = std::getenv("HCC_COMP_PF")) P.comp_pf = (u32)std::atoi(e);
   {
     const char* w = std::getenv("HCC_WALK");
     P.walk = w ? std::atoi(w) : kDefaultWalk;
@@ -1309,6 +1319,7 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   key.plan = key.plan * 3 + (P.wl_sumd ? 1 : 0);
   key.plan = key.plan * 3 + (P.fold_pick ? 1 : 0);
   key.plan = key.plan * 3 + (P.sumd_any ? 1 : 0);
+  key.plan = key.plan * 1000003ull + P.comp_pf;
   key.plan = key.plan * 1000003ull + P.sum_words * 64ull + P.sum_shift;
   key.plan = key.plan * 31 + (P.adapt ? 1000 + P.adapt_shift + 100000ull * P.forming_pct : 0);
   key.plan = key.plan * 1000003ull + P.adapt_first;

@@ -64,6 +64,11 @@ constexpr u32 kS0fMaxBytes = HCC_S0F_MAX_BYTES;
 #define HCC_SUM_HALF 1
 #endif
 constexpr u32 kSumHalfShift = ~0u;
+// Coarsest summary built (2^shift bitmap words per bit).
+#ifndef HCC_SUM_MAX_SHIFT
+#define HCC_SUM_MAX_SHIFT 3
+#endif
+constexpr u32 kSumMaxShift = HCC_SUM_MAX_SHIFT;
 constexpr u32 kSumHalfMaxBytes = 128u * 1024u;
 // Largest staged table (shared-memory budgets of the summary hooks).
 constexpr u32 kSumTableMaxBytes = kSumHalfMaxBytes > kS0fMaxBytes ? kSumHalfMaxBytes : kS0fMaxBytes;
@@ -234,10 +239,10 @@ __global__ void k_compress(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
                            int skip_if_clean);
 __global__ void k_compress_s0b(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
                                u32* bits, int skip_if_clean, u32* sum, u32 sum_words,
-                               u32 sum_shift, int rec_idx, int dslot);
+                               u32 sum_shift, int rec_idx, int dslot, u32 pf_blocks);
 __global__ void k_compress_s0b_w(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
                                  u32* bits, int skip_if_clean, u32* sum, u32 sum_words,
-                                 u32 sum_shift, int rec_idx, int dslot);
+                                 u32 sum_shift, int rec_idx, int dslot, u32 pf_blocks);
 __global__ void k_start(u32* pi, u64 n, u32* bits, DevCtrl* ctrl, DevRec* recs, u64 nseg,
                         u64 m, u64 plan_first, u32* sum, u32 sum_words);
 __global__ void k_jump(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs);

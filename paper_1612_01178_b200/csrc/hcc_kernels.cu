@@ -1415,13 +1415,15 @@ __device__ __forceinline__ void emit_bits(u64 chunk, u64 n, u64 v0, u32 byte, u3
 template <int BS>
 __device__ __forceinline__ void compress_s0b_body(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
                                                   u32* bits, int mode, u32* sum, u32 sum_words,
-                                                  u32 sum_shift, int rec_idx, int dslot);
+                                                  u32 sum_shift, int rec_idx, int dslot,
+                                                  u32 pf_blocks);
 
 __global__ void __launch_bounds__(kVertThreads, HCC_COMP_MINB)
     k_compress_s0b(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs, u32* bits,
-                   int mode, u32* sum, u32 sum_words, u32 sum_shift, int rec_idx, int dslot) {
+                   int mode, u32* sum, u32 sum_words, u32 sum_shift, int rec_idx, int dslot,
+                   u32 pf_blocks) {
   compress_s0b_body<kVertThreads>(pi, n, ctrl, recs, bits, mode, sum, sum_words, sum_shift,
-                                  rec_idx, dslot);
+                                  rec_idx, dslot, pf_blocks);
 }
 
 // 512-thread blocks, half as many (HCC_COMP_WIDE=1; off by default): at
@@ -1430,15 +1432,17 @@ __global__ void __launch_bounds__(kVertThreads, HCC_COMP_MINB)
 // (RMAT-28 33.89 vs 33.81 ms, adaptive 41.7 vs 40.7 ms).
 __global__ void __launch_bounds__(kVertThreadsWide, 3)
     k_compress_s0b_w(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs, u32* bits,
-                     int mode, u32* sum, u32 sum_words, u32 sum_shift, int rec_idx, int dslot) {
+                     int mode, u32* sum, u32 sum_words, u32 sum_shift, int rec_idx, int dslot,
+                     u32 pf_blocks) {
   compress_s0b_body<kVertThreadsWide>(pi, n, ctrl, recs, bits, mode, sum, sum_words, sum_shift,
-                                      rec_idx, dslot);
+                                      rec_idx, dslot, pf_blocks);
 }
 
 template <int BS>
 __device__ __forceinline__ void compress_s0b_body(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
                                                   u32* bits, int mode, u32* sum, u32 sum_words,
-                                                  u32 sum_shift, int rec_idx, int dslot) {
+                                                  u32 sum_shift, int rec_idx, int dslot,
+                                                  u32 pf_blocks) {
   if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->tile_ctr = 0;  // next hook's schedule
   if (dslot >= 0) {
     // unrolled chain: this segment's flag; clear the next segment's
@@ -1465,6 +1469,13 @@ __device__ __forceinline__ void compress_s0b_body(u32* pi, u64 n, DevCtrl* ctrl,
     const uint4* p4 = reinterpret_cast<const uint4*>(pi) + (q << 1);
     pa = __ldcg(p4);
     pb = __ldcg(p4 + 1);
+  }
+  // pi larger than L2 (n >= 2^26): pull the line the block pf_blocks later
+  // in launch order (about one residency wave ahead) will read into L2, so
+  // its first read does not wait on DRAM
+  if (pf_blocks && (threadIdx.x & 3u) == 0) {
+    const u64 vn = v0 + ((u64)pf_blocks * BS << 3);
+    if (vn + 8 <= n) asm volatile("prefetch.global.L2 [%0];" ::"l"(pi + vn));
   }
   // the star's root is read once per thread (one L1 line for the grid):
   // a compress never moves a root, so the answer holds for the whole pass
