@@ -329,6 +329,8 @@ struct Plan {
   bool sumd_any = false;
   // compress L2 prefetch distance in blocks (0: off), for pi beyond L2
   u32 comp_pf = 0;
+  // sixteen vertices per compress thread (k_compress_s0b16; HCC_COMP16)
+  bool comp16 = false;
 };
 
 HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
@@ -387,11 +389,23 @@ bool slot_small(const Plan& P, u64 sgi) {
          seg_edges < (u64)P.grid_hook * P.block_hook * kHookEPT * 2;
 }
 
+// Sixteen vertices per compress thread (k_compress_s0b16): measured RMAT-24
+// 1.377 -> 1.381 ms, adaptive 2.659 -> 2.674, ER equal, RMAT-28 -0.06 ms,
+// grid's adaptive engine 1.08 -> 0.855 ms (its row chains resolve in the
+// thread's second half).  Off by default; HCC_COMP16=1.
+#ifndef HCC_COMP16
+#define HCC_COMP16 0
+#endif
 // Star-bitmap compress over the full grid (a persistent grid with cp.async
 // prefetch was slower: DESIGN.md §3.2).
 void launch_compress_s0b(hcc_ctx* c, const Plan& P, cudaStream_t s, int rec_idx = -1,
                          int dslot = -1) {
-  if (P.wide_compress)
+  if (P.comp16 && (!P.sum || P.sum_shift == kSumHalfShift || P.sum_shift == 0))
+    k_compress_s0b16<<<grid_for((P.n + 15) / 16, kVertThreads, 0x7fffffffull), kVertThreads, 0,
+                       s>>>(P.pi, P.n, c->d_ctrl, c->d_recs, c->s0b, kCompressIfDirty,
+                            P.sum ? c->s0f : nullptr, P.sum_words, P.sum_shift, rec_idx, dslot,
+                            P.comp_pf ? P.comp_pf / 2 : 0u);
+  else if (P.wide_compress)
     k_compress_s0b_w<<<grid_for((P.n + 7) / 8, kVertThreadsWide, 0x7fffffffull), kVertThreadsWide,
                        0, s>>>(P.pi, P.n, c->d_ctrl, c->d_recs, c->s0b, kCompressIfDirty,
                                P.sum ? c->s0f : nullptr, P.sum_words, P.sum_shift, rec_idx, dslot,
@@ -1199,6 +1213,8 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   // SM) ahead (RMAT-28's compresses 1.94 -> 1.89 ms in total)
   P.comp_pf = n >= (1ull << 26) ? (u32)c->sms * 6u : 0u;
   if (const char* e = std::getenv("HCC_COMP_PF")) P.comp_pf = (u32)std::atoi(e);
+  P.comp16 = HCC_COMP16 != 0;
+  if (const char* e = std::getenv("HCC_COMP16")) P.comp16 = std::atoi(e) != 0;
   {
     const char* w = std::getenv("HCC_WALK");
     P.walk = w ? std::atoi(w) : kDefaultWalk;
@@ -1320,6 +1336,7 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   key.plan = key.plan * 3 + (P.fold_pick ? 1 : 0);
   key.plan = key.plan * 3 + (P.sumd_any ? 1 : 0);
   key.plan = key.plan * 1000003ull + P.comp_pf;
+  key.plan = key.plan * 3 + (P.comp16 ? 1 : 0);
   key.plan = key.plan * 1000003ull + P.sum_words * 64ull + P.sum_shift;
   key.plan = key.plan * 31 + (P.adapt ? 1000 + P.adapt_shift + 100000ull * P.forming_pct : 0);
   key.plan = key.plan * 1000003ull + P.adapt_first;

@@ -240,6 +240,9 @@ __global__ void k_compress(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
 __global__ void k_compress_s0b(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
                                u32* bits, int skip_if_clean, u32* sum, u32 sum_words,
                                u32 sum_shift, int rec_idx, int dslot, u32 pf_blocks);
+__global__ void k_compress_s0b16(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
+                                 u32* bits, int skip_if_clean, u32* sum, u32 sum_words,
+                                 u32 sum_shift, int rec_idx, int dslot, u32 pf_blocks);
 __global__ void k_compress_s0b_w(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs,
                                  u32* bits, int skip_if_clean, u32* sum, u32 sum_words,
                                  u32 sum_shift, int rec_idx, int dslot, u32 pf_blocks);

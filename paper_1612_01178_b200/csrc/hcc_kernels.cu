@@ -1487,6 +1487,92 @@ __device__ __forceinline__ void compress_s0b_body(u32* pi, u64 n, DevCtrl* ctrl,
   block_t1(&r->comp_t1);
 }
 
+// Sixteen vertices per thread (four 16-byte reads in flight): the control
+// reads, index math and bitmap emission are paid once per 16 vertices, and
+// a settled group of 16 (the common case once the giant is a star) is one
+// compare chain.  Otherwise the two halves run compress8 one after the
+// other (the second sees the first's writes).  Serves the star summaries
+// whose bits map onto a warp without block merging: none, one bit per word,
+// one bit per 16 vertices.
+__device__ __forceinline__ void emit_bits16(u64 q, u64 n, u64 v0, u32 b16, u32* bits, u32* sum,
+                                            u32 sum_words, u32 sum_shift) {
+  const u32 lane = threadIdx.x & 31u;
+  u32 w = b16 << (16u * (lane & 1u));
+  w |= __shfl_xor_sync(0xffffffffu, w, 1);
+  if ((lane & 1u) == 0 && v0 < n) bits[v0 >> 5] = w;
+  if (!sum) return;
+  if (sum_shift == kSumHalfShift) {
+    // one bit per 16 vertices = one bit per thread: a warp is one word
+    const u32 ball = __ballot_sync(0xffffffffu, v0 < n && b16 == 0xffffu);
+    if (lane == 0 && (q >> 5) < sum_words) sum[q >> 5] = ball;
+    return;
+  }
+  // one bit per word (two lanes): a warp's 16 words are one halfword
+  u32 x = __ballot_sync(0xffffffffu, (lane & 1u) == 0 && v0 < n && w == ~0u) & 0x55555555u;
+  x = (x | (x >> 1)) & 0x33333333u;
+  x = (x | (x >> 2)) & 0x0f0f0f0fu;
+  x = (x | (x >> 4)) & 0x00ff00ffu;
+  x = (x | (x >> 8)) & 0x0000ffffu;
+  if (lane == 0 && (q >> 5) < (u64)sum_words * 2)
+    reinterpret_cast<unsigned short*>(sum)[q >> 5] = (unsigned short)x;
+}
+
+#ifndef HCC_COMP16_MINB
+#define HCC_COMP16_MINB 4
+#endif
+__global__ void __launch_bounds__(kVertThreads, HCC_COMP16_MINB)
+    k_compress_s0b16(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs, u32* bits, int mode, u32* sum,
+                     u32 sum_words, u32 sum_shift, int rec_idx, int dslot, u32 pf_blocks) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->tile_ctr = 0;  // next hook's schedule
+  if (dslot >= 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->dirtyp[dslot ^ 1] = 0;
+    if (mode && __ldg(&ctrl->dirtyp[dslot]) == 0) return;
+  } else if (mode && __ldg(&ctrl->dirty) == 0) {
+    return;
+  }
+  DevRec* r = rec_of(ctrl, recs, rec_idx);
+  block_t0(&r->comp_t0);
+  u64 steps = 0;
+  const u32 star = __ldg(&ctrl->star);
+  const u64 q = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 v0 = q << 4;
+  const bool whole = v0 + 16 <= n;
+  uint4 pa = make_uint4(0u, 0u, 0u, 0u), pb = pa, pc = pa, pd = pa;
+  if (whole) {
+    const uint4* p4 = reinterpret_cast<const uint4*>(pi) + (q << 2);
+    pa = __ldcg(p4);
+    pb = __ldcg(p4 + 1);
+    pc = __ldcg(p4 + 2);
+    pd = __ldcg(p4 + 3);
+  }
+  if (pf_blocks && (threadIdx.x & 1u) == 0) {
+    const u64 vn = v0 + ((u64)pf_blocks * kVertThreads << 4);
+    if (vn + 16 <= n) asm volatile("prefetch.global.L2 [%0];" ::"l"(pi + vn));
+  }
+  const bool star_root = star < n && ld_pi(pi + star) == star;
+  u32 b16 = 0;
+  bool done = false;
+  if (whole && star_root) {
+    const u32 a[16] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w,
+                       pc.x, pc.y, pc.z, pc.w, pd.x, pd.y, pd.z, pd.w};
+    u32 settled = 1;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      settled &= (a[j] == (u32)v0 + j) | (a[j] == star);
+      b16 |= (u32)(a[j] == star) << j;
+    }
+    done = settled != 0;
+  }
+  if (!done) {
+    const u32 lo = compress8(pi, n, v0, v0 + 8 <= n, pa, pb, star, star_root, steps);
+    const u32 hi = compress8(pi, n, v0 + 8, whole, pc, pd, star, star_root, steps);
+    b16 = lo | (hi << 8);
+  }
+  emit_bits16(q, n, v0, b16, bits, sum, sum_words, sum_shift);
+  add_counter(&r->jump_stripe[blockIdx.x & (kJumpStripes - 1)], steps);
+  block_t1(&r->comp_t1);
+}
+
 // Single-level jump pass (forest.hpp:93-99) with a device change flag.
 __global__ void __launch_bounds__(kVertThreads)
     k_jump(u32* pi, u64 n, DevCtrl* ctrl, DevRec* recs) {
