@@ -522,8 +522,32 @@ __device__ __forceinline__ u32 resolve_edges(const HookArgs& a, u32& links, u32&
 }
 
 // Copy the star-0 summary into shared memory (swizzled rows).
+// 16-byte reads, eight in flight per thread before their stores: a
+// one-word load-store loop waited an L2 round trip per word (~5 us per
+// launch for the 64 KB table, 12% of the stall samples of an adaptive
+// segment hook).
+__device__ __forceinline__ void store_summary4(u32* s_sum, u32 j, uint4 v) {
+  // j is a multiple of 4: the four words share one padded row
+  const u32 p = sum_swz(j);
+  s_sum[p] = v.x;
+  s_sum[p + 1] = v.y;
+  s_sum[p + 2] = v.z;
+  s_sum[p + 3] = v.w;
+}
+
 __device__ __forceinline__ void load_summary(const HookArgs& a, u32* s_sum) {
-  for (u32 i = threadIdx.x; i < a.s0f_words; i += blockDim.x) s_sum[sum_swz(i)] = a.s0f[i];
+  const u32 w = a.s0f_words, n16 = w >> 2, bd = blockDim.x;
+  const uint4* src = reinterpret_cast<const uint4*>(a.s0f);
+  u32 i = threadIdx.x;
+  for (; i + 7 * bd < n16; i += 8 * bd) {
+    uint4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldcg(src + i + k * bd);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) store_summary4(s_sum, (i + k * bd) << 2, v[k]);
+  }
+  for (; i < n16; i += bd) store_summary4(s_sum, i << 2, __ldcg(src + i));
+  for (u32 j = (n16 << 2) + threadIdx.x; j < w; j += bd) s_sum[sum_swz(j)] = __ldcg(a.s0f + j);
   __syncthreads();
 }
 
