@@ -125,10 +125,10 @@ void ensure_merge(hcc_ctx* c, u64 n, u64 cap) {
 
 // Shard r: export its forest into its merge buffers (stream-ordered after
 // its local CC) and record the export event the peers wait on.
-void enqueue_export(hcc_ctx* sc, MergeShard& ms, const hcc_forest* f) {
+void enqueue_export(hcc_ctx* sc, MergeShard& ms, const hcc_forest* f, bool peers) {
   HCC_CUDA(cudaMemsetAsync(ms.cnt, 0, sizeof(u64), sc->stream));
   const u64 nwords = (f->n + 31) / 32;
-  if (f->n)
+  if (f->n && peers)  // (one shard: nobody reads it, the merge is the identity)
     k_export<<<grid_for(nwords * 32, 256, (u64)sc->sms * 32), 256, 0, sc->stream>>>(
         f->d_pi, f->n, ms.bits, ms.pairs, ms.cap, ms.cnt);
   HCC_CUDA(cudaGetLastError());
@@ -147,11 +147,13 @@ void merge_shard(hcc_ctx* c, int r, hcc_forest* f, u64 records_cap) {
   ensure_wl(sc, records_cap);
   HCC_CUDA(cudaEventRecord(ms.ev_m0, sc->stream));
   k_begin<<<1, 1, 0, sc->stream>>>(sc->d_ctrl, sc->d_recs, 1);
-  k_merge_gather<<<std::max<unsigned>(1u, (unsigned)sc->sms * 8u), 256, 0, sc->stream>>>(
-      ms.tab, (u32)r, f->d_pi, n, sc->wl[0], &sc->d_ctrl->wl_count[0], sc->wl_cap,
-      &sc->d_ctrl->err, &sc->d_ctrl->dirty, &sc->d_ctrl->merged_links);
-  HCC_CUDA(cudaGetLastError());
-  enqueue_rehook(sc, f->d_pi, n);
+  if (G > 1) {
+    k_merge_gather<<<std::max<unsigned>(1u, (unsigned)sc->sms * 8u), 256, 0, sc->stream>>>(
+        ms.tab, (u32)r, f->d_pi, n, sc->wl[0], &sc->d_ctrl->wl_count[0], sc->wl_cap,
+        &sc->d_ctrl->err, &sc->d_ctrl->dirty, &sc->d_ctrl->merged_links);
+    HCC_CUDA(cudaGetLastError());
+    enqueue_rehook(sc, f->d_pi, n);
+  }
   HCC_CUDA(cudaEventRecord(ms.ev_t1, sc->stream));
   // components (metrics only, after the timed region)
   if (r == 0)
@@ -335,7 +337,7 @@ int multi_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o_in, hcc_forest* f
     HCC_CUDA(cudaEventRecord(ms.ev_t0, sc->stream));
     if (int st = run_cc_sized(sc, g->shards[r], &o, forest_of(r), &lm[r])) return st;
     ms.local_ms = lm[r].total_ms;
-    enqueue_export(sc, ms, forest_of(r));
+    enqueue_export(sc, ms, forest_of(r), G > 1);
     return HCC_OK;
   });
   // 2. merge; repeated (export + merge) while some pair list overflowed
@@ -375,7 +377,7 @@ int multi_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o_in, hcc_forest* f
     rc = for_shards(G, [&](int r) -> int {
       HCC_CUDA(cudaSetDevice(c->subs[r]->dev));
       HCC_CUDA(cudaEventRecord(c->merge[r].ev_t0, c->subs[r]->stream));
-      enqueue_export(c->subs[r], c->merge[r], forest_of(r));
+      enqueue_export(c->subs[r], c->merge[r], forest_of(r), G > 1);
       return HCC_OK;
     });
   }

@@ -173,7 +173,9 @@ int hcc_peer_export(hcc_ctx* c, hcc_forest* f) {
   HCC_GUARD_BEGIN
   HCC_CUDA(cudaEventRecord(p->ev_m0, c->stream));
   HCC_CUDA(cudaMemsetAsync(p->cnt, 0, sizeof(u64), c->stream));
-  if (f->n)
+  // (a world of one has no peer to read the export: the merge is the
+  // identity)
+  if (f->n && p->world > 1)
     k_export<<<grid_for(p->nwords * 32, 256, (u64)c->sms * 32), 256, 0, c->stream>>>(
         f->d_pi, f->n, p->bits, p->pairs, p->cap, p->cnt);
   HCC_CUDA(cudaGetLastError());
@@ -194,15 +196,17 @@ int hcc_peer_merge(hcc_ctx* c, hcc_forest* f, hcc_metrics* mx, int* overflow) {
   const u64 n = f->n;
   for (int r = 0; r < p->world; ++r)
     if (r != p->rank) HCC_CUDA(cudaStreamWaitEvent(c->stream, p->peer_ev[r], 0));
-  u64 pairs_total = 0;
-  for (const PeerBlob& b : p->blobs) pairs_total += b.cap;
-  ensure_wl(c, n + pairs_total + 1);
   k_begin<<<1, 1, 0, c->stream>>>(c->d_ctrl, c->d_recs, 1);
-  k_merge_gather<<<std::max<unsigned>(1u, (unsigned)c->sms * 8u), 256, 0, c->stream>>>(
-      p->d_tab, (u32)p->rank, f->d_pi, n, c->wl[0], &c->d_ctrl->wl_count[0], c->wl_cap,
-      &c->d_ctrl->err, &c->d_ctrl->dirty, &c->d_ctrl->merged_links);
-  HCC_CUDA(cudaGetLastError());
-  enqueue_rehook(c, f->d_pi, n);
+  if (p->world > 1) {
+    u64 pairs_total = 0;
+    for (const PeerBlob& b : p->blobs) pairs_total += b.cap;
+    ensure_wl(c, n + pairs_total + 1);
+    k_merge_gather<<<std::max<unsigned>(1u, (unsigned)c->sms * 8u), 256, 0, c->stream>>>(
+        p->d_tab, (u32)p->rank, f->d_pi, n, c->wl[0], &c->d_ctrl->wl_count[0], c->wl_cap,
+        &c->d_ctrl->err, &c->d_ctrl->dirty, &c->d_ctrl->merged_links);
+    HCC_CUDA(cudaGetLastError());
+    enqueue_rehook(c, f->d_pi, n);
+  }
   HCC_CUDA(cudaEventRecord(p->ev_m1, c->stream));
   // components (metrics only, after the timed region)
   k_count_roots<<<grid_for(n, 256, (u64)c->sms * 16), 256, 0, c->stream>>>(f->d_pi, n,
