@@ -396,6 +396,10 @@ bool slot_small(const Plan& P, u64 sgi) {
 #ifndef HCC_COMP16
 #define HCC_COMP16 0
 #endif
+#ifndef HCC_S0B_MIN_LOG2
+#define HCC_S0B_MIN_LOG2 20
+#endif
+constexpr u32 kS0bMinLog2 = HCC_S0B_MIN_LOG2;
 // Star-bitmap compress over the full grid (a persistent grid with cp.async
 // prefetch was slower: DESIGN.md §3.2).
 void launch_compress_s0b(hcc_ctx* c, const Plan& P, cudaStream_t s, int rec_idx = -1,
@@ -1145,7 +1149,15 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   bool cas_stream = (o->algo == HCC_ALGO_ADAPTIVE || o->algo == HCC_ALGO_ATOMIC) &&
                     o->max_threads == 0 && n >= (1ull << 16);
   if (const char* e = std::getenv("HCC_CAS_STREAM")) cas_stream = cas_stream && std::atoi(e) != 0;
-  bool s0b = (uses_wl || cas_stream) && o->max_threads == 0 && n >= (1ull << 16);
+  // The worklist engine's star bitmap from n = 2^20 (HCC_S0B_MIN_LOG2):
+  // below, its compress and sampling steps cost more than the lookups save
+  // (RMAT-16 0.120 -> 0.101 ms without it, RMAT-18 0.19 -> 0.17, grid 512^2
+  // 0.20 -> 0.13; RMAT-20 and ER 2^20 still gain from it).  The adaptive
+  // chain always keeps it.
+  u32 s0b_min_log2 = kS0bMinLog2;
+  if (const char* e = std::getenv("HCC_S0B_MIN_LOG2")) s0b_min_log2 = (u32)std::atoi(e);
+  bool s0b = ((uses_wl && s0b_min_log2 < 64 && n >= (1ull << s0b_min_log2)) || cas_stream) &&
+             o->max_threads == 0 && n >= (1ull << 16);
   if (const char* e = std::getenv("HCC_S0B")) s0b = s0b && std::atoi(e) != 0;
 
   Plan P;

@@ -468,14 +468,15 @@ def test_star0_bitmap_paths(ctx, oracle, spec):
     g = ctx.generate(spec)
     want = oracle.cc(g.n, g.edges())
     for s0b, walk in [("1", "32"), ("0", "32"), ("1", "2"), ("1", "1"), ("0", "1")]:
-        os.environ.update(HCC_S0B=s0b, HCC_WALK=walk)
+        # (HCC_S0B_MIN_LOG2: the bitmap below its default n = 2^20 floor too)
+        os.environ.update(HCC_S0B=s0b, HCC_WALK=walk, HCC_S0B_MIN_LOG2="16")
         try:
             for fps in [0, 1, 3]:
                 lab, mx = ctx.cc(g, "baseline-mj", first_pass_segments=fps)
                 assert np.array_equal(lab, want), (spec, s0b, walk, fps)
                 assert mx["star0_bitmap"] == (s0b == "1")
         finally:
-            for k in ("HCC_S0B", "HCC_WALK"):
+            for k in ("HCC_S0B", "HCC_WALK", "HCC_S0B_MIN_LOG2"):
                 os.environ.pop(k, None)
 
 
@@ -493,12 +494,17 @@ def test_degenerate_graphs_with_star_machinery(ctx, oracle):
         "path_rev": np.stack([np.arange(n - 1, 0, -1, dtype=np.uint64),
                               np.arange(n - 2, -1, -1, dtype=np.uint64)], axis=1),
     }
-    for name, e in cases.items():
-        want = oracle.cc(n, e)
-        for algo in ALGOS:
-            lab, mx = run(ctx, n, e, algo)
-            assert np.array_equal(lab, want.astype(np.uint64)), (name, algo)
-            assert mx["components"] == int(np.sum(want == np.arange(n, dtype=np.uint32)))
+    import os
+    os.environ["HCC_S0B_MIN_LOG2"] = "16"  # (the worklist engine's bitmap too)
+    try:
+        for name, e in cases.items():
+            want = oracle.cc(n, e)
+            for algo in ALGOS:
+                lab, mx = run(ctx, n, e, algo)
+                assert np.array_equal(lab, want.astype(np.uint64)), (name, algo)
+                assert mx["components"] == int(np.sum(want == np.arange(n, dtype=np.uint32)))
+    finally:
+        os.environ.pop("HCC_S0B_MIN_LOG2", None)
 
 
 @pytest.mark.parametrize("shift", [1, 977])
@@ -631,7 +637,12 @@ def test_stale_star_after_a_slot_without_stores(ctx, oracle):
     want = oracle.cc(n, e)
     assert want[1] == 0 and want[first + 1] == 0
     g = ctx.graph_from_edges(e, n)
-    lab, mx = ctx.cc(g, "baseline-mj")
+    import os
+    os.environ["HCC_S0B_MIN_LOG2"] = "16"  # the bitmap at this size too
+    try:
+        lab, mx = ctx.cc(g, "baseline-mj")
+    finally:
+        os.environ.pop("HCC_S0B_MIN_LOG2", None)
     assert mx["star0_bitmap"]
     assert np.array_equal(lab, want)
     g.close()
@@ -647,10 +658,16 @@ def test_graph_cache_survives_buffer_regrowth(ctx, oracle):
     gb = ctx.generate("erx:n=2097152,m=4194304,seed=5")   # n = 2^21, m = 2^22
     wa = oracle.cc(ga.n, ga.edges())
     wb = oracle.cc(gb.n, gb.edges())
-    for _ in range(3):
-        for g, w in ((ga, wa), (gb, wb)):
-            lab, _ = ctx.cc(g, "baseline-mj")
-            assert np.array_equal(lab, w)
+    import os
+    os.environ["HCC_S0B_MIN_LOG2"] = "16"  # both graphs on the bitmap
+    try:
+        for _ in range(3):
+            for g, w in ((ga, wa), (gb, wb)):
+                lab, mx = ctx.cc(g, "baseline-mj")
+                assert np.array_equal(lab, w)
+                assert mx["star0_bitmap"]
+    finally:
+        os.environ.pop("HCC_S0B_MIN_LOG2", None)
     ga.close()
     gb.close()
 
