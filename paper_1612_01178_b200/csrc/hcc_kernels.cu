@@ -1368,18 +1368,18 @@ __device__ __forceinline__ void emit_bits(u64 chunk, u64 n, u64 v0, u32 byte, u3
   if ((lane & 3u) == 0 && v0 < n) bits[v0 >> 5] = w;
   if (!sum) return;
   if (sum_shift == kSumHalfShift) {
-    // one bit per 16 vertices: word j of the warp (lanes 4j..4j+3) gives
-    // bits 2j (low half all in the star) and 2j + 1 (high half); a warp's
-    // 8 words are one 16-bit summary halfword
-    const u32 h2 = ((lane & 3u) == 0 && v0 < n)
-                       ? (((w & 0xffffu) == 0xffffu) ? 1u : 0u) | ((w >> 16) == 0xffffu ? 2u : 0u)
-                       : 0u;
-    u32 b16 = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) b16 |= __shfl_sync(0xffffffffu, h2, 4 * j) << (2 * j);
+    // one bit per 16 vertices = two neighbouring threads' bytes all in the
+    // star: one ballot, then the pairs' bits packed into the warp's 16-bit
+    // summary halfword (was eight shuffles)
+    const u32 f8 = __ballot_sync(0xffffffffu, v0 < n && byte == 0xffu);
+    u32 x = f8 & (f8 >> 1) & 0x55555555u;
+    x = (x | (x >> 1)) & 0x33333333u;
+    x = (x | (x >> 2)) & 0x0f0f0f0fu;
+    x = (x | (x >> 4)) & 0x00ff00ffu;
+    x = (x | (x >> 8)) & 0x0000ffffu;
     const u64 hw_idx = (chunk * blockDim.x + threadIdx.x) >> 5;
     if (lane == 0 && hw_idx < (u64)sum_words * 2)
-      reinterpret_cast<unsigned short*>(sum)[hw_idx] = (unsigned short)b16;
+      reinterpret_cast<unsigned short*>(sum)[hw_idx] = (unsigned short)x;
     return;
   }
   // Star-0 summary: this chunk's 64 words -> 64 >> sum_shift bits (bit =
