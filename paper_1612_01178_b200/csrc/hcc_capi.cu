@@ -948,7 +948,14 @@ void rehook_loop(hcc_ctx* c, const Plan& P) {
   DevCtrl* ctrl = c->d_ctrl;
   DevRec* recs = c->d_recs;
   q.loop([&](cudaGraphConditionalHandle h, int u) {
-    launch_hook(P, q.s(), hook_args(c, P, kSrcWorklist, 1));
+    // CAS stores and unbounded walks: no link is lost, so nothing is
+    // re-recorded and one pass (plus the compress) converges (the plain
+    // hook took a second pass and compress: 0.23 ms per merge at n = 2^28)
+    HookArgs a = hook_args(c, P, kSrcWorklist, 1);
+    a.cas = 1;
+    a.chunked = 1;
+    a.walk = kUnboundedWalk;
+    k_hook_cas<<<(unsigned)(c->sms * c->occ_hook_cas), kHookCasCta, 0, q.s()>>>(a);
     k_compress<<<P.grid_vert, P.block_vert, 0, q.s()>>>(P.pi, P.n, ctrl, recs, 1);
     k_step_worklist<<<1, 1, 0, q.s()>>>(ctrl, recs, h, u);
   });

@@ -116,9 +116,14 @@ __global__ void k_merge_gather(const PeerTab* tab, u32 self, u32* pi, u64 n, uin
   // 128-byte read per peer), then the warp decodes the words one by one
   for (u64 w0 = gwarp * 32; w0 < nwords; w0 += warps * 32) {
     u32 x = 0;
-    if (w0 + lane < nwords)
+    if (w0 + lane < nwords) {
       for (u32 r = 0; r < np; ++r)
         if (r != self) x |= __ldcg(tab->bits[r] + w0 + lane);
+      // vertices already in this rank's star of 0 (its own exported row)
+      // need nothing: their pi is not even read (at 8 GPUs on RMAT-28 about
+      // half of the peers' star members)
+      x &= ~__ldcg(tab->bits[self] + w0 + lane);
+    }
     // Every set bit is a vertex of the global star of 0.  The local forest
     // is a set of stars (a converged local CC, or the end of a re-hook
     // pass), so pi(v) is v's root: link that root to 0 in place (every

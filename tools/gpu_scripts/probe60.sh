@@ -1,0 +1,3 @@
+python tools/ncu_target_multi.py rmatx:scale=28,ef=16,seed=1 8 2
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/p60_multi8.csv python tools/ncu_target_multi.py rmatx:scale=28,ef=16,seed=1 8 1 > /dev/null 2>&1
+echo done
