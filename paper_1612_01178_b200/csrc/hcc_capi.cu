@@ -1080,6 +1080,7 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   bool adapt = false;
   u32 adapt_shift = kAdaptShift;
   u64 adapt_first = 0;
+  u32 adapt_growth = kAdaptGrowth;
   if (geo_plan) {
     const char* pe = std::getenv("HCC_PLAN");
     int sh = 0;
@@ -1109,8 +1110,11 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
       adapt_first = first;
       u64 len = first, covered = first;
       nseg = 1;
+      u32 growth = kAdaptGrowth;
+      if (const char* e2 = std::getenv("HCC_ADAPT_GROWTH")) growth = (u32)std::max(2, std::atoi(e2));
+      adapt_growth = growth;
       while (covered < m && nseg < (u64)slots) {
-        len = std::min<u64>(len * kAdaptGrowth, m - covered);
+        len = std::min<u64>(len * growth, m - covered);
         covered += len;
         ++nseg;
       }
@@ -1121,7 +1125,7 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
       for (u64 i = 0; i < nseg; ++i) {
         bounds[i] = b;
         b = std::min<u64>(m, b + l);
-        l *= kAdaptGrowth;
+        l *= growth;
       }
       bounds[nseg] = m;
       if (nseg >= 2) bounds[nseg - 1] = std::min(bounds[nseg - 1], m);
@@ -1192,6 +1196,8 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   if (const char* e = std::getenv("HCC_SUMD")) P.sumd = std::atoi(e);
   P.forming_pct = std::getenv("HCC_FORMING_PCT") ? (u32)std::atoi(std::getenv("HCC_FORMING_PCT"))
                                                   : kAdaptFormingPct;
+  P.forming_pct = (P.forming_pct & 0xffu) |
+                  (adapt_growth != kAdaptGrowth ? (adapt_growth & 0xffu) << 8 : 0u);
   if (P.s0b) {
     ensure_s0b(c, (n + 31) / 32);
   }

@@ -1672,8 +1672,10 @@ __global__ void k_step_adapt(DevCtrl* c, DevRec* recs, u64 m, u32 forming_pct,
   const u64 r_in = recs[ri].edges_in, r_out = recs[ri].edges_out;
   const u64 seg = c->seg, nseg = c->nseg, old_b = c->seg_b, old_e = c->seg_e;
   const u64 len = old_e - old_b;
-  const bool forming = r_in > 0 && r_out * 100 > r_in * forming_pct;
-  u64 next = forming ? len * kAdaptGrowth : m;
+  // (forming_pct bits 8-15: the growth factor, 0 = kAdaptGrowth)
+  const u32 growth = (forming_pct >> 8) & 0xffu ? (forming_pct >> 8) & 0xffu : kAdaptGrowth;
+  const bool forming = r_in > 0 && r_out * 100 > r_in * (forming_pct & 0xffu);
+  u64 next = forming ? len * growth : m;
   if (next < 1) next = 1;
   if (seg + 2 >= nseg) next = m;  // the next slot is the last one
   const u64 s_b = old_e;
