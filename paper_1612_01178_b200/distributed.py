@@ -219,6 +219,11 @@ class CudaBackend:
         return self.forest.snapshot()
 
 
+class PeerUnavailable(RuntimeError):
+    """The CUDA-IPC transport cannot be set up on every rank (raised on all
+    ranks together)."""
+
+
 class PeerMerge:
     """Merge over CUDA IPC (hcc_peer_*): k_merge_gather reads the peers'
     export arenas in place over NVLink.  Host traffic per run: one barrier
@@ -243,10 +248,30 @@ class PeerMerge:
         self._connect()
 
     def _connect(self):
-        blob = self.ctx.peer_open(self.n, self.cap, self.rank, self.world)
+        # Every step is collective, so a rank that cannot open or map an
+        # arena (no CUDA IPC between the processes, no peer access) makes all
+        # ranks raise PeerUnavailable together instead of leaving the others
+        # blocked in a collective: the caller can fall back to NCCL.
+        err = ""
+        try:
+            blob = self.ctx.peer_open(self.n, self.cap, self.rank, self.world)
+        except Exception as exc:  # noqa: BLE001 (any failure: same protocol)
+            blob, err = b"", f"rank {self.rank}: {exc}"
         blobs = [None] * self.world
         self.dist.all_gather_object(blobs, blob, group=self.group)
-        self.ctx.peer_connect(b"".join(blobs))
+        if not all(blobs):
+            if blob:
+                self.ctx.peer_close()
+            raise PeerUnavailable(err or "a peer could not open its export arena")
+        try:
+            self.ctx.peer_connect(b"".join(blobs))
+        except Exception as exc:  # noqa: BLE001
+            err = f"rank {self.rank}: {exc}"
+        if self._any(bool(err)):
+            self.ctx.peer_disconnect()
+            self.dist.barrier(group=self.group)
+            self.ctx.peer_close()
+            raise PeerUnavailable(err or "a peer could not map the export arenas")
 
     def _any(self, flag: bool) -> bool:
         import torch

@@ -261,6 +261,72 @@ def test_gloo_peer_merge_protocol(oracle, tmp_path, world, gi, cap):
             assert reopens >= 1
 
 
+class _FailingPeerCtx(FakePeerCtx):
+    def __init__(self, *a, fail_rank=0, fail_at="connect", **k):
+        super().__init__(*a, **k)
+        self.fail_rank, self.fail_at = fail_rank, fail_at
+        self.closed = self.disconnected = 0
+
+    def peer_open(self, n, cap, rank, world):
+        if self.fail_at == "open" and rank == self.fail_rank:
+            raise RuntimeError("no CUDA IPC (test)")
+        return super().peer_open(n, cap, rank, world)
+
+    def peer_connect(self, handles):
+        if self.fail_at == "connect" and self.rank == self.fail_rank:
+            raise RuntimeError("cudaIpcOpenMemHandle failed (test)")
+        super().peer_connect(handles)
+
+    def peer_disconnect(self):
+        self.disconnected += 1
+
+    def peer_close(self):
+        self.closed += 1
+
+
+def _unavailable_worker(rank, world, port, spec, root, fail_at, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import oracle as O
+        from paper_1612_01178_b200.distributed import PeerMerge, PeerUnavailable
+        kind, n, e = spec
+        first, count = edge_range(e.shape[0], world, rank)
+        fc = _FailingPeerCtx(O, n, e[first:first + count], root, fail_rank=world - 1,
+                             fail_at=fail_at)
+        try:
+            PeerMerge(fc, n)
+            q.put((rank, "connected"))
+        except PeerUnavailable:
+            q.put((rank, f"unavailable closed={fc.closed}"))
+        dist.destroy_process_group()
+    except Exception as ex:  # surface errors to the parent
+        q.put((rank, repr(ex)))
+
+
+@pytest.mark.parametrize("world,fail_at", [(2, "open"), (3, "open"), (2, "connect"),
+                                           (3, "connect")])
+def test_gloo_peer_merge_unavailable_everywhere(oracle, tmp_path, world, fail_at):
+    """One rank cannot open or map the CUDA-IPC arenas: every rank raises
+    PeerUnavailable together (no rank is left blocked in a collective) and
+    releases what it opened, so bench.py can fall back to the NCCL merge."""
+    spec = _graphs()[0]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_unavailable_worker,
+                         args=(r, world, port, spec, str(tmp_path), fail_at, q))
+             for r in range(world)]
+    [p.start() for p in procs]
+    res = dict(q.get(timeout=180) for _ in range(world))
+    [p.join(timeout=60) for p in procs]
+    for rank in range(world):
+        msg = res[rank]
+        assert msg.startswith("unavailable"), (rank, msg)
+        failed_open = fail_at == "open" and rank == world - 1
+        assert msg.endswith("closed=0" if failed_open else "closed=1"), (rank, msg)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,cap", [(2, 0), (3, 0), (2, 16)])
 def test_gpu_ipc_merge_multiprocess(oracle, tmp_path, world, cap):
