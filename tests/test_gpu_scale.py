@@ -128,3 +128,87 @@ def test_labels_compare_device(ctx):
 def oracle_partition(lab):
     first = {}
     return [first.setdefault(int(x), i) for i, x in enumerate(lab)]
+
+
+def _sparse_huge_n(oracle, n, k_touch=50000, m=200000, seed=11):
+    """A few hundred thousand edges over a vertex set spread across [0, n),
+    including the top ids; expected labels from the oracle on the compressed
+    id space (order-preserving, so the minimum id maps back)."""
+    rng = np.random.default_rng(seed)
+    touch = np.unique(np.concatenate([
+        rng.integers(0, n, size=k_touch, dtype=np.int64),
+        np.array([0, 1, n - 1, n - 2, (n - 1) // 2, 1 << 31 if n > (1 << 31) else 3], np.int64)]))
+    idx = rng.integers(0, touch.size, size=(m, 2))
+    # chains along the sorted ids (long trees) plus random pairs
+    chain = np.stack([np.arange(touch.size - 1), np.arange(1, touch.size)], 1)[::3]
+    e_idx = np.concatenate([idx, chain[rng.permutation(chain.shape[0])]])
+    want_c = oracle.cc(touch.size, e_idx.astype(np.uint64))
+    want = touch[want_c.astype(np.int64)]
+    comps = n - touch.size + int(np.sum(want_c == np.arange(touch.size)))
+    return touch[e_idx].astype(np.uint32), touch, want, comps
+
+
+@pytest.mark.parametrize("algo", ["baseline-mj", "adaptive"])
+def test_huge_vertex_count_sparse(ctx, oracle, algo):
+    """n = 2^31 + 7 (an 8 GiB forest, 64-bit vertex offsets everywhere) with
+    250 K edges touching ids up to n - 1: the device check finds every edge
+    inside one star, the component count is exact, and the touched vertices
+    (plus untouched samples) carry the oracle's labels."""
+    n = (1 << 31) + 7
+    e, touch, want, comps = _sparse_huge_n(oracle, n)
+    g = ctx.graph_from_edges(e, n)
+    f = ctx.forest(n)
+    _, mx = ctx.cc(g, algo, forest=f, labels=False)
+    assert mx["components"] == comps
+    assert ctx.verify(g, f) == (0, 0)
+    rng = np.random.default_rng(3)
+    for i in rng.choice(touch.size, size=1500, replace=False).tolist() + [0, touch.size - 1]:
+        assert f.load(int(touch[i])) == int(want[i]), (algo, int(touch[i]))
+    for v in rng.integers(0, n, size=300).tolist():
+        j = np.searchsorted(touch, v)
+        if j < touch.size and touch[j] == v:
+            continue
+        assert f.load(int(v)) == v
+    f.close()
+    g.close()
+
+
+def test_huge_vertex_count_sparse_multi(capi, oracle):
+    """The same on a 2-shard context (both shards on device 0): two 8 GiB
+    forests, the merge gather over 67 M bitmap words."""
+    n = (1 << 31) + 7
+    e, touch, want, comps = _sparse_huge_n(oracle, n, seed=12)
+    mc = capi.Context(devices=[0, 0])
+    g = mc.graph_from_edges(e, n)
+    f = mc.forest(n)
+    _, mx = mc.cc(g, "baseline-mj", forest=f, labels=False)
+    assert mx["components"] == comps
+    rng = np.random.default_rng(4)
+    for i in rng.choice(touch.size, size=800, replace=False).tolist():
+        assert f.load(int(touch[i])) == int(want[i]), int(touch[i])
+    f.close()
+    g.close()
+    mc.close()
+
+
+@pytest.mark.parametrize("hub", ["low", "high", "both"])
+def test_hub_graphs_exact(ctx, oracle, hub):
+    """Worst-case contention: every edge touches one hub (vertex 0, vertex
+    n - 1, or alternately both), with duplicates and self-loops mixed in,
+    n = 2^22, m = 2^24; both engines and the 2-shard path, label-exact."""
+    n, m = 1 << 22, 1 << 24
+    rng = np.random.default_rng({"low": 1, "high": 2, "both": 3}[hub])
+    other = rng.integers(0, n, size=m, dtype=np.int64)
+    h = {"low": np.zeros(m, np.int64), "high": np.full(m, n - 1, np.int64),
+         "both": np.where(np.arange(m) % 2 == 0, 0, n - 1)}[hub]
+    e = np.stack([h, other], 1)
+    flip = rng.random(m) < 0.5
+    e[flip] = e[flip][:, ::-1]
+    e[rng.integers(0, m, size=m // 64)] = 7  # self-loops (7, 7)
+    e = e.astype(np.uint32)
+    want = oracle.cc(n, e)
+    g = ctx.graph_from_edges(e, n)
+    for algo in ("baseline-mj", "adaptive", "baseline"):
+        lab, mx = ctx.cc(g, algo)
+        assert np.array_equal(lab, want), (hub, algo)
+    g.close()
