@@ -192,7 +192,7 @@ def test_huge_vertex_count_sparse_multi(capi, oracle):
 
 
 @pytest.mark.parametrize("hub", ["low", "high", "both"])
-def test_hub_graphs_exact(ctx, oracle, hub):
+def test_hub_graphs_exact(ctx, capi, oracle, hub):
     """Worst-case contention: every edge touches one hub (vertex 0, vertex
     n - 1, or alternately both), with duplicates and self-loops mixed in,
     n = 2^22, m = 2^24; both engines and the 2-shard path, label-exact."""
@@ -212,3 +212,9 @@ def test_hub_graphs_exact(ctx, oracle, hub):
         lab, mx = ctx.cc(g, algo)
         assert np.array_equal(lab, want), (hub, algo)
     g.close()
+    mc = capi.Context(devices=[0, 0])
+    g2 = mc.graph_from_edges(e, n)
+    lab, _ = mc.cc(g2, "baseline-mj")
+    assert np.array_equal(lab, want), (hub, "2 shards")
+    g2.close()
+    mc.close()
