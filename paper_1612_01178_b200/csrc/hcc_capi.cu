@@ -331,6 +331,9 @@ struct Plan {
   u32 comp_pf = 0;
   // sixteen vertices per compress thread (k_compress_s0b16; HCC_COMP16)
   bool comp16 = false;
+  // middle topology slots on the two-sided streaming hook (k_hook_both;
+  // HCC_HOOK_BOTH=0: the one-sided k_hook)
+  bool hook_both = true;
 };
 
 HookArgs hook_args(hcc_ctx* c, const Plan& P, int mode, int append) {
@@ -618,6 +621,11 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
               HookArgs hd = ha;
               hd.gate = kGateAlways;
               launch_hook_sumd(c, P, q.s(), hd);
+            } else if (P.hook_both && !hp.cas && hp.chunked) {
+              // forming-side streaming slots: two-sided walks (768-thread
+              // CTAs for their registers) leave shallower trees for the
+              // compress (ER 1.876 -> 1.850 ms, grid -1%, RMAT unchanged)
+              k_hook_both<<<P.grid_cas, kHookCasCta, 0, q.s()>>>(hp);
             } else {
               launch_hook(P, q.s(), hp);
             }
@@ -1239,6 +1247,10 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   P.comp_pf = n >= (1ull << 26) ? (u32)c->sms * 6u : 0u;
   if (const char* e = std::getenv("HCC_COMP_PF")) P.comp_pf = (u32)std::atoi(e);
   P.comp16 = HCC_COMP16 != 0;
+  // (not when pi exceeds L2: RMAT-28's steady slot then ran 27.5 -> 28.7 ms
+  // after two-sided middle slots, 2-shard ranks 11.6 -> 12.1 ms)
+  P.hook_both = n < (1ull << 26);
+  if (const char* e = std::getenv("HCC_HOOK_BOTH")) P.hook_both = std::atoi(e) != 0;
   if (const char* e = std::getenv("HCC_COMP16")) P.comp16 = std::atoi(e) != 0;
   {
     const char* w = std::getenv("HCC_WALK");
@@ -1362,6 +1374,7 @@ int run_cc(hcc_ctx* c, const hcc_graph* g, const hcc_opts* o,
   key.plan = key.plan * 3 + (P.sumd_any ? 1 : 0);
   key.plan = key.plan * 1000003ull + P.comp_pf;
   key.plan = key.plan * 3 + (P.comp16 ? 1 : 0);
+  key.plan = key.plan * 3 + (P.hook_both ? 1 : 0);
   key.plan = key.plan * 1000003ull + P.sum_words * 64ull + P.sum_shift;
   key.plan = key.plan * 31 + (P.adapt ? 1000 + P.adapt_shift + 100000ull * P.forming_pct : 0);
   key.plan = key.plan * 1000003ull + P.adapt_first;

@@ -225,6 +225,7 @@ __global__ void k_hook_small(HookArgs a);
 __global__ void k_hook_sum(HookArgs a);
 __global__ void k_hook_legacy(HookArgs a);
 __global__ void k_hook_cas(HookArgs a);
+__global__ void k_hook_both(HookArgs a);
 __global__ void k_hook_sum_cas(HookArgs a);
 __global__ void k_hook_seg_cas(HookArgs a);
 __global__ void k_hook_sumd(HookArgs a);

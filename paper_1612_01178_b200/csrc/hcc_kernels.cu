@@ -809,7 +809,7 @@ __device__ __forceinline__ void emit(const HookArgs& a, WarpOut& w, uint2* wl_ou
 // size for the bitmap's hot words; e.g. RMAT, whose isolated vertices break
 // most words) every edge takes the bitmap / gather path directly.
 template <int EPT, bool SUM, bool CAS = false, bool APPEND = true, bool SUMD = false,
-          bool DYNOK = true, int FIXSH = -1>
+          bool DYNOK = true, int FIXSH = -1, bool BOTH = false>
 __device__ __forceinline__ void hook_stream(const HookArgs& a) {
   constexpr int S = kHookSlow;
   const uint2* src;
@@ -936,7 +936,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
     }
     if (!SUM) {
       u32 h[EPT], l[EPT];
-      const u32 act = resolve_edges<EPT, false, false, CAS>(a, links, tries, bits, s_sum, star, ed, h, l);
+      const u32 act = resolve_edges<EPT, false, BOTH, CAS>(a, links, tries, bits, s_sum, star, ed, h, l);
       emit<EPT, APPEND>(a, wo, wl_out, cnt_out, lane, act, h, l);
       continue;
     }
@@ -1004,6 +1004,13 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
 #ifndef HCC_HOOK_MINB
 #define HCC_HOOK_MINB (1024 / HCC_HOOK_CTA)
 #endif
+// Two-sided walks (k_hook_small's BOTH) in the streaming hook, at 768
+// threads for the registers they need: the middle topology slots (at 1024
+// threads the extra state spilled).
+__global__ void __launch_bounds__(kHookCasCta, 1) k_hook_both(HookArgs a) {
+  hook_stream<kHookEPT, false, false, true, false, true, -1, true>(a);
+}
+
 __global__ void __launch_bounds__(kHookCta, HCC_HOOK_MINB) k_hook(HookArgs a) {
   // (the summary path is k_hook_sum; s0f is ignored here)
   if (a.gate == kGateIfPlain && __ldg(&a.ctrl->use_sum)) return;

@@ -740,12 +740,13 @@ def test_steady_hook_variants(ctx, oracle, spec):
     sampled summary coverage (default; the worklist passes follow with
     k_hook_cas_sumd), the k_hook_sum / k_hook device vote (HCC_SUM_VOTE=1),
     the plain hook (HCC_SUMD=0), sumd in every streaming slot (HCC_SUMD=2),
-    plain worklist passes (HCC_WL_SUMD=0)."""
+    plain worklist passes (HCC_WL_SUMD=0), one-sided walks in the middle
+    slots (HCC_HOOK_BOTH=0)."""
     import os
     g = ctx.generate(spec)
     want = oracle.cc(g.n, g.edges())
     for env in ({}, {"HCC_SUM_VOTE": "1"}, {"HCC_SUMD": "0"}, {"HCC_SUMD": "2"},
-                {"HCC_SUMD": "1", "HCC_DYN": "0"}, {"HCC_WL_SUMD": "0"}):
+                {"HCC_SUMD": "1", "HCC_DYN": "0"}, {"HCC_WL_SUMD": "0"}, {"HCC_HOOK_BOTH": "0"}):
         os.environ.update(env)
         try:
             lab, _ = ctx.cc(g, "baseline-mj")
