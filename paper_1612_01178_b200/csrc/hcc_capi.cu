@@ -625,7 +625,7 @@ void enqueue_run(hcc_ctx* c, const Plan& P, Seq& q) {
               // forming-side streaming slots: two-sided walks (768-thread
               // CTAs for their registers) leave shallower trees for the
               // compress (ER 1.876 -> 1.850 ms, grid -1%, RMAT unchanged)
-              k_hook_both<<<P.grid_cas, kHookCasCta, 0, q.s()>>>(hp);
+              k_hook_both<<<(unsigned)c->sms, kHookBothCta, 0, q.s()>>>(hp);
             } else {
               launch_hook(P, q.s(), hp);
             }

@@ -50,6 +50,16 @@ constexpr int kHookSumCta = HCC_HOOK_SUM_CTA;  // k_hook_sum (one CTA per SM)
 #define HCC_HOOK_CAS_CTA 768
 #endif
 constexpr int kHookCasCta = HCC_HOOK_CAS_CTA;
+// Two-sided streaming hook (k_hook_both): CTA size and edges per thread
+// (768 / 4: ER 2^24/2^28 1.877 -> 1.836 ms, RMAT-24 1.353 -> 1.345 against
+// 768 / 8; 1024 / 8 spilled 160 B, 1024 / 4 measured no gain).
+#ifndef HCC_BOTH_CTA
+#define HCC_BOTH_CTA 768
+#endif
+#ifndef HCC_BOTH_EPT
+#define HCC_BOTH_EPT 4
+#endif
+constexpr int kHookBothCta = HCC_BOTH_CTA;
 // Summary-predicated streaming hook (k_hook_sumd).
 #ifndef HCC_HOOK_SUMD_CTA
 #define HCC_HOOK_SUMD_CTA 1024

@@ -1007,8 +1007,8 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
 // Two-sided walks (k_hook_small's BOTH) in the streaming hook, at 768
 // threads for the registers they need: the middle topology slots (at 1024
 // threads the extra state spilled).
-__global__ void __launch_bounds__(kHookCasCta, 1) k_hook_both(HookArgs a) {
-  hook_stream<kHookEPT, false, false, true, false, true, -1, true>(a);
+__global__ void __launch_bounds__(kHookBothCta, 1) k_hook_both(HookArgs a) {
+  hook_stream<HCC_BOTH_EPT, false, false, true, false, true, -1, true>(a);
 }
 
 __global__ void __launch_bounds__(kHookCta, HCC_HOOK_MINB) k_hook(HookArgs a) {
