@@ -1008,6 +1008,7 @@ __device__ __forceinline__ void hook_stream(const HookArgs& a) {
 // threads for the registers they need: the middle topology slots (at 1024
 // threads the extra state spilled).
 __global__ void __launch_bounds__(kHookBothCta, 1) k_hook_both(HookArgs a) {
+  if (a.gate == kGateIfPlain && __ldg(&a.ctrl->use_sum)) return;
   hook_stream<HCC_BOTH_EPT, false, false, true, false, true, -1, true>(a);
 }
 
