@@ -91,10 +91,13 @@ def main() -> None:
                         round(e[KEYS[10]], 1)])
     if workload != "rmat24":
         return
-    # the streaming topology hook's launches (k_hook / k_hook_sum that did
-    # work: a gated-out launch exits in a few microseconds), as the bench's
-    # roofline: k_hook_small (slot 0) and the worklist kernels are others
-    hooks = [e for e in rs if e["kernel"].split("::")[-1] in ("k_hook", "k_hook_sum", "k_hook_sumd")
+    # the streaming topology hook's launches (k_hook / k_hook_both /
+    # k_hook_sumd that did work: a gated-out launch exits in a few
+    # microseconds), as the bench's roofline (its records name all of them
+    # the streaming hook): k_hook_small (slot 0) and the worklist kernels are
+    # others
+    hooks = [e for e in rs if e["kernel"].split("::")[-1] in ("k_hook", "k_hook_both", "k_hook_sum",
+                                                             "k_hook_sumd")
              and e[KEYS[0]] > 20e-6]
     topo = hooks
     traffic = [e[KEYS[1]] + e[KEYS[2]] for e in topo]
